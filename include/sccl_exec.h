@@ -1,0 +1,119 @@
+/*
+ * sccl_exec.h -- C ABI of the B200 executor for SCCL-synthesized collectives.
+ *
+ * Drop-in boundary.  The operation it replaces is the
+ * reference's schedule.execute (`execute(s | (s1,s2), inst,
+ * payload_seed) -> per-node buffers`, entered through `cmd_exec`,
+ * SPEC.md:576-580); its input is the same canonical schedule file the CPU
+ * executor takes ("the contract any downstream lowering
+ * tool consumes").  Errors map the reference hierarchy
+ * (/root/reference/proj/include/sccl/error.hpp:9-30) to status codes.
+ * No C++ types, no CUDA types: streams are passed as void*.
+ *
+ * Threading: plans are immutable after creation and
+ * bind; at most one launch of a plan may be in flight per stream order;
+ * distinct plans may run concurrently.  sccl_last_error is thread-local.
+ */
+#ifndef SCCL_EXEC_H
+#define SCCL_EXEC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+enum {
+  SCCL_OK = 0,
+  SCCL_INVALID_ARGUMENT = 1, /* sccl::invalid_argument_error: schema, unverified schedule, bad rank/size */
+  SCCL_CUDA_ERROR = 4,       /* CUDA runtime failure                                                    */
+  SCCL_PEER_TIMEOUT = 5,     /* watchdog: a peer never signalled                                        */
+  SCCL_INTERNAL = 6
+};
+
+/* element types; redops */
+enum { SCCL_U8 = 0, SCCL_I32 = 1, SCCL_F32 = 2, SCCL_BF16 = 3, SCCL_F16 = 4 };
+enum { SCCL_SUM = 0 };
+
+typedef struct sccl_plan sccl_plan;
+
+typedef struct {
+  int device;         /* CUDA device ordinal; -1 = host-only plan (lowering, handle logic; no launch) */
+  int nchannels;      /* CTAs per rank; 0 = auto                                                      */
+  int tile_bytes;     /* bytes per pipelined tile (multiple of 16); 0 = auto                          */
+  int64_t timeout_ms; /* peer-wait watchdog; 0 = default (10 s), <0 = disabled                        */
+} sccl_plan_opts;
+
+void sccl_plan_opts_init(sccl_plan_opts* o);
+
+/* ---- schedule utilities (the L2 layer) -------------------
+ * Output strings use the two-call convention: *len is the buffer size on
+ * input, the required size (including the NUL) on output; out may be NULL. */
+
+/* verify / verify_combining every phase.  Returns SCCL_OK when the schedule
+ * is valid, SCCL_INVALID_ARGUMENT otherwise; report gets a JSON list of
+ * violations [[kind, step, chunk, src, dst], ...]. */
+int sccl_schedule_verify(const char* schedule_json, char* report, size_t* len);
+/* deserialize + canonical serialize */
+int sccl_schedule_canonicalize(const char* schedule_json, char* out, size_t* len);
+/* invert_schedule: allgather->reducescatter, broadcast->reduce */
+int sccl_schedule_invert(const char* schedule_json, char* out, size_t* len);
+/* Allreduce = (RS, AG) composition */
+int sccl_schedule_compose_allreduce(const char* rs_json, const char* ag_json, char* out, size_t* len);
+
+/* ---- plans ------------------------------------------------------------------ */
+
+/* One rank of a multi-process (one process per GPU) execution.  Parses,
+ * verifies (unverified schedules are rejected) and lowers the
+ * schedule; allocates the rank's registered receive buffer, scratch and
+ * flags.  bytes_per_rank follows NCCL conventions: allgather/gather = send
+ * bytes per rank, reducescatter/scatter = receive bytes per rank, others =
+ * the buffer size. */
+int sccl_plan_create(const char* schedule_json, int rank, int nranks, size_t bytes_per_rank, int dtype,
+                     int redop, const sccl_plan_opts* opts, sccl_plan** out);
+
+/* All ranks of the schedule on ONE GPU (loopback): every rank's buffers in
+ * the same device memory, one launch runs every rank's channel program. */
+int sccl_plan_create_loopback(const char* schedule_json, size_t bytes_per_rank, int dtype, int redop,
+                              const sccl_plan_opts* opts, sccl_plan** out);
+
+/* Out-of-band handle exchange (multi-process): export this rank's blob,
+ * gather every rank's blob (e.g. torch.distributed all_gather), bind. */
+int sccl_plan_export_handles(sccl_plan* plan, void* blob, size_t* len);
+int sccl_plan_bind_peers(sccl_plan* plan, const void* const* peer_blobs, size_t blob_len);
+
+/* The registered (peer-writable) receive buffer of a multi-process plan.
+ * Passing it as recvbuf to sccl_launch is zero-copy; any other recvbuf gets
+ * a trailing device-to-device copy. */
+int sccl_plan_recv_buffer(sccl_plan* plan, void** ptr, size_t* bytes);
+
+/* Asynchronous, stream-ordered launch (multi-process). */
+int sccl_launch(sccl_plan* plan, const void* sendbuf, void* recvbuf, void* stream);
+
+/* Loopback launch: sendbufs[r]/recvbufs[r] for r < P, all on the plan's device. */
+int sccl_launch_loopback(sccl_plan* plan, const void* const* sendbufs, void* const* recvbufs, void* stream);
+
+/* After the stream is synchronized: SCCL_PEER_TIMEOUT if the watchdog fired
+ * (details in sccl_last_error), else SCCL_OK. */
+int sccl_plan_check(sccl_plan* plan);
+
+/* Lowered program summary (JSON): ops per rank, channels, tile, scratch. */
+int sccl_plan_info(sccl_plan* plan, char* out, size_t* len);
+
+/* Kernel launches issued by this plan so far. */
+int64_t sccl_plan_launch_count(sccl_plan* plan);
+
+int sccl_plan_destroy(sccl_plan* plan);
+
+/* thread-local message of the last failing call */
+const char* sccl_last_error(void);
+
+/* library version string */
+const char* sccl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCCL_EXEC_H */

@@ -1,0 +1,55 @@
+// Device-side channel-program encoding shared by the host plan (plan.cpp)
+// and the sm_100a executor kernel (kernels/exec_kernel.cu).  Plain structs,
+// no CUDA types, so the host part compiles with g++ as well.
+#pragma once
+
+#include <cstdint>
+
+namespace sccl {
+
+constexpr int kMaxRanks = 16;   // pointer table width (kernel parameter space)
+constexpr int kMaxOpIn = 32;    // inputs of one copy/reduce op (staged in smem)
+constexpr int kMaxOpOut = 32;   // destinations of one op
+constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
+
+struct DevIn {
+  uint64_t off;   // byte offset of the chunk start in (rank, space)
+  uint64_t len;   // chunk length (used by WAIT ops; equal to op len otherwise)
+  int32_t flag;   // receipt slot at the executing rank, -1 = none
+  uint8_t rank, space, pad0, pad1;
+};
+
+struct DevOut {
+  uint64_t off;
+  int32_t flag;   // receipt slot at `rank` to signal, -1 = none
+  uint8_t rank, space, every_tile, pad;
+};
+
+struct DevOp {
+  uint64_t len;   // chunk length in bytes
+  uint32_t in_begin, out_begin;
+  uint16_t nin, nout;
+  uint8_t kind;   // 0 copy, 1 reduce, 2 wait
+  uint8_t vec;    // all offsets 16-byte aligned -> 16 B vector path
+  uint8_t pad0, pad1;
+};
+
+enum ErrCode : int { ERR_NONE = 0, ERR_TIMEOUT = 5 };
+
+struct KParams {
+  char* base[kMaxRanks][4];  // [rank][space]: SEND, RECV, SCRATCH, FLAGS
+  const DevOp* ops;
+  const DevIn* ins;
+  const DevOut* outs;
+  const uint32_t* prog;  // [P+1] op ranges per rank
+  uint64_t* epochs;      // [nranks_launch * nch] per-CTA launch counters
+  int* errinfo;          // host-mapped watchdog record
+  long long timeout_ns;
+  int P, nch, rank0, nranks_launch;
+  int tile;              // bytes per tile (multiple of 16)
+  int entry_base;        // index of the entry-handshake flags in FLAGS
+  int multiprocess;      // 1: peers are other processes (entry handshake)
+  int send_readonly;     // 1: SEND does not alias RECV (non-coherent loads ok)
+};
+
+}  // namespace sccl

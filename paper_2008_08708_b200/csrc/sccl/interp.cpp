@@ -1,0 +1,182 @@
+// TEST HOOK, not an execution path: a CPU interpreter of the lowered channel
+// program (one std::thread per (rank, channel), std::atomic counters for the
+// flags) used by the CPU test suite to check the LOWERING against the
+// oracle without a GPU (SURVEY.md section 4, T0 "lowering interpreter").
+// sccl_launch / sccl_launch_loopback never call it; the GPU path has no CPU
+// fallback.  Declared in include/sccl_debug.h.
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "../../../include/sccl_debug.h"
+#include "../../../include/sccl_exec.h"
+#include "error.hpp"
+#include "plan.hpp"
+
+namespace {
+
+thread_local std::string g_ierr;
+
+inline float bf16f(uint16_t h) {
+  uint32_t u = uint32_t(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+inline uint16_t f2bf16(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fff;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
+void elem_range(int dtype, const char* const* in, int nin, char* const* out, int nout, int64_t off, int64_t nbytes) {
+  const int es = dtype == 0 ? 1 : (dtype == 3 || dtype == 4) ? 2 : 4;
+  for (int64_t b = off; b < off + nbytes; b += es) {
+    char tmp[4];
+    if (nin == 1) {
+      std::memcpy(tmp, in[0] + b, es);
+    } else if (dtype == 0) {
+      uint8_t a = uint8_t(in[0][b]);
+      for (int k = 1; k < nin; ++k) a = uint8_t(a + uint8_t(in[k][b]));
+      tmp[0] = char(a);
+    } else if (dtype == 1) {
+      uint32_t a, x;
+      std::memcpy(&a, in[0] + b, 4);
+      for (int k = 1; k < nin; ++k) {
+        std::memcpy(&x, in[k] + b, 4);
+        a += x;
+      }
+      std::memcpy(tmp, &a, 4);
+    } else if (dtype == 2) {
+      float a, x;
+      std::memcpy(&a, in[0] + b, 4);
+      for (int k = 1; k < nin; ++k) {
+        std::memcpy(&x, in[k] + b, 4);
+        a = a + x;
+      }
+      std::memcpy(tmp, &a, 4);
+    } else if (dtype == 3) {
+      uint16_t h;
+      std::memcpy(&h, in[0] + b, 2);
+      float a = bf16f(h);
+      for (int k = 1; k < nin; ++k) {
+        std::memcpy(&h, in[k] + b, 2);
+        a = a + bf16f(h);
+      }
+      h = f2bf16(a);
+      std::memcpy(tmp, &h, 2);
+    } else {
+      _Float16 h;
+      std::memcpy(&h, in[0] + b, 2);
+      float a = float(h);
+      for (int k = 1; k < nin; ++k) {
+        std::memcpy(&h, in[k] + b, 2);
+        a = a + float(h);
+      }
+      h = _Float16(a);
+      std::memcpy(tmp, &h, 2);
+    }
+    for (int o = 0; o < nout; ++o) std::memcpy(out[o] + b, tmp, es);
+  }
+}
+
+}  // namespace
+
+extern "C" const char* sccl_debug_last_error(void) { return g_ierr.c_str(); }
+
+extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* sendbufs, void* const* recvbufs,
+                                             double timeout_s) {
+  using namespace sccl;
+  if (!p || !p->loopback) {
+    g_ierr = "needs a loopback plan";
+    return SCCL_INVALID_ARGUMENT;
+  }
+  const int P = p->nranks, nch = p->nch;
+  const int64_t tile = p->tile;
+  const size_t nflags = size_t(p->entry_base + P * nch);
+  std::vector<std::vector<std::atomic<uint64_t>>> flags(P);
+  std::vector<std::vector<char>> scratch(P);
+  for (int r = 0; r < P; ++r) {
+    flags[r] = std::vector<std::atomic<uint64_t>>(nflags);
+    for (auto& f : flags[r]) f.store(0);
+    scratch[r].assign(size_t(p->pg.scratch_bytes) + 16, 0);
+  }
+  auto base = [&](int rank, int space) -> char* {
+    if (space == SP_SEND) return const_cast<char*>(static_cast<const char*>(sendbufs[rank]));
+    if (space == SP_RECV) return static_cast<char*>(recvbufs[rank]);
+    return scratch[rank].data();
+  };
+  std::atomic<int> failed{0};
+  const uint64_t e = 1;
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
+  auto wait_ge = [&](std::atomic<uint64_t>& f, uint64_t target) -> uint64_t {
+    uint64_t v;
+    while ((v = f.load(std::memory_order_acquire)) < target) {
+      if (failed.load()) return target;
+      if (std::chrono::steady_clock::now() > deadline) {
+        failed.store(1);
+        return target;
+      }
+      std::this_thread::yield();
+    }
+    return v;
+  };
+
+  auto run = [&](int rank, int ch) {
+    for (uint32_t oi = p->prog[rank]; oi < p->prog[rank + 1]; ++oi) {
+      const DevOp& op = p->ops[oi];
+      if (op.kind == OP_WAIT) {
+        for (int i = 0; i < op.nin; ++i) {
+          const DevIn& in = p->ins[op.in_begin + i];
+          Part q = split16(int64_t(in.len), nch, ch);
+          uint64_t nt = uint64_t((q.len + tile - 1) / tile);
+          if (nt) wait_ge(flags[rank][size_t(in.flag) * nch + ch], e * nt);
+        }
+        continue;
+      }
+      Part q = split16(int64_t(op.len), nch, ch);
+      uint64_t ntiles = uint64_t((q.len + tile - 1) / tile);
+      std::vector<const char*> inp(op.nin);
+      std::vector<char*> outp(op.nout);
+      for (int i = 0; i < op.nin; ++i) {
+        const DevIn& in = p->ins[op.in_begin + i];
+        inp[i] = base(in.rank, in.space) + in.off;
+      }
+      for (int o = 0; o < op.nout; ++o) {
+        const DevOut& out = p->outs[op.out_begin + o];
+        outp[o] = base(out.rank, out.space) + out.off;
+      }
+      const uint64_t b0 = (e - 1) * ntiles;
+      for (uint64_t t = 0; t < ntiles; ++t) {
+        for (int i = 0; i < op.nin; ++i) {
+          const DevIn& in = p->ins[op.in_begin + i];
+          if (in.flag >= 0) wait_ge(flags[rank][size_t(in.flag) * nch + ch], b0 + t + 1);
+        }
+        if (failed.load()) return;
+        int64_t off = q.off + int64_t(t) * tile;
+        int64_t nb = std::min<int64_t>(tile, q.len - int64_t(t) * tile);
+        elem_range(op.kind == OP_COPY ? 0 : p->dtype, inp.data(), op.kind == OP_COPY ? 1 : op.nin, outp.data(),
+                   op.nout, off, nb);
+        bool last = t + 1 == ntiles;
+        for (int o = 0; o < op.nout; ++o) {
+          const DevOut& out = p->outs[op.out_begin + o];
+          if (out.flag >= 0 && (last || out.every_tile))
+            flags[out.rank][size_t(out.flag) * nch + ch].store(b0 + t + 1, std::memory_order_release);
+        }
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int r = 0; r < P; ++r)
+    for (int c = 0; c < nch; ++c) th.emplace_back(run, r, c);
+  for (auto& t : th) t.join();
+  if (failed.load()) {
+    g_ierr = "interpreter: a wait never completed (deadlock or missing signal)";
+    return SCCL_PEER_TIMEOUT;
+  }
+  return SCCL_OK;
+}

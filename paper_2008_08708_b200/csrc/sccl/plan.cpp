@@ -1,0 +1,510 @@
+// Plans and the C-ABI (include/sccl_exec.h).
+#include "plan.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <sstream>
+
+#include "../../../include/sccl_exec.h"
+#include "error.hpp"
+
+namespace sccl {
+cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st);
+cudaError_t exec_occupancy(int dtype, bool sys, int* blocks_per_sm);
+int exec_threads();
+}  // namespace sccl
+
+namespace {
+
+thread_local std::string g_err;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw sccl::cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SCCL_OK;
+  } catch (const sccl::invalid_argument_error& e) {
+    g_err = e.what();
+    return SCCL_INVALID_ARGUMENT;
+  } catch (const sccl::cuda_error& e) {
+    g_err = e.what();
+    return SCCL_CUDA_ERROR;
+  } catch (const sccl::timeout_error& e) {
+    g_err = e.what();
+    return SCCL_PEER_TIMEOUT;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SCCL_INTERNAL;
+  }
+}
+
+void put_string(const std::string& s, char* out, size_t* len) {
+  if (!len) throw sccl::invalid_argument_error("len must not be NULL");
+  size_t need = s.size() + 1;
+  if (out && *len >= need) std::memcpy(out, s.c_str(), need);
+  else if (out) {
+    *len = need;
+    throw sccl::invalid_argument_error("output buffer too small");
+  }
+  *len = need;
+}
+
+int esize_of(int dtype) {
+  switch (dtype) {
+    case SCCL_U8: return 1;
+    case SCCL_I32: return 4;
+    case SCCL_F32: return 4;
+    case SCCL_BF16: return 2;
+    case SCCL_F16: return 2;
+  }
+  throw sccl::invalid_argument_error("unknown dtype");
+}
+
+struct IpcBlob {
+  char magic[8];
+  char fingerprint[24];
+  int32_t rank, nranks, nch, tile;
+  uint64_t region_bytes;
+  cudaIpcMemHandle_t handle;
+};
+
+}  // namespace
+
+namespace sccl {
+
+void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks, int64_t bytes, int dtype,
+                     int redop, int device, int nch, int tile, int64_t timeout_ms, bool loopback) {
+  if (redop != SCCL_SUM) throw invalid_argument_error("only SCCL_SUM is supported");
+  const int es = esize_of(dtype);
+  p.sched = parse_schedule(json);
+  if (p.sched.P > kMaxRanks) throw invalid_argument_error("P exceeds the executor's 16-rank pointer table");
+  if (!loopback) {
+    if (nranks != p.sched.P) throw invalid_argument_error("nranks != schedule P");
+    if (rank < 0 || rank >= nranks) throw invalid_argument_error("rank out of range");
+  }
+  p.pg = lower(p.sched, bytes, es);
+  p.rank = loopback ? 0 : rank;
+  p.nranks = p.sched.P;
+  p.loopback = loopback;
+  p.dtype = dtype;
+  p.redop = redop;
+  p.device = device;
+  p.host_only = device < 0;
+  p.timeout_ns = timeout_ms < 0 ? 0 : (timeout_ms == 0 ? 10000LL : timeout_ms) * 1000000LL;
+
+  // channels: enough CTAs to cover the GPU in loopback, NVLink-sized in
+  // multi-process mode, and no channel below 32 KiB of the largest chunk
+  int64_t maxlen = 0;
+  for (auto& g : p.pg.geo) maxlen = std::max(maxlen, g.len);
+  if (nch <= 0) {
+    int cap = loopback ? std::max(1, p.nch /*preset: SMs*bps*/ / p.sched.P) : 32;
+    int64_t want = (maxlen + 32767) / 32768;
+    nch = int(std::max<int64_t>(1, std::min<int64_t>(cap, want)));
+  }
+  p.nch = nch;
+  if (tile <= 0) tile = 65536;
+  if (tile % 16) throw invalid_argument_error("tile_bytes must be a multiple of 16");
+  p.tile = tile;
+
+  // device encoding
+  const int P = p.sched.P;
+  p.ops.clear();
+  p.ins.clear();
+  p.outs.clear();
+  p.prog.assign(P + 1, 0);
+  for (int r = 0; r < P; ++r) {
+    p.prog[r] = uint32_t(p.ops.size());
+    for (const Op& op : p.pg.ranks[r].ops) {
+      if (op.kind != OP_WAIT && (op.ins.size() > size_t(kMaxOpIn) || op.outs.size() > size_t(kMaxOpOut)))
+        throw invalid_argument_error("op fan-in/fan-out exceeds executor limits (32)");
+      DevOp d{};
+      d.len = uint64_t(op.len);
+      d.kind = uint8_t(op.kind);
+      d.in_begin = uint32_t(p.ins.size());
+      d.out_begin = uint32_t(p.outs.size());
+      d.nin = uint16_t(op.ins.size());
+      d.nout = uint16_t(op.outs.size());
+      bool vec = true;
+      for (auto& in : op.ins) {
+        if (in.loc.rank != r) throw invalid_argument_error("internal: op reads remote memory");
+        DevIn x{};
+        x.off = uint64_t(in.loc.off);
+        x.len = uint64_t(in.len);
+        x.flag = in.flag;
+        x.rank = uint8_t(in.loc.rank);
+        x.space = uint8_t(in.loc.space);
+        vec &= in.loc.off % 16 == 0;
+        p.ins.push_back(x);
+      }
+      for (auto& o : op.outs) {
+        DevOut x{};
+        x.off = uint64_t(o.loc.off);
+        x.flag = o.flag;
+        x.rank = uint8_t(o.loc.rank);
+        x.space = uint8_t(o.loc.space);
+        x.every_tile = o.every_tile ? 1 : 0;
+        vec &= o.loc.off % 16 == 0;
+        p.outs.push_back(x);
+      }
+      d.vec = vec ? 1 : 0;
+      p.ops.push_back(d);
+    }
+  }
+  p.prog[P] = uint32_t(p.ops.size());
+
+  // memory layout of one rank's region
+  auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
+  p.entry_base = p.pg.max_slots * p.nch;
+  p.flags_bytes = up(sizeof(uint64_t) * size_t(p.entry_base + P * p.nch), 4096);
+  p.scratch_off = p.flags_bytes;
+  size_t scratch = up(size_t(p.pg.scratch_bytes), 4096);
+  p.recv_off = p.scratch_off + scratch;
+  p.region_bytes = p.recv_off + (loopback ? 0 : up(size_t(p.pg.recv_bytes), 4096));
+  p.region_bytes = up(p.region_bytes, 1 << 21);
+}
+
+}  // namespace sccl
+
+using namespace sccl;
+
+namespace {
+
+void plan_device_setup(sccl_plan& p) {
+  cuda_check(cudaSetDevice(p.device), "cudaSetDevice");
+  auto upload = [](auto& vec, auto** dptr) {
+    size_t n = std::max<size_t>(1, vec.size()) * sizeof(vec[0]);
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(dptr), n), "cudaMalloc(program)");
+    if (!vec.empty()) cuda_check(cudaMemcpy(*dptr, vec.data(), vec.size() * sizeof(vec[0]), cudaMemcpyHostToDevice), "upload");
+  };
+  upload(p.ops, &p.d_ops);
+  upload(p.ins, &p.d_ins);
+  upload(p.outs, &p.d_outs);
+  upload(p.prog, &p.d_prog);
+  int nlaunch = p.loopback ? p.nranks : 1;
+  size_t ne = size_t(nlaunch) * p.nch;
+  cuda_check(cudaMalloc(&p.d_epochs, ne * sizeof(uint64_t)), "cudaMalloc(epochs)");
+  cuda_check(cudaMemset(p.d_epochs, 0, ne * sizeof(uint64_t)), "memset(epochs)");
+  size_t total = p.region_bytes * size_t(nlaunch);
+  cuda_check(cudaMalloc(&p.d_region, total), "cudaMalloc(region)");
+  cuda_check(cudaMemset(p.d_region, 0, total), "memset(region)");
+  cuda_check(cudaHostAlloc(&p.h_err, 64 * sizeof(int), cudaHostAllocMapped), "cudaHostAlloc(err)");
+  std::memset(p.h_err, 0, 64 * sizeof(int));
+  cuda_check(cudaHostGetDevicePointer(&p.d_err, p.h_err, 0), "cudaHostGetDevicePointer");
+  cuda_check(cudaDeviceSynchronize(), "plan setup");
+  if (!p.loopback) {
+    p.peer_region.assign(p.nranks, nullptr);
+    p.peer_region[p.rank] = p.d_region;
+  }
+}
+
+int auto_channels_cap(int device, int dtype) {
+  // loopback: CTAs resident at once (all ranks' programs must be co-resident)
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  int bps = 0;
+  cuda_check(exec_occupancy(dtype, false, &bps), "occupancy");
+  return prop.multiProcessorCount * std::max(1, std::min(bps, 2));
+}
+
+void check_aligned(const void* p, const char* what) {
+  if (reinterpret_cast<uintptr_t>(p) % 16) throw invalid_argument_error(std::string(what) + " must be 16-byte aligned");
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return na && nb && x < y + nb && y < x + na;
+}
+
+void fill_common(const sccl_plan& p, KParams& k) {
+  std::memset(&k, 0, sizeof k);
+  k.ops = p.d_ops;
+  k.ins = p.d_ins;
+  k.outs = p.d_outs;
+  k.prog = p.d_prog;
+  k.epochs = p.d_epochs;
+  k.errinfo = p.d_err;
+  k.timeout_ns = p.timeout_ns;
+  k.P = p.nranks;
+  k.nch = p.nch;
+  k.tile = p.tile;
+  k.entry_base = p.entry_base;
+}
+
+}  // namespace
+
+extern "C" {
+
+void sccl_plan_opts_init(sccl_plan_opts* o) {
+  if (!o) return;
+  o->device = 0;
+  o->nchannels = 0;
+  o->tile_bytes = 0;
+  o->timeout_ms = 0;
+}
+
+const char* sccl_last_error(void) { return g_err.c_str(); }
+const char* sccl_version(void) { return "sccl-b200 1.0 (sm_100a)"; }
+
+int sccl_schedule_verify(const char* json, char* report, size_t* len) {
+  bool bad = false;
+  int rc = guarded([&] {
+    if (!json) throw invalid_argument_error("schedule_json is NULL");
+    Schedule s = parse_schedule(json);
+    auto v = verify(s);
+    std::ostringstream o;
+    o << "[";
+    for (size_t i = 0; i < v.size(); ++i)
+      o << (i ? "," : "") << "[" << v[i].kind << "," << v[i].step << "," << v[i].chunk << "," << v[i].src << ","
+        << v[i].dst << "]";
+    o << "]";
+    if (len) put_string(o.str(), report, len);
+    bad = !v.empty();
+    if (bad) g_err = "schedule has " + std::to_string(v.size()) + " violation(s): " + v[0].str();
+  });
+  return rc != SCCL_OK ? rc : (bad ? SCCL_INVALID_ARGUMENT : SCCL_OK);
+}
+
+int sccl_schedule_canonicalize(const char* json, char* out, size_t* len) {
+  return guarded([&] {
+    if (!json) throw invalid_argument_error("schedule_json is NULL");
+    put_string(serialize(parse_schedule(json)), out, len);
+  });
+}
+
+int sccl_schedule_invert(const char* json, char* out, size_t* len) {
+  return guarded([&] {
+    if (!json) throw invalid_argument_error("schedule_json is NULL");
+    put_string(serialize(invert_schedule(parse_schedule(json))), out, len);
+  });
+}
+
+int sccl_schedule_compose_allreduce(const char* rs, const char* ag, char* out, size_t* len) {
+  return guarded([&] {
+    if (!rs || !ag) throw invalid_argument_error("schedule_json is NULL");
+    put_string(serialize(compose_allreduce(parse_schedule(rs), parse_schedule(ag))), out, len);
+  });
+}
+
+static int create_common(const char* json, int rank, int nranks, size_t bytes, int dtype, int redop,
+                         const sccl_plan_opts* opts, sccl_plan** out, bool loopback) {
+  return guarded([&] {
+    if (!json || !out) throw invalid_argument_error("NULL argument");
+    *out = nullptr;
+    sccl_plan_opts o;
+    sccl_plan_opts_init(&o);
+    if (opts) o = *opts;
+    auto* p = new sccl_plan();
+    try {
+      int nch = o.nchannels;
+      if (loopback && nch <= 0) {
+        // cap derived from the device when there is one (nch preset = SMs*bps)
+        p->nch = (o.device >= 0) ? auto_channels_cap(o.device, dtype) : 296;
+      }
+      plan_build_host(*p, json, rank, nranks, int64_t(bytes), dtype, redop, o.device, nch, o.tile_bytes,
+                      o.timeout_ms, loopback);
+      if (loopback && o.device >= 0) {
+        int cap = auto_channels_cap(o.device, dtype);
+        if (p->nch * p->nranks > cap)
+          throw invalid_argument_error("loopback needs P*nchannels <= resident CTAs (" + std::to_string(cap) + ")");
+      }
+      if (!p->host_only) plan_device_setup(*p);
+    } catch (...) {
+      sccl_plan_destroy(p);
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int sccl_plan_create(const char* json, int rank, int nranks, size_t bytes, int dtype, int redop,
+                     const sccl_plan_opts* opts, sccl_plan** out) {
+  return create_common(json, rank, nranks, bytes, dtype, redop, opts, out, false);
+}
+
+int sccl_plan_create_loopback(const char* json, size_t bytes, int dtype, int redop, const sccl_plan_opts* opts,
+                              sccl_plan** out) {
+  return create_common(json, 0, 0, bytes, dtype, redop, opts, out, true);
+}
+
+int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
+  return guarded([&] {
+    if (!p || !len) throw invalid_argument_error("NULL argument");
+    if (p->loopback) throw invalid_argument_error("loopback plans have no peers");
+    if (!blob || *len < sizeof(IpcBlob)) {
+      *len = sizeof(IpcBlob);
+      if (blob) throw invalid_argument_error("blob buffer too small");
+      return;
+    }
+    IpcBlob b{};
+    std::memcpy(b.magic, "SCCLIPC1", 8);
+    std::strncpy(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1);
+    b.rank = p->rank;
+    b.nranks = p->nranks;
+    b.nch = p->nch;
+    b.tile = p->tile;
+    b.region_bytes = p->region_bytes;
+    if (!p->host_only) {
+      cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+      cuda_check(cudaIpcGetMemHandle(&b.handle, p->d_region), "cudaIpcGetMemHandle");
+    }
+    std::memcpy(blob, &b, sizeof b);
+    *len = sizeof b;
+  });
+}
+
+int sccl_plan_bind_peers(sccl_plan* p, const void* const* blobs, size_t blob_len) {
+  return guarded([&] {
+    if (!p || !blobs) throw invalid_argument_error("NULL argument");
+    if (p->loopback) throw invalid_argument_error("loopback plans have no peers");
+    if (p->bound) throw invalid_argument_error("plan already bound");
+    if (blob_len < sizeof(IpcBlob)) throw invalid_argument_error("blob too short");
+    std::vector<IpcBlob> bs(p->nranks);
+    for (int r = 0; r < p->nranks; ++r) {
+      if (!blobs[r]) throw invalid_argument_error("missing blob for rank " + std::to_string(r));
+      std::memcpy(&bs[r], blobs[r], sizeof(IpcBlob));
+      const IpcBlob& b = bs[r];
+      if (std::memcmp(b.magic, "SCCLIPC1", 8)) throw invalid_argument_error("bad blob magic from rank " + std::to_string(r));
+      if (b.rank != r || b.nranks != p->nranks)
+        throw invalid_argument_error("blob " + std::to_string(r) + " has rank/nranks mismatch");
+      if (std::strncmp(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1))
+        throw invalid_argument_error("rank " + std::to_string(r) + " lowered a different program (fingerprint mismatch)");
+      if (b.nch != p->nch || b.tile != p->tile || b.region_bytes != p->region_bytes)
+        throw invalid_argument_error("rank " + std::to_string(r) + " uses different channels/tile/region size");
+    }
+    if (!p->host_only) {
+      cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+      for (int r = 0; r < p->nranks; ++r) {
+        if (r == p->rank) continue;
+        void* ptr = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&ptr, bs[r].handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        p->peer_region[r] = static_cast<char*>(ptr);
+      }
+    }
+    p->bound = true;
+  });
+}
+
+int sccl_plan_recv_buffer(sccl_plan* p, void** ptr, size_t* bytes) {
+  return guarded([&] {
+    if (!p || !ptr) throw invalid_argument_error("NULL argument");
+    if (p->loopback || p->host_only) throw invalid_argument_error("no registered receive buffer");
+    *ptr = p->d_region + p->recv_off;
+    if (bytes) *bytes = size_t(p->pg.recv_bytes);
+  });
+}
+
+int sccl_launch(sccl_plan* p, const void* sendbuf, void* recvbuf, void* stream) {
+  return guarded([&] {
+    if (!p) throw invalid_argument_error("NULL plan");
+    if (p->loopback) throw invalid_argument_error("use sccl_launch_loopback for loopback plans");
+    if (p->host_only) throw invalid_argument_error("host-only plan cannot launch (no CUDA device)");
+    if (!p->bound) throw invalid_argument_error("plan not bound to peers (sccl_plan_bind_peers)");
+    if (p->pg.send_bytes && !sendbuf) throw invalid_argument_error("sendbuf is NULL");
+    check_aligned(sendbuf, "sendbuf");
+    char* reg = p->d_region + p->recv_off;
+    if (recvbuf) check_aligned(recvbuf, "recvbuf");
+    KParams k;
+    fill_common(*p, k);
+    for (int r = 0; r < p->nranks; ++r) {
+      char* reg_r = p->peer_region[r];
+      k.base[r][SP_SEND] = r == p->rank ? const_cast<char*>(static_cast<const char*>(sendbuf)) : nullptr;
+      k.base[r][SP_RECV] = reg_r + p->recv_off;
+      k.base[r][SP_SCRATCH] = reg_r + p->scratch_off;
+      k.base[r][SP_FLAGS] = reg_r;
+    }
+    k.rank0 = p->rank;
+    k.nranks_launch = 1;
+    k.multiprocess = 1;
+    k.send_readonly = !overlaps(sendbuf, size_t(p->pg.send_bytes), reg, size_t(p->pg.recv_bytes));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+    cuda_check(launch_exec(k, p->dtype, true, st), "launch");
+    p->launches++;
+    if (recvbuf && recvbuf != reg && p->pg.recv_bytes)
+      cuda_check(cudaMemcpyAsync(recvbuf, reg, size_t(p->pg.recv_bytes), cudaMemcpyDeviceToDevice, st),
+                 "copy-out of the registered receive buffer");
+  });
+}
+
+int sccl_launch_loopback(sccl_plan* p, const void* const* sendbufs, void* const* recvbufs, void* stream) {
+  return guarded([&] {
+    if (!p || !sendbufs || !recvbufs) throw invalid_argument_error("NULL argument");
+    if (!p->loopback) throw invalid_argument_error("not a loopback plan");
+    if (p->host_only) throw invalid_argument_error("host-only plan cannot launch (no CUDA device)");
+    KParams k;
+    fill_common(*p, k);
+    bool ro = true;
+    for (int r = 0; r < p->nranks; ++r) {
+      if (p->pg.send_bytes && !sendbufs[r]) throw invalid_argument_error("sendbuf is NULL");
+      if (p->pg.recv_bytes && !recvbufs[r]) throw invalid_argument_error("recvbuf is NULL");
+      check_aligned(sendbufs[r], "sendbuf");
+      check_aligned(recvbufs[r], "recvbuf");
+      char* reg = p->d_region + size_t(r) * p->region_bytes;
+      k.base[r][SP_SEND] = const_cast<char*>(static_cast<const char*>(sendbufs[r]));
+      k.base[r][SP_RECV] = static_cast<char*>(recvbufs[r]);
+      k.base[r][SP_SCRATCH] = reg + p->scratch_off;
+      k.base[r][SP_FLAGS] = reg;
+      for (int q = 0; q < p->nranks; ++q)
+        ro &= !overlaps(sendbufs[r], size_t(p->pg.send_bytes), recvbufs[q], size_t(p->pg.recv_bytes));
+    }
+    k.rank0 = 0;
+    k.nranks_launch = p->nranks;
+    k.multiprocess = 0;
+    k.send_readonly = ro ? 1 : 0;
+    cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+    cuda_check(launch_exec(k, p->dtype, false, static_cast<cudaStream_t>(stream)), "launch");
+    p->launches++;
+  });
+}
+
+int sccl_plan_check(sccl_plan* p) {
+  return guarded([&] {
+    if (!p) throw invalid_argument_error("NULL plan");
+    if (p->h_err && p->h_err[0] == ERR_TIMEOUT) {
+      volatile int* e = p->h_err;
+      throw timeout_error("peer timeout: rank " + std::to_string(e[1]) + " channel " + std::to_string(e[2]) +
+                          " op " + std::to_string(e[3]) + " slot " + std::to_string(e[4]) + " waited for " +
+                          std::to_string(e[5]) + ", saw " + std::to_string(e[6]));
+    }
+  });
+}
+
+int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
+  return guarded([&] {
+    if (!p) throw invalid_argument_error("NULL plan");
+    std::ostringstream o;
+    o << "{\"nchannels\":" << p->nch << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
+      << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
+      << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";
+    put_string(o.str(), out, len);
+  });
+}
+
+int64_t sccl_plan_launch_count(sccl_plan* p) { return p ? p->launches : -1; }
+
+int sccl_plan_destroy(sccl_plan* p) {
+  if (!p) return SCCL_OK;
+  if (!p->host_only && p->device >= 0) {
+    cudaSetDevice(p->device);
+    for (size_t r = 0; r < p->peer_region.size(); ++r)
+      if (int(r) != p->rank && p->peer_region[r]) cudaIpcCloseMemHandle(p->peer_region[r]);
+    cudaFree(p->d_ops);
+    cudaFree(p->d_ins);
+    cudaFree(p->d_outs);
+    cudaFree(p->d_prog);
+    cudaFree(p->d_epochs);
+    cudaFree(p->d_region);
+    if (p->h_err) cudaFreeHost(p->h_err);
+  }
+  delete p;
+  return SCCL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// Plan object behind the C-ABI: the lowered program, its device encoding,
+// the plan-owned memory (flags, scratch, registered receive buffer) and the
+// peer mappings.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "devprog.hpp"
+#include "lower.hpp"
+#include "schedule.hpp"
+
+struct sccl_plan {
+  sccl::Schedule sched;
+  sccl::Program pg;
+  int rank = 0, nranks = 0;
+  bool loopback = false, host_only = false;
+  int device = -1, dtype = 0, redop = 0;
+  int nch = 1, tile = 65536;
+  long long timeout_ns = 0;
+
+  // host copy of the device program (also used by the CPU interpreter)
+  std::vector<sccl::DevOp> ops;
+  std::vector<sccl::DevIn> ins;
+  std::vector<sccl::DevOut> outs;
+  std::vector<uint32_t> prog;  // [P+1]
+
+  // device program
+  sccl::DevOp* d_ops = nullptr;
+  sccl::DevIn* d_ins = nullptr;
+  sccl::DevOut* d_outs = nullptr;
+  uint32_t* d_prog = nullptr;
+  uint64_t* d_epochs = nullptr;
+
+  // plan memory: per rank region = [flags | scratch | recv (multi-process)]
+  char* d_region = nullptr;
+  size_t region_bytes = 0, flags_bytes = 0, scratch_off = 0, recv_off = 0;
+  int entry_base = 0;
+  std::vector<char*> peer_region;  // multi-process: every rank's region (own included)
+  bool bound = false;
+
+  int* h_err = nullptr;  // host-mapped watchdog record
+  int* d_err = nullptr;
+  int64_t launches = 0;
+  void* stream_hint = nullptr;
+};
+
+namespace sccl {
+
+// host-side construction (no CUDA calls)
+void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks, int64_t bytes, int dtype,
+                     int redop, int device, int nch, int tile, int64_t timeout_ms, bool loopback);
+
+}  // namespace sccl

@@ -1,0 +1,267 @@
+"""ctypes binding of libsccl_exec.so (the C-ABI in include/sccl_exec.h).
+
+This is the Python face of the drop-in boundary: the reference's
+``schedule.execute`` / ``cmd_exec`` become plan
+creation + launch on B200.  There is no CPU or eager fallback: if the
+extension is missing the import fails.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from typing import List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsccl_exec.so")
+
+OK, INVALID_ARGUMENT, CUDA_ERROR, PEER_TIMEOUT, INTERNAL = 0, 1, 4, 5, 6
+U8, I32, F32, BF16, F16 = 0, 1, 2, 3, 4
+SUM = 0
+DTYPES = {"u8": U8, "i32": I32, "f32": F32, "bf16": BF16, "f16": F16}
+ESIZE = {U8: 1, I32: 4, F32: 4, BF16: 2, F16: 2}
+
+
+class SCCLError(RuntimeError):
+    """Base error (maps sccl::error, /root/reference/proj/include/sccl/error.hpp:9)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[sccl status {code}] {msg}")
+        self.code = code
+
+
+class InvalidArgumentError(SCCLError, ValueError):
+    """sccl::invalid_argument_error (error.hpp:14-18)."""
+
+
+class PeerTimeoutError(SCCLError):
+    """Watchdog fired: a peer never signalled."""
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("nchannels", ctypes.c_int), ("tile_bytes", ctypes.c_int),
+                ("timeout_ms", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree extension; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libsccl_exec.so not built ({LIB_PATH}); run __graft_entry__.build() or make")
+        L = ctypes.CDLL(LIB_PATH)
+        c_p, c_sz = ctypes.c_void_p, ctypes.c_size_t
+        L.sccl_last_error.restype = ctypes.c_char_p
+        L.sccl_version.restype = ctypes.c_char_p
+        for name in ("sccl_schedule_verify", "sccl_schedule_canonicalize", "sccl_schedule_invert"):
+            getattr(L, name).argtypes = [ctypes.c_char_p, c_p, ctypes.POINTER(c_sz)]
+        L.sccl_schedule_compose_allreduce.argtypes = [ctypes.c_char_p, ctypes.c_char_p, c_p, ctypes.POINTER(c_sz)]
+        L.sccl_plan_create.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, c_sz, ctypes.c_int,
+                                       ctypes.c_int, ctypes.POINTER(_Opts), ctypes.POINTER(c_p)]
+        L.sccl_plan_create_loopback.argtypes = [ctypes.c_char_p, c_sz, ctypes.c_int, ctypes.c_int,
+                                                ctypes.POINTER(_Opts), ctypes.POINTER(c_p)]
+        L.sccl_plan_export_handles.argtypes = [c_p, c_p, ctypes.POINTER(c_sz)]
+        L.sccl_plan_bind_peers.argtypes = [c_p, ctypes.POINTER(c_p), c_sz]
+        L.sccl_plan_recv_buffer.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_sz)]
+        L.sccl_launch.argtypes = [c_p, c_p, c_p, c_p]
+        L.sccl_launch_loopback.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
+        L.sccl_plan_check.argtypes = [c_p]
+        L.sccl_plan_info.argtypes = [c_p, c_p, ctypes.POINTER(c_sz)]
+        L.sccl_plan_launch_count.argtypes = [c_p]
+        L.sccl_plan_launch_count.restype = ctypes.c_int64
+        L.sccl_plan_destroy.argtypes = [c_p]
+        L.sccl_debug_interpret_loopback.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p),
+                                                    ctypes.c_double]
+        L.sccl_debug_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _raise(code: int, msg: Optional[str] = None):
+    if code == OK:
+        return
+    msg = msg if msg is not None else lib().sccl_last_error().decode()
+    if code == INVALID_ARGUMENT:
+        raise InvalidArgumentError(code, msg)
+    if code == PEER_TIMEOUT:
+        raise PeerTimeoutError(code, msg)
+    raise SCCLError(code, msg)
+
+
+def _string_call(fn, *args) -> str:
+    n = ctypes.c_size_t(0)
+    rc = fn(*args, None, ctypes.byref(n))
+    if rc != OK:
+        _raise(rc)
+    buf = ctypes.create_string_buffer(n.value)
+    rc = fn(*args, buf, ctypes.byref(n))
+    _raise(rc)
+    return buf.value.decode()
+
+
+def _text(s) -> bytes:
+    if isinstance(s, dict):
+        s = json.dumps(s)
+    return s.encode() if isinstance(s, str) else s
+
+
+# ---------------------------------------------------------------- schedules
+def canonicalize(schedule) -> str:
+    """deserialize + canonical serialize."""
+    return _string_call(lib().sccl_schedule_canonicalize, _text(schedule))
+
+
+def verify(schedule) -> List[list]:
+    """Violations [[kind, step, chunk, src, dst], ...]; [] when valid
+    (SPEC.md:400-417).  Schema errors raise InvalidArgumentError."""
+    L = lib()
+    n = ctypes.c_size_t(1 << 20)
+    buf = ctypes.create_string_buffer(n.value)
+    rc = L.sccl_schedule_verify(_text(schedule), buf, ctypes.byref(n))
+    if rc == OK or (rc == INVALID_ARGUMENT and buf.value.startswith(b"[")):
+        return json.loads(buf.value.decode())
+    _raise(rc)
+    return []
+
+
+def invert(schedule) -> str:
+    """invert_schedule."""
+    return _string_call(lib().sccl_schedule_invert, _text(schedule))
+
+
+def compose_allreduce(rs, ag) -> str:
+    """Allreduce = (RS, AG)."""
+    return _string_call(lib().sccl_schedule_compose_allreduce, _text(rs), _text(ag))
+
+
+def version() -> str:
+    return lib().sccl_version().decode()
+
+
+# ---------------------------------------------------------------- plans
+def _opts(device: int, nchannels: int, tile_bytes: int, timeout_ms: int) -> _Opts:
+    return _Opts(device, nchannels, tile_bytes, timeout_ms)
+
+
+def _ptr(x) -> int:
+    """device pointer of a torch tensor (or an int)"""
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class _PlanBase:
+    def __init__(self):
+        self._h = ctypes.c_void_p(0)
+
+    def info(self) -> dict:
+        return json.loads(_string_call(lib().sccl_plan_info, self._h))
+
+    def check(self):
+        _raise(lib().sccl_plan_check(self._h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().sccl_plan_launch_count(self._h))
+
+    def close(self):
+        if self._h:
+            lib().sccl_plan_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LoopbackPlan(_PlanBase):
+    """Every rank of the schedule on one GPU; one launch runs them all."""
+
+    def __init__(self, schedule, bytes_per_rank: int, dtype: int = U8, device: int = 0,
+                 nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0):
+        super().__init__()
+        o = _opts(device, nchannels, tile_bytes, timeout_ms)
+        rc = lib().sccl_plan_create_loopback(_text(schedule), bytes_per_rank, dtype, SUM,
+                                             ctypes.byref(o), ctypes.byref(self._h))
+        _raise(rc)
+        meta = self.info()
+        self.nranks = meta["nranks"]
+        self.send_bytes = meta["program"]["send_bytes"]
+        self.recv_bytes = meta["program"]["recv_bytes"]
+
+    def launch(self, sendbufs: Sequence, recvbufs: Sequence, stream=None):
+        P = self.nranks
+        s = (ctypes.c_void_p * P)(*[_ptr(x) for x in sendbufs])
+        r = (ctypes.c_void_p * P)(*[_ptr(x) for x in recvbufs])
+        _raise(lib().sccl_launch_loopback(self._h, s, r, ctypes.c_void_p(_stream_ptr(stream))))
+
+    def interpret_on_cpu(self, sendbufs: Sequence, recvbufs: Sequence, timeout_s: float = 30.0):
+        """TEST HOOK (sccl_debug.h): run the lowered program on CPU threads
+        over host numpy buffers.  Not an execution path of the product."""
+        P = self.nranks
+        s = (ctypes.c_void_p * P)(*[b.ctypes.data for b in sendbufs])
+        r = (ctypes.c_void_p * P)(*[b.ctypes.data for b in recvbufs])
+        rc = lib().sccl_debug_interpret_loopback(self._h, s, r, ctypes.c_double(timeout_s))
+        if rc != OK:
+            _raise(rc, lib().sccl_debug_last_error().decode())
+
+
+class Plan(_PlanBase):
+    """One rank of a one-process-per-GPU execution (peers over CUDA IPC)."""
+
+    def __init__(self, schedule, rank: int, nranks: int, bytes_per_rank: int, dtype: int = U8,
+                 device: int = 0, nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0):
+        super().__init__()
+        o = _opts(device, nchannels, tile_bytes, timeout_ms)
+        rc = lib().sccl_plan_create(_text(schedule), rank, nranks, bytes_per_rank, dtype, SUM,
+                                    ctypes.byref(o), ctypes.byref(self._h))
+        _raise(rc)
+        self.rank, self.nranks = rank, nranks
+        meta = self.info()
+        self.send_bytes = meta["program"]["send_bytes"]
+        self.recv_bytes = meta["program"]["recv_bytes"]
+
+    def export_handles(self) -> bytes:
+        n = ctypes.c_size_t(0)
+        lib().sccl_plan_export_handles(self._h, None, ctypes.byref(n))
+        buf = ctypes.create_string_buffer(n.value)
+        _raise(lib().sccl_plan_export_handles(self._h, buf, ctypes.byref(n)))
+        return buf.raw[:n.value]
+
+    def bind_peers(self, blobs: Sequence[bytes]):
+        bufs = [ctypes.create_string_buffer(b, len(b)) for b in blobs]
+        arr = (ctypes.c_void_p * len(bufs))(*[ctypes.addressof(b) for b in bufs])
+        _raise(lib().sccl_plan_bind_peers(self._h, arr, len(blobs[0])))
+
+    def bind_with(self, group=None):
+        """Exchange handles through torch.distributed (all_gather_object)."""
+        import torch.distributed as dist
+        blobs: List[Optional[bytes]] = [None] * self.nranks
+        dist.all_gather_object(blobs, self.export_handles(), group=group)
+        self.bind_peers(blobs)
+
+    def recv_buffer(self):
+        p = ctypes.c_void_p(0)
+        n = ctypes.c_size_t(0)
+        _raise(lib().sccl_plan_recv_buffer(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    def launch(self, sendbuf, recvbuf=None, stream=None):
+        _raise(lib().sccl_launch(self._h, ctypes.c_void_p(_ptr(sendbuf)), ctypes.c_void_p(_ptr(recvbuf)),
+                                 ctypes.c_void_p(_stream_ptr(stream))))
