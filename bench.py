@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""Benchmark: collective bus GB/s of the B200 executor for SCCL-synthesized
+schedules (BASELINE.json metric), with the CPU reference executor beside it.
+
+N=1 (default): BASELINE config 2's allgather (C,S,R) = (7,7,7) on full(8),
+all 8 ranks in LOOPBACK on cuda:0 (one launch runs every rank's channel
+program; rank buffers live in the same HBM), 128 MiB per rank.
+N>1 (torchrun): one rank per GPU, peers' buffers mapped through CUDA IPC,
+schedule = (7,7,7) at N=8 else one-shot (1,1,1); NCCL all_gather timed on the
+same buffers for reference.
+
+value   = aggregate bus bytes / s = sum over ranks of (P-1)*m per launch / t
+e2e     = same metric through the public API with the inputs copied from
+          pinned host memory and every rank's output copied back, per step
+--impl reference: the CPU reference executor (oracle restatement of
+          SPEC.md:418-426, C + pthreads on all host cores) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "collective bus GB/s and latency vs buffer size at 2/4/8 B200 vs NCCL and CPU ref"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def schedule_for(P: int, name: str):
+    from paper_2008_08708_b200 import schedules as S
+    if name == "auto":
+        name = "777" if P == 8 else "oneshot"
+    if name == "777":
+        return S.to_json(S.hamiltonian_allgather(P)), f"allgather ({P-1},{P-1},{P-1}) hamiltonian, full:{P}"
+    if name == "oneshot":
+        return S.to_json(S.one_shot_allgather(P)), f"allgather (1,1,1) one-shot, full:{P}"
+    if name == "ring":
+        return S.to_json(S.ring_allgather(P)), f"allgather (1,{P-1},{P-1}) ring:{P}"
+    raise ValueError(name)
+
+
+def hbm_bytes_per_launch(plan) -> int:
+    """Algorithmic HBM bytes of one loopback launch: every lowered op reads
+    each input once and writes each output once."""
+    info = plan.info()["program"]
+    tot = 0
+    for rk in info["ranks"]:
+        for op in rk["ops"]:
+            if op["kind"] == "wait":
+                continue
+            tot += op["len"] * (len(op["ins"]) + len(op["outs"]))
+    return tot
+
+
+# --------------------------------------------------------------------------- CPU reference
+def cpu_reference_run(P: int, js: str, m: int, seconds: float, threads: int):
+    """Time the oracle executor loop (CPU restatement of SPEC.md:418-426) on
+    the same schedule; returns (aggregate bus GB/s, seconds, runs)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    d = json.loads(js)
+    ins = O.seeded_inputs(d["collective"], P, m, O.U8, 0)
+    ex = O.Execution(d, ins, m, O.U8, check=True)
+    ex.run(threads)  # warm-up
+    n, t0 = 0, time.perf_counter()
+    while True:
+        ex.run(threads)
+        n += 1
+        dt = time.perf_counter() - t0
+        if dt >= seconds:
+            break
+    return P * (P - 1) * m * n / dt / 1e9, dt, n
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    P = 8 if args.gpus == 1 else args.gpus
+    js, sname = schedule_for(P, args.schedule)
+    m = min(args.bytes, args.ref_bytes)
+    threads = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    d = json.loads(js)
+    ins = O.seeded_inputs(d["collective"], P, m, O.U8, 0)
+    ex = O.Execution(d, ins, m, O.U8, check=True)
+    for _ in range(args.warmup):
+        ex.run(threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ex.run(threads)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    val = P * (P - 1) * m * args.steps / tot / 1e9
+    sample = (f"oracle executor loop (SPEC.md:418-426 restated in C, {threads} threads) on {P} ranks x {m} B per "
+              f"rank of the same schedule ({sname}); bus bytes = P*(P-1)*m per step")
+    line = {"metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded PRNG bytes)",
+            "impl": "reference",
+            "config": {"workload": f"{sname}; CPU reference executor", "ranks": P, "bytes_per_rank": m,
+                       "parallelism": f"{threads} host threads"},
+            "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU, N = 1
+def run_loopback(args):
+    import torch
+    from paper_2008_08708_b200 import sccl
+    P = 8
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    js, sname = schedule_for(P, args.schedule)
+    m = args.bytes
+    plan = sccl.LoopbackPlan(js, m, sccl.U8, device=0, nchannels=args.nchannels, tile_bytes=args.tile)
+    info = plan.info()
+    send = [torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev) for _ in range(P)]
+    recv = [torch.empty(P * m, dtype=torch.uint8, device=dev) for _ in range(P)]
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            plan.launch(send, recv, stream)
+    stream.synchronize()
+    # correctness of what is timed: every rank holds the concatenation
+    want = torch.cat(send)
+    assert all(torch.equal(r, want) for r in recv), "bench: allgather result wrong"
+
+    n0 = plan.launch_count
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_all = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        t_all[0].record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            plan.launch(send, recv, stream)
+            ev[i][1].record(stream)
+        t_all[1].record(stream)
+        torch.cuda.synchronize()
+    launches = plan.launch_count - n0
+    plan.check()
+    total_ms = t_all[0].elapsed_time(t_all[1])
+    per = [a.elapsed_time(b) for a, b in ev]
+    ms = total_ms / args.steps
+    kern_ms = sum(per) / len(per)
+    bus = P * (P - 1) * m
+    value = bus / (ms * 1e-3) / 1e9
+    peaks, src = _peaks()
+    hbm = hbm_bytes_per_launch(plan)
+    achieved = hbm / (kern_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.schedule}:{m}")
+        except Exception:
+            traffic = None
+
+    # latency sweep (small/medium sizes) and the one-shot schedule at full size
+    sweep = []
+    if not args.no_sweep:
+        for sz in (1 << 10, 64 << 10, 1 << 20, 16 << 20):
+            p2 = sccl.LoopbackPlan(js, sz, sccl.U8, device=0)
+            s2 = [x[:sz] for x in send]
+            r2 = [x[:P * sz] for x in recv]
+            for _ in range(5):
+                p2.launch(s2, r2, stream)
+            stream.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            it = 50
+            a.record(stream)
+            for _ in range(it):
+                p2.launch(s2, r2, stream)
+            b.record(stream)
+            stream.synchronize()
+            us = a.elapsed_time(b) * 1e3 / it
+            sweep.append({"bytes_per_rank": sz, "us": round(us, 2),
+                          "busbw_per_rank_GBps": round((P - 1) * sz / (us * 1e-6) / 1e9, 2)})
+            p2.close()
+
+    # e2e: through the public API with host buffers (pinned) both ways
+    hsend = [torch.empty(m, dtype=torch.uint8, pin_memory=True) for _ in range(P)]
+    for h, s in zip(hsend, send):
+        h.copy_(s.cpu())
+    hrecv = [torch.empty(P * m, dtype=torch.uint8, pin_memory=True) for _ in range(P)]
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        for h, s in zip(hsend, send):
+            s.copy_(h, non_blocking=True)
+        plan.launch(send, recv, torch.cuda.current_stream())
+        for h, r in zip(hrecv, recv):
+            h.copy_(r, non_blocking=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cs = torch.cuda.current_stream()
+    a.record(cs)
+    for _ in range(e2e_steps):
+        for h, s in zip(hsend, send):
+            s.copy_(h, non_blocking=True)
+        plan.launch(send, recv, cs)
+        for h, r in zip(hrecv, recv):
+            h.copy_(r, non_blocking=True)
+    b.record(cs)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / e2e_steps
+    assert torch.equal(hrecv[3], want.cpu()), "e2e result wrong"
+    e2e_val = bus / (e2e_ms * 1e-3) / 1e9
+
+    # CPU baseline (oracle, 1 thread as the reference executor is specified)
+    cpu_m = min(m, args.cpu_bytes)
+    cpu_val, cpu_s, cpu_n = cpu_reference_run(P, js, cpu_m, args.cpu_seconds, 1)
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
+        "config": {"workload": f"{sname}; {P} ranks loopback on 1 B200 (all rank buffers in one HBM)",
+                   "ranks": P, "bytes_per_rank": m, "schedule": sname, "nchannels": info["nchannels"],
+                   "tile_bytes": info["tile_bytes"], "grid": info["grid"], "threads": info["threads"],
+                   "l2": f"no flush: inputs {P * m >> 20} MiB + outputs {P * P * m >> 20} MiB per step >> 126 MB L2",
+                   "parallelism": "loopback8"},
+        "busbw_per_rank_GBps": round((P - 1) * m / (ms * 1e-3) / 1e9, 2),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                     "peak_source": src, "algorithmic_bytes_per_launch": hbm,
+                     "kernel_ms": round(kern_ms, 4)},
+        "cpu_baseline": {"value": round(cpu_val, 3), "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": f"oracle executor, same schedule, {P} ranks x {cpu_m} B, {cpu_n} runs in "
+                                   f"{cpu_s:.1f} s, 1 thread (SPEC.md:447)"},
+        "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": P * m,
+                "d2h_bytes_per_step": P * P * m, "ms_per_step": round(e2e_ms, 3)},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "latency_sweep": sweep,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU, N > 1
+def run_multi(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2008_08708_b200 import sccl
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = world
+    js, sname = schedule_for(P, args.schedule)
+    m = args.bytes
+    plan = sccl.Plan(js, rank, P, m, sccl.U8, device=local, nchannels=args.nchannels, tile_bytes=args.tile)
+    plan.bind_with()
+    dev = torch.device("cuda", local)
+    send = torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev)
+    recv = torch.empty(P * m, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.launch(send, recv, stream)
+    torch.cuda.synchronize()
+    ref = torch.empty(P * m, dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(ref, send)
+    torch.cuda.synchronize()
+    assert torch.equal(ref, recv), f"rank {rank}: allgather differs from NCCL"
+    regptr, _ = plan.recv_buffer()
+
+    def timed(fn, steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    n0 = plan.launch_count
+    with ClockSampler(local) as clk:
+        ms = timed(lambda: plan.launch(send, regptr, stream), args.steps)
+    launches = plan.launch_count - n0
+    ms_nccl = timed(lambda: dist.all_gather_into_tensor(ref, send), args.steps)
+    plan.check()
+    bus = P * (P - 1) * m
+    value = bus / (ms * 1e-3) / 1e9
+    per_gpu = (P - 1) * m / (ms * 1e-3) / 1e9
+    # e2e through the public API with pinned host buffers
+    hs = torch.empty(m, dtype=torch.uint8, pin_memory=True)
+    hs.copy_(send.cpu())
+    hr = torch.empty(P * m, dtype=torch.uint8, pin_memory=True)
+
+    def e2e_step():
+        send.copy_(hs, non_blocking=True)
+        plan.launch(send, recv, stream)
+        hr.copy_(recv, non_blocking=True)
+    e2e_ms = timed(e2e_step, max(3, min(args.steps, 10)))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": P, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
+            "config": {"workload": f"{sname}; one rank per GPU, CUDA IPC peers over NVLink", "ranks": P,
+                       "bytes_per_rank": m, "parallelism": f"ranks{P}", "nchannels": plan.info()["nchannels"],
+                       "l2": "no flush: buffers >> L2"},
+            "busbw_per_rank_GBps": round(per_gpu, 2),
+            "nccl": {"ms": round(ms_nccl, 4), "busbw_per_rank_GBps": round((P - 1) * m / (ms_nccl * 1e-3) / 1e9, 2)},
+            "roofline": {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": 900.0, "unit": "GB/s",
+                         "frac": round(per_gpu / 900.0, 4), "traffic": None,
+                         "peak_source": "nominal NVLink 5 per direction per GPU"},
+            "e2e": {"value": round(bus / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": P * m,
+                    "d2h_bytes_per_step": P * P * m},
+            "clocks": clk.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bytes", type=int, default=128 << 20, help="per-rank allgather input")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "777", "oneshot", "ring"])
+    ap.add_argument("--nchannels", type=int, default=0)
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--ref-bytes", type=int, default=16 << 20)
+    ap.add_argument("--cpu-bytes", type=int, default=16 << 20)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-sweep", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.gpus == 1 and args.schedule == "auto":
+        args.schedule = "777"
+    if args.impl == "reference":
+        run_reference(args)
+    elif args.gpus == 1 and "WORLD_SIZE" not in os.environ or os.environ.get("WORLD_SIZE") == "1":
+        run_loopback(args)
+    else:
+        run_multi(args)
+
+
+if __name__ == "__main__":
+    main()

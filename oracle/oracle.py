@@ -332,6 +332,80 @@ def _run_phase(ph: dict, slots: List[np.ndarray], present: np.ndarray, off, ln, 
         raise ValueError("oracle_execute rejected its arguments")
 
 
+class Execution:
+    """One execution of a schedule (or composition) over the payload model
+    of SPEC.md:393-397: per-node chunk slots packed from the per-rank input
+    buffers by the Appendix C layout.  ``run`` is the timed executor loop
+    (the C restatement of SPEC.md:418-426); packing/unpacking is layout
+    plumbing around it."""
+
+    def __init__(self, sched: dict, inputs: Sequence[np.ndarray], nbytes: int, dtype: int = U8,
+                 check: bool = True):
+        if check:
+            v = verify(sched)
+            if v:
+                raise ValueError(f"unverified schedule rejected (SPEC.md:420): {v[:4]}")
+        self.sched = sched
+        self.kind = sched["collective"]
+        self.phases = _phases(sched)
+        self.P = P = sched["P"]
+        self.root = sched.get("root", 0) or 0
+        self.G = G = self.phases[-1]["G"]
+        self.dtype = dtype
+        self.nbytes = nbytes
+        C_geo = G // P if self.kind not in ("broadcast", "reduce") else G
+        self.geo = geo = chunk_geometry(self.kind, P, C_geo, nbytes, G)
+        self.ln = np.asarray([g[0] for g in geo], np.int64)
+        self.off = np.zeros(G, np.int64)
+        if G:
+            self.off[1:] = np.cumsum(self.ln)[:-1]
+        total = int(self.ln.sum())
+        self.slots = [np.zeros(max(total, 1), np.uint8) for _ in range(P)]
+        self.inputs = inputs
+        pre, _ = pre_post(self.phases[0]["collective"], self.phases[0]["G"], P, self.root)
+        self.pre = pre
+        self.combining_first = self.phases[0]["collective"] in COMBINING
+        self.present = np.zeros((P, G), np.uint8)
+        self.pack()
+
+    def pack(self):
+        for c in range(self.G):
+            L, io = int(self.ln[c]), self.geo[c][1]
+            o = int(self.off[c])
+            for n in range(self.P):
+                if self.pre[c, n]:
+                    self.slots[n][o:o + L] = self.inputs[n][io:io + L]
+        self.present[:] = self.pre.T
+
+    def run(self, nthreads: int = 1):
+        """The executor proper; re-packs first when the previous run reduced
+        into the slots (combining phases are not idempotent)."""
+        if getattr(self, "_dirty", False):
+            self.pack()
+        self.present[:] = self.pre.T
+        for k, ph in enumerate(self.phases):
+            if k > 0:  # composition: the next phase starts from its own pre
+                p2, _ = pre_post(ph["collective"], ph["G"], self.P, self.root)
+                self.present[:] = p2.T
+            _run_phase(ph, self.slots, self.present, self.off, self.ln, self.dtype, nthreads)
+        self._dirty = any(ph["collective"] in COMBINING for ph in self.phases)
+
+    def outputs(self, outputs: Optional[Sequence[np.ndarray]] = None) -> List[np.ndarray]:
+        _, rb = buffer_sizes(self.kind, self.P, self.nbytes)
+        if outputs is None:
+            outputs = [np.zeros(rb, np.uint8) for _ in range(self.P)]
+        last = self.phases[-1]
+        _, post = pre_post(last["collective"], last["G"], self.P, self.root)
+        for c in range(self.G):
+            L, oo, o = int(self.ln[c]), self.geo[c][2], int(self.off[c])
+            for n in range(self.P):
+                if post[c, n]:
+                    if not self.present[n, c]:
+                        raise ValueError(f"chunk {c} missing at node {n}")
+                    outputs[n][oo:oo + L] = self.slots[n][o:o + L]
+        return outputs
+
+
 def execute(sched: dict, inputs: Sequence[np.ndarray], nbytes: int, dtype: int = U8,
             nthreads: int = 1, check: bool = True,
             outputs: Optional[Sequence[np.ndarray]] = None) -> List[np.ndarray]:
@@ -339,54 +413,11 @@ def execute(sched: dict, inputs: Sequence[np.ndarray], nbytes: int, dtype: int =
     byte buffers laid out as the GPU executor lays them out (Appendix C).
     Output bytes no chunk covers keep their initial value (zero, or the
     ``outputs`` passed in)."""
-    if check:
-        v = verify(sched)
-        if v:
-            raise ValueError(f"unverified schedule rejected (SPEC.md:420): {v[:4]}")
-    kind = sched["collective"]
-    phases = _phases(sched)
-    P = sched["P"]
-    root = sched.get("root", 0) or 0
-    G = phases[-1]["G"]
-    C_geo = G // P if kind not in ("broadcast", "reduce") else G
-    if kind == "alltoall":
-        C_geo = G // P
-    geo = chunk_geometry(kind, P, C_geo, nbytes, G)
-    ln = np.asarray([g[0] for g in geo], np.int64)
-    off = np.zeros(G, np.int64)
-    if G:
-        off[1:] = np.cumsum(ln)[:-1]
-    total = int(ln.sum())
-    slots = [np.zeros(max(total, 1), np.uint8) for _ in range(P)]
-    sb, rb = buffer_sizes(kind, P, nbytes)
-    if outputs is None:
-        outputs = [np.zeros(rb, np.uint8) for _ in range(P)]
-    else:
+    ex = Execution(sched, inputs, nbytes, dtype, check)
+    ex.run(nthreads)
+    if outputs is not None:
         outputs = [np.array(o, dtype=np.uint8, copy=True) for o in outputs]
-
-    first = phases[0]
-    fkind = first["collective"]
-    pre, _ = pre_post(fkind, first["G"], P, root)
-    present = np.zeros((P, G), np.uint8)
-    for c in range(G):
-        for n in range(P):
-            if pre[c, n]:
-                present[n, c] = 1
-                slots[n][off[c]:off[c] + ln[c]] = inputs[n][geo[c][1]:geo[c][1] + ln[c]]
-    for k, ph in enumerate(phases):
-        if k > 0:  # composition: the next phase starts from its own pre
-            p2, _ = pre_post(ph["collective"], ph["G"], P, root)
-            present = np.ascontiguousarray(p2.T.copy())
-        _run_phase(ph, slots, present, off, ln, dtype, nthreads)
-    last = phases[-1]
-    _, post = pre_post(last["collective"], last["G"], P, root)
-    for c in range(G):
-        for n in range(P):
-            if post[c, n]:
-                if not present[n, c]:
-                    raise ValueError(f"chunk {c} missing at node {n}")
-                outputs[n][geo[c][2]:geo[c][2] + ln[c]] = slots[n][off[c]:off[c] + ln[c]]
-    return outputs
+    return ex.outputs(outputs)
 
 
 # --------------------------------------------------------------------------

@@ -1,0 +1,130 @@
+"""The C-ABI boundary: libsccl_exec.so loads, exports every symbol the
+headers declare, maps errors to the documented status codes, and the
+multi-process handle exchange works across processes (gloo, world 2)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2008_08708_b200 import sccl
+from paper_2008_08708_b200 import schedules as S
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(r"\b(sccl_[a-z_]+)\s*\(", text)) - {"sccl_plan_opts"})
+
+
+@pytest.mark.parametrize("header", ["sccl_exec.h", "sccl_debug.h"])
+def test_library_exports_declared_symbols(header):
+    names = _declared(header)
+    assert len(names) >= 2
+    out = subprocess.run(["nm", "-D", "--defined-only", sccl.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (sccl_\w+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    L = sccl.lib()
+    for n in names:
+        assert getattr(L, n) is not None
+
+
+def test_kernels_are_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", sccl.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_last_error():
+    assert "sm_100a" in sccl.version()
+    with pytest.raises(sccl.InvalidArgumentError) as e:
+        sccl.canonicalize('{"collective":"nope"}')
+    assert e.value.code == sccl.INVALID_ARGUMENT
+
+
+def test_host_only_plan_cannot_launch():
+    js = S.to_json(S.one_shot_allgather(4))
+    p = sccl.LoopbackPlan(js, 4096, sccl.U8, device=-1)
+    with pytest.raises(sccl.InvalidArgumentError, match="host-only"):
+        p.launch([0] * 4, [0] * 4, stream=0)
+    q = sccl.Plan(js, 1, 4, 4096, sccl.U8, device=-1)
+    with pytest.raises(sccl.InvalidArgumentError, match="host-only|not bound"):
+        q.launch(0, 0, stream=0)
+
+
+def test_bad_arguments():
+    js = S.to_json(S.one_shot_allgather(4))
+    with pytest.raises(sccl.InvalidArgumentError, match="nranks"):
+        sccl.Plan(js, 0, 8, 4096, sccl.U8, device=-1)
+    with pytest.raises(sccl.InvalidArgumentError, match="rank"):
+        sccl.Plan(js, 4, 4, 4096, sccl.U8, device=-1)
+    with pytest.raises(sccl.InvalidArgumentError, match="multiple of the element size"):
+        sccl.LoopbackPlan(S.allreduce_from(S.one_shot_allgather(4)), 4098, sccl.F32, device=-1)
+    with pytest.raises(sccl.InvalidArgumentError, match="tile"):
+        sccl.LoopbackPlan(js, 4096, sccl.U8, device=-1, tile_bytes=100)
+
+
+def test_blob_exchange_single_process():
+    js = S.to_json(S.hamiltonian_allgather(8))
+    plans = [sccl.Plan(js, r, 8, 1 << 16, sccl.U8, device=-1) for r in range(8)]
+    blobs = [p.export_handles() for p in plans]
+    for p in plans:
+        p.bind_peers(blobs)
+    with pytest.raises(sccl.InvalidArgumentError, match="already bound"):
+        plans[0].bind_peers(blobs)
+    other = sccl.Plan(js, 3, 8, 1 << 17, sccl.U8, device=-1)  # different size -> different program
+    fresh = sccl.Plan(js, 0, 8, 1 << 16, sccl.U8, device=-1)
+    bad = list(blobs)
+    bad[3] = other.export_handles()
+    with pytest.raises(sccl.InvalidArgumentError, match="fingerprint"):
+        fresh.bind_peers(bad)
+    bad = list(blobs)
+    bad[2], bad[4] = bad[4], bad[2]
+    with pytest.raises(sccl.InvalidArgumentError, match="rank"):
+        fresh.bind_peers(bad)
+
+
+_WORKER = r"""
+import os, sys
+sys.path.insert(0, {root!r})
+import torch.distributed as dist
+from paper_2008_08708_b200 import sccl, schedules as S
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=int(sys.argv[1]), world_size=2)
+r = dist.get_rank()
+js = S.to_json(S.one_shot_allgather(2))
+nbytes = 4096 if (r == 0 or sys.argv[2] == "same") else 8192
+p = sccl.Plan(js, r, 2, nbytes, sccl.U8, device=-1)
+try:
+    p.bind_with()
+    print("BOUND", r, p.info()["program"]["fingerprint"], flush=True)
+except sccl.InvalidArgumentError as e:
+    print("MISMATCH", r, str(e)[:60], flush=True)
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("mode", ["same", "differ"])
+def test_gloo_two_process_handle_exchange(tmp_path, mode):
+    """world_size-2 gloo: each rank lowers the schedule, exchanges its blob
+    through torch.distributed and binds; mismatched programs are refused."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = tmp_path / "w.py"
+    script.write_text(_WORKER.format(root=ROOT, port=port))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    procs = [subprocess.Popen(["python", str(script), str(r), mode], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                              text=True, env=env) for r in range(2)]
+    outs = [p.communicate(timeout=120) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e
+    text = "".join(o for o, _ in outs)
+    if mode == "same":
+        assert text.count("BOUND") == 2
+        fps = {line.split()[2] for line in text.splitlines() if line.startswith("BOUND")}
+        assert len(fps) == 1
+    else:
+        assert text.count("MISMATCH") == 2

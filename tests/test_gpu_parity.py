@@ -1,0 +1,207 @@
+"""GPU parity: the sm_100a executor (through the C-ABI) against the CPU oracle.
+
+Bit-exact for every collective and element type: copies are bitwise, and
+reductions follow the fixed order the oracle defines (DESIGN.md "Reduction
+order"); no tolerance is needed or used.  Loopback mode runs every rank of
+the schedule on cuda:0 (one launch, P x nchannels CTAs).
+"""
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle as O  # noqa: E402
+from paper_2008_08708_b200 import sccl  # noqa: E402
+from paper_2008_08708_b200 import schedules as S  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def _schedules():
+    ag8 = S.hamiltonian_allgather(8)
+    return {
+        "ag_b1_recdbl": S.to_json(S.recursive_doubling_ring4()),
+        "ag_b2_ring4": S.to_json(S.ring4_s2r2()),
+        "ag_b3_dgx1": S.to_json(S.dgx1_allgather_122()),
+        "ag_b4_oneshot8": S.to_json(S.one_shot_allgather(8)),
+        "ag_b7_ring8": S.to_json(S.ring_allgather(8)),
+        "ag_b8_bidir8": S.to_json(S.bidir_ring_allgather(8)),
+        "ag_777": S.to_json(ag8),
+        "a2a_b5": S.to_json(S.direct_alltoall(8)),
+        "a2a_k2": S.to_json(S.direct_alltoall(4, 8)),
+        "bcast": S.to_json(S.one_shot_broadcast(4, 3, 1)),
+        "bcast_chain": S.to_json(S.pipelined_chain_broadcast(5, 4, 2)),
+        "gather": S.to_json(S.direct_gather(4, 2)),
+        "scatter": S.to_json(S.direct_scatter(4, 1)),
+        "rs_oneshot8": S.reducescatter_from(S.one_shot_allgather(8)),
+        "rs_ring8": S.reducescatter_from(S.ring_allgather(8)),
+        "reduce_chain": S.reduce_from(S.pipelined_chain_broadcast(5, 4, 2)),
+        "ar_822": S.allreduce_from(S.one_shot_allgather(8)),
+        "ar_ring": S.allreduce_from(S.ring_allgather(8)),
+        "ar_56_14_14": S.allreduce_from(ag8),
+        "ar_dgx1": S.allreduce_from(S.dgx1_allgather_122()),
+        "ar_recdbl": S.allreduce_from(S.recursive_doubling_ring4()),
+    }
+
+
+SCHED = _schedules()
+
+
+def run_gpu(js, nbytes, dtype, seed=3, mode="random", nch=0, tile=0, repeats=1):
+    d = json.loads(js)
+    kind, P = d["collective"], d["P"]
+    plan = sccl.LoopbackPlan(js, nbytes, dtype, device=0, nchannels=nch, tile_bytes=tile)
+    try:
+        for it in range(repeats):
+            ins = O.seeded_inputs(kind, P, nbytes, dtype, seed + it, mode)
+            ref = O.execute(d, ins, nbytes, dtype)
+            send = [torch.from_numpy(x).to(DEV) for x in ins]
+            recv = [torch.full((max(r.size, 1),), 0xEE, dtype=torch.uint8, device=DEV) for r in ref]
+            plan.launch(send, recv)
+            torch.cuda.synchronize()
+            plan.check()
+            for r, (a, b) in enumerate(zip(recv, ref)):
+                got = a.cpu().numpy()[:b.size]
+                if kind in ("gather", "reduce", "scatter", "reducescatter", "alltoall", "broadcast", "allgather",
+                            "allreduce"):
+                    mask = _covered(d, nbytes, r, b.size)
+                    got = np.where(mask, got, 0)
+                assert np.array_equal(got, b), f"{kind} rank {r} iter {it} differs"
+    finally:
+        plan.close()
+
+
+def _covered(d, nbytes, rank, size):
+    """bytes of rank's output that the collective defines (rooted
+    collectives leave non-root outputs untouched)."""
+    kind = d["collective"]
+    P = d["P"]
+    phases = d["phases"] if "phases" in d else [d]
+    G = phases[-1]["G"]
+    _, post = O.pre_post(phases[-1]["collective"], G, P, d.get("root", 0) or 0)
+    C = G // P if kind not in ("broadcast", "reduce") else G
+    geo = O.chunk_geometry(kind, P, C, nbytes, G)
+    m = np.zeros(size, bool)
+    for c in range(G):
+        if post[c, rank]:
+            m[geo[c][2]:geo[c][2] + geo[c][0]] = True
+    return m
+
+
+@pytest.mark.parametrize("name", sorted(SCHED))
+@pytest.mark.parametrize("nbytes", [0, 16, 1040, 65536 + 32, 1 << 20])
+def test_parity_u8_and_float(name, nbytes):
+    js = SCHED[name]
+    kind = json.loads(js)["collective"]
+    dts = [O.U8] if kind not in ("reduce", "reducescatter", "allreduce") else [O.I32, O.F32, O.BF16, O.F16, O.U8]
+    for dt in dts:
+        if nbytes % O.ESIZE[dt]:
+            continue
+        if kind == "alltoall" and nbytes % (json.loads(js)["P"] * O.ESIZE[dt]):
+            continue
+        run_gpu(js, nbytes, dt)
+
+
+@pytest.mark.parametrize("nch,tile", [(1, 256), (3, 4096), (7, 65536), (0, 0)])
+@pytest.mark.parametrize("name", ["ag_777", "ag_b7_ring8", "ar_56_14_14", "ar_ring", "rs_ring8", "a2a_b5"])
+def test_channels_and_tiles(name, nch, tile):
+    js = SCHED[name]
+    kind = json.loads(js)["collective"]
+    dt = O.BF16 if kind in ("allreduce", "reducescatter") else O.U8
+    run_gpu(js, 3 * 65536 + 1024, dt, nch=nch, tile=tile)
+
+
+def test_back_to_back_launches_advance_epochs():
+    run_gpu(SCHED["ar_56_14_14"], 1 << 18, O.F32, repeats=5)
+    run_gpu(SCHED["ag_777"], 1 << 18, O.U8, repeats=5, tile=4096)
+
+
+def test_inplace_allreduce():
+    js = SCHED["ar_56_14_14"]
+    d = json.loads(js)
+    nbytes = 1 << 20
+    ins = O.seeded_inputs("allreduce", 8, nbytes, O.F32, 5)
+    ref = O.execute(d, ins, nbytes, O.F32)
+    plan = sccl.LoopbackPlan(js, nbytes, O.F32, device=0)
+    bufs = [torch.from_numpy(x).to(DEV) for x in ins]
+    plan.launch(bufs, bufs)
+    torch.cuda.synchronize()
+    for a, b in zip(bufs, ref):
+        assert np.array_equal(a.cpu().numpy(), b)
+
+
+def test_cuda_graph_replay():
+    js = SCHED["ar_822"]
+    d = json.loads(js)
+    nbytes = 1 << 16
+    plan = sccl.LoopbackPlan(js, nbytes, O.BF16, device=0)
+    send = [torch.zeros(nbytes, dtype=torch.uint8, device=DEV) for _ in range(8)]
+    recv = [torch.zeros(nbytes, dtype=torch.uint8, device=DEV) for _ in range(8)]
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.launch(send, recv, stream=s)
+    for it in range(3):
+        ins = O.seeded_inputs("allreduce", 8, nbytes, O.BF16, 100 + it)
+        for t, x in zip(send, ins):
+            t.copy_(torch.from_numpy(x))
+        g.replay()
+        torch.cuda.synchronize()
+        ref = O.execute(d, ins, nbytes, O.BF16)
+        for a, b in zip(recv, ref):
+            assert np.array_equal(a.cpu().numpy(), b), f"graph replay {it}"
+
+
+@pytest.mark.parametrize("name", ["ag_777", "ag_b4_oneshot8"])
+def test_allgather_large_property(name):
+    """64 MiB per rank: output of every rank == concatenation of the inputs."""
+    js = SCHED[name]
+    m = 64 << 20
+    plan = sccl.LoopbackPlan(js, m, O.U8, device=0)
+    g = torch.Generator(device=DEV)
+    g.manual_seed(0)
+    send = [torch.randint(0, 256, (m,), dtype=torch.uint8, device=DEV, generator=g) for _ in range(8)]
+    recv = [torch.empty(8 * m, dtype=torch.uint8, device=DEV) for _ in range(8)]
+    plan.launch(send, recv)
+    torch.cuda.synchronize()
+    want = torch.cat(send)
+    for r in recv:
+        assert torch.equal(r, want)
+
+
+@pytest.mark.parametrize("dt", [O.F32, O.BF16, O.I32])
+def test_allreduce_large_exact_sum(dt):
+    """64 MiB: integer-valued inputs in [-16,16] make the sum exact in any
+    order, so every rank must equal the torch sum bit for bit."""
+    js = SCHED["ar_56_14_14"]
+    M = 64 << 20
+    tdt = {O.F32: torch.float32, O.BF16: torch.bfloat16, O.I32: torch.int32}[dt]
+    plan = sccl.LoopbackPlan(js, M, dt, device=0)
+    g = torch.Generator(device=DEV)
+    g.manual_seed(1)
+    n = M // O.ESIZE[dt]
+    xs = [torch.randint(-16, 17, (n,), device=DEV, generator=g).to(tdt) for _ in range(8)]
+    send = [x.view(torch.uint8) for x in xs]
+    recv = [torch.empty(M, dtype=torch.uint8, device=DEV) for _ in range(8)]
+    plan.launch(send, recv)
+    torch.cuda.synchronize()
+    want = torch.stack([x.to(torch.float64) for x in xs]).sum(0).to(tdt).view(torch.uint8)
+    for r in recv:
+        assert torch.equal(r, want)
+
+
+def test_allreduce_bf16_bitexact_16MiB():
+    js = SCHED["ar_56_14_14"]
+    run_gpu(js, 16 << 20, O.BF16, seed=9)
+
+
+def test_unverified_schedule_rejected_on_gpu():
+    d = json.loads(SCHED["ag_b4_oneshot8"])
+    d["sends"] = d["sends"][1:]
+    with pytest.raises(sccl.InvalidArgumentError):
+        sccl.LoopbackPlan(d, 4096, O.U8, device=0)
