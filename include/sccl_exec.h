@@ -41,8 +41,9 @@ typedef struct sccl_plan sccl_plan;
 
 typedef struct {
   int device;         /* CUDA device ordinal; -1 = host-only plan (lowering, handle logic; no launch) */
-  int nchannels;      /* CTAs per rank; 0 = auto                                                      */
-  int tile_bytes;     /* bytes per pipelined tile (multiple of 16); 0 = auto                          */
+  int nchannels;      /* byte parts per chunk (CTAs per rank per chunk group); 0 = auto              */
+  int chunk_groups;   /* chunk groups (independent chunks run on different CTAs); 0 = auto          */
+  int tile_bytes;     /* pipeline stage / copy tile bytes, multiple of 16 in [256, 32768]; 0 = auto  */
   int64_t timeout_ms; /* peer-wait watchdog; 0 = default (10 s), <0 = disabled                        */
 } sccl_plan_opts;
 

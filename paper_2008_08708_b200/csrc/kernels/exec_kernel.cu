@@ -4,23 +4,29 @@
 // S steps of a schedule in one launch, chunks pushed straight into the
 // destination rank's memory, a dedicated flag per (chunk, connection) set
 // after a system-scope fence, receivers spinning on the flag before they
-// forward or reduce.  Here:
-//   * one CTA per (rank, channel); a channel is a contiguous 16 B-aligned
-//     sub-range of every chunk, so a CTA runs its rank's whole op list on
-//     its sub-range and program order covers all intra-rank dependencies;
-//   * flags are per (receipt slot, channel) 64-bit counters that count tiles
-//     across launches (value (epoch-1)*ntiles + t + 1 after tile t), so a
-//     consumer can start forwarding tile t while later tiles are in flight
-//     and nothing is ever reset;
-//   * data moves as 16 B vectors, loads batched ahead of stores; the
-//     reduction of combining receipts is fused into the receive and
-//     into the forward of the result (one pass over the inputs, results
-//     stored to every destination);
-//   * loopback mode (every rank of the schedule on this GPU: one launch of
-//     P*nch CTAs) uses gpu-scope release/acquire; multi-process mode (one
-//     rank per GPU, peers' buffers mapped through CUDA IPC over NVLink)
-//     uses system scope and an entry handshake per (peer, channel) so a
-//     rank never writes into a peer that has not yet entered the launch.
+// forward or reduce.  B200 form:
+//
+//  * one CTA per (rank, channel).  A channel is a contiguous 16 B-aligned
+//    sub-range of every chunk; the CTA runs its rank's whole op list on that
+//    sub-range, so program order replaces intra-rank synchronisation and
+//    only cross-rank receipts carry flags;
+//  * warp-specialised TMA pipeline over a ring of NSTAGE shared-memory
+//    stages (mbarrier full / ready / empty per stage):
+//      warp 0  producer  waits the receipt counters a tile needs, then
+//                        cp.async.bulk global->smem for every input;
+//      warps 2+ compute  REDUCE ops: in-place f32-accumulate of the nin
+//                        input tiles in smem (fixed order, one rounding);
+//      warp 1  storer    cp.async.bulk smem->global to every destination
+//                        (local output and/or peer HBM), bulk groups
+//                        retired with a lag, then fence + counter release;
+//  * flags count BYTES of a (receipt, channel) sub-range that have landed:
+//    (epoch-1)*len + bytes_done.  Producer and consumer may tile the same
+//    chunk differently (copy tiles are a whole stage, reduce tiles a stage
+//    divided by fan-in); counters are never reset and each CTA keeps its own
+//    epoch in device memory (graph capture safe);
+//  * loopback (every rank on this GPU, one launch) uses gpu scope;
+//    multi-process (one rank per GPU, peers mapped through CUDA IPC over
+//    NVLink) uses sys scope plus an entry handshake per (peer, channel).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -31,8 +37,17 @@
 namespace sccl {
 namespace {
 
-constexpr int NT = 512;  // threads per CTA
-constexpr int U = 4;     // 16 B vectors in flight per thread per input
+constexpr int NCW = 8;               // compute warps
+constexpr int NT = kThreads;         // producer, storer, signaler + NCW compute warps
+static_assert(NT == (3 + NCW) * 32, "thread layout");
+constexpr int CW0 = 3;               // first compute warp
+constexpr int NPART = NT - 32;       // threads of the unaligned path (all but the signaler)
+constexpr int SIGQ = 64;             // storer -> signaler queue entries
+constexpr int NSTAGE = kStages;      // stage size = KParams::tile (runtime)
+constexpr int FIFO = 8;              // storer's in-flight tile records (> max sig_lag)
+constexpr uint64_t kStorerPatienceNs = 3000;  // storer spins this long before draining
+constexpr size_t SMEM_HDR = 2048;    // mbarriers, signal queue, control words, ahead of the stages
+__host__ __device__ constexpr size_t smem_bytes(int tile) { return SMEM_HDR + size_t(NSTAGE) * tile; }
 
 struct DPart {
   int64_t off, len;
@@ -44,7 +59,50 @@ __device__ __forceinline__ DPart dsplit16(int64_t L, int64_t K, int64_t i) {
   return {lo, hi - lo};
 }
 
-// ---------------------------------------------------------------- flags
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <bool SYS>
 __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
   uint64_t v;
@@ -53,16 +111,42 @@ __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
   return v;
 }
 template <bool SYS>
-__device__ __forceinline__ void signal(uint64_t* p, uint64_t v) {
-  // fence.acq_rel + relaxed store == release; the preceding bar.sync makes
-  // the whole CTA's stores of the tile part of what is released.
-  if (SYS) asm volatile("fence.acq_rel.sys;\n\tst.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-  else asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void fence_rel() {
+  if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  if (SYS) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void named_sync(int id) {  // every warp except the signaler
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "n"(NPART) : "memory");
+}
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
 }
 
 // Spin until *f >= target; returns the value seen.  Watchdog: after
@@ -76,7 +160,7 @@ __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p
   uint64_t t0 = globaltimer();
   uint32_t spins = 0;
   while ((v = ld_acquire<SYS>(f)) < target) {
-    if (++spins > 256) __nanosleep(40);
+    if (++spins > 64) __nanosleep(32);
     if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
       volatile int* e = p.errinfo;
       if (e && atomicCAS(p.errinfo, 0, -1) == 0) {
@@ -96,71 +180,74 @@ __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p
   return v;
 }
 
-// ---------------------------------------------------------------- data
-__device__ __forceinline__ int4 ld_vec(const int4* p, bool nc) { return nc ? __ldg(p) : __ldcg(p); }
-__device__ __forceinline__ void st_vec(int4* p, const int4& v) { __stcg(p, v); }
-
-// accumulator of one 16 B vector, per element type
+// ---------------------------------------------------------------- arithmetic
+// accumulator of one 16 B vector, per element type (fixed order, f32 for
+// the 16-bit types, one rounding at the end: DESIGN.md "Reduction order")
 template <int DT>
 struct Vec;
 template <>
 struct Vec<0> {  // u8, wrapping
   uint4 a;
-  __device__ void init(int4 v) { a = make_uint4(v.x, v.y, v.z, v.w); }
-  __device__ void add(int4 v) {
+  __device__ void init(uint4 v) { a = v; }
+  __device__ void add(uint4 v) {
     a.x = __vadd4(a.x, v.x);
     a.y = __vadd4(a.y, v.y);
     a.z = __vadd4(a.z, v.z);
     a.w = __vadd4(a.w, v.w);
   }
-  __device__ int4 out() const { return make_int4(a.x, a.y, a.z, a.w); }
+  __device__ uint4 out() const { return a; }
 };
 template <>
 struct Vec<1> {  // i32, two's-complement wrap
   uint4 a;
-  __device__ void init(int4 v) { a = make_uint4(v.x, v.y, v.z, v.w); }
-  __device__ void add(int4 v) {
-    a.x += uint32_t(v.x);
-    a.y += uint32_t(v.y);
-    a.z += uint32_t(v.z);
-    a.w += uint32_t(v.w);
+  __device__ void init(uint4 v) { a = v; }
+  __device__ void add(uint4 v) {
+    a.x += v.x;
+    a.y += v.y;
+    a.z += v.z;
+    a.w += v.w;
   }
-  __device__ int4 out() const { return make_int4(a.x, a.y, a.z, a.w); }
+  __device__ uint4 out() const { return a; }
 };
 template <>
 struct Vec<2> {  // f32, adds in input order
-  float4 a;
-  __device__ void init(int4 v) { a = make_float4(__int_as_float(v.x), __int_as_float(v.y), __int_as_float(v.z), __int_as_float(v.w)); }
-  __device__ void add(int4 v) {
-    a.x = __fadd_rn(a.x, __int_as_float(v.x));
-    a.y = __fadd_rn(a.y, __int_as_float(v.y));
-    a.z = __fadd_rn(a.z, __int_as_float(v.z));
-    a.w = __fadd_rn(a.w, __int_as_float(v.w));
+  float a[4];
+  __device__ void init(uint4 v) {
+    a[0] = __uint_as_float(v.x);
+    a[1] = __uint_as_float(v.y);
+    a[2] = __uint_as_float(v.z);
+    a[3] = __uint_as_float(v.w);
   }
-  __device__ int4 out() const { return make_int4(__float_as_int(a.x), __float_as_int(a.y), __float_as_int(a.z), __float_as_int(a.w)); }
+  __device__ void add(uint4 v) {
+    a[0] = __fadd_rn(a[0], __uint_as_float(v.x));
+    a[1] = __fadd_rn(a[1], __uint_as_float(v.y));
+    a[2] = __fadd_rn(a[2], __uint_as_float(v.z));
+    a[3] = __fadd_rn(a[3], __uint_as_float(v.w));
+  }
+  __device__ uint4 out() const {
+    return make_uint4(__float_as_uint(a[0]), __float_as_uint(a[1]), __float_as_uint(a[2]), __float_as_uint(a[3]));
+  }
 };
 template <>
 struct Vec<3> {  // bf16: widen, add in f32 in input order, round once
   float a[8];
-  __device__ static float lo(uint32_t w) { return __uint_as_float(w << 16); }
-  __device__ static float hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-  __device__ void init(int4 v) {
-    uint32_t w[4] = {uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w)};
+  __device__ void init(uint4 v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      a[2 * k] = lo(w[k]);
-      a[2 * k + 1] = hi(w[k]);
+      a[2 * k] = __uint_as_float(w[k] << 16);
+      a[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
     }
   }
-  __device__ void add(int4 v) {
-    uint32_t w[4] = {uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w)};
+  __device__ void add(uint4 v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      a[2 * k] = __fadd_rn(a[2 * k], lo(w[k]));
-      a[2 * k + 1] = __fadd_rn(a[2 * k + 1], hi(w[k]));
+      a[2 * k] = __fadd_rn(a[2 * k], __uint_as_float(w[k] << 16));
+      a[2 * k + 1] = __fadd_rn(a[2 * k + 1], __uint_as_float(w[k] & 0xffff0000u));
     }
   }
-  __device__ int4 out() const {
+  __device__ uint4 out() const {
     uint32_t w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -168,13 +255,13 @@ struct Vec<3> {  // bf16: widen, add in f32 in input order, round once
       uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(a[2 * k + 1]));
       w[k] = l | (h << 16);
     }
-    return make_int4(w[0], w[1], w[2], w[3]);
+    return make_uint4(w[0], w[1], w[2], w[3]);
   }
 };
 template <>
 struct Vec<4> {  // f16: widen, add in f32 in input order, round once
   float a[8];
-  __device__ void init(int4 v) {
+  __device__ void init(uint4 v) {
     const __half2* h = reinterpret_cast<const __half2*>(&v);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -183,7 +270,7 @@ struct Vec<4> {  // f16: widen, add in f32 in input order, round once
       a[2 * k + 1] = f.y;
     }
   }
-  __device__ void add(int4 v) {
+  __device__ void add(uint4 v) {
     const __half2* h = reinterpret_cast<const __half2*>(&v);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -192,8 +279,8 @@ struct Vec<4> {  // f16: widen, add in f32 in input order, round once
       a[2 * k + 1] = __fadd_rn(a[2 * k + 1], f.y);
     }
   }
-  __device__ int4 out() const {
-    int4 r;
+  __device__ uint4 out() const {
+    uint4 r;
     __half2* h = reinterpret_cast<__half2*>(&r);
 #pragma unroll
     for (int k = 0; k < 4; ++k) h[k] = __halves2half2(__float2half_rn(a[2 * k]), __float2half_rn(a[2 * k + 1]));
@@ -201,10 +288,10 @@ struct Vec<4> {  // f16: widen, add in f32 in input order, round once
   }
 };
 
-// element-wise path (unaligned ops and the < 16 B chunk tail)
+// element-wise path (unaligned ops, the < 16 B chunk tail): global -> global
 template <int DT>
-__device__ void elem_op(const char* const* in, const uint8_t* nc, int nin, char* const* out, int nout,
-                        int64_t off, int64_t nbytes, int tid, int nthr) {
+__device__ void elem_op(const char* const* in, int nin, char* const* out, int nout, int64_t off, int64_t nbytes,
+                        int tid, int nthr) {
   constexpr int ES = (DT == 0) ? 1 : (DT == 3 || DT == 4) ? 2 : 4;
   for (int64_t i = tid; i < nbytes / ES; i += nthr) {
     const int64_t b = off + i * ES;
@@ -233,171 +320,350 @@ __device__ void elem_op(const char* const* in, const uint8_t* nc, int nin, char*
   }
 }
 
-// one tile of a copy op: one input, nout destinations
-__device__ __forceinline__ void copy_tile(const char* in, bool nc, char* const* out, int nout, int64_t off,
-                                          int64_t nbytes) {
-  const int4* src = reinterpret_cast<const int4*>(in + off);
-  const int64_t nv = nbytes >> 4;
-  for (int64_t i = threadIdx.x; i < nv; i += NT * U) {
-    int4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i + u * NT < nv) v[u] = ld_vec(src + i + u * NT, nc);
-    for (int o = 0; o < nout; ++o) {
-      int4* dst = reinterpret_cast<int4*>(out[o] + off);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i + u * NT < nv) st_vec(dst + i + u * NT, v[u]);
-    }
-  }
-}
-
-template <int DT>
-__device__ __forceinline__ void reduce_tile(const char* const* in, const uint8_t* nc, int nin, char* const* out,
-                                            int nout, int64_t off, int64_t nbytes) {
-  const int64_t nv = nbytes >> 4;
-  for (int64_t i = threadIdx.x; i < nv; i += NT * U) {
-    Vec<DT> acc[U];
-    {
-      const int4* s = reinterpret_cast<const int4*>(in[0] + off);
-      int4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i + u * NT < nv) v[u] = ld_vec(s + i + u * NT, nc[0]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc[u].init(v[u]);
-    }
-    for (int k = 1; k < nin; ++k) {
-      const int4* s = reinterpret_cast<const int4*>(in[k] + off);
-      int4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i + u * NT < nv) v[u] = ld_vec(s + i + u * NT, nc[k]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc[u].add(v[u]);
-    }
-    int4 r[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = acc[u].out();
-    for (int o = 0; o < nout; ++o) {
-      int4* dst = reinterpret_cast<int4*>(out[o] + off);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i + u * NT < nv) st_vec(dst + i + u * NT, r[u]);
-    }
-  }
-}
+struct SigEntry {
+  uint32_t op, last;
+  uint64_t end;
+};
+struct Smem {
+  uint64_t full[NSTAGE], ready[NSTAGE], empty[NSTAGE];
+  SigEntry q[SIGQ];                 // completed tiles whose counters must be released
+  uint32_t q_head, q_tail, q_done;  // storer pushes, signaler pops (release/acquire, cta)
+  volatile uint32_t completed_seq;  // storer: tiles < completed_seq fully written
+  uint32_t entry_mask;
+};
+static_assert(sizeof(Smem) <= SMEM_HDR, "smem header");
 
 template <int DT, bool SYS>
 __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KParams p) {
-  const int tid = threadIdx.x;
-  const int lr = blockIdx.x / p.nch, ch = blockIdx.x % p.nch;
-  const int rank = p.rank0 + lr;
-
-  __shared__ uint64_t s_e;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  uint8_t* const bufs = smem_raw + SMEM_HDR;
+  const size_t STAGE = size_t(p.tile);
   __shared__ const char* s_inp[kMaxOpIn];
   __shared__ char* s_outp[kMaxOpOut];
-  __shared__ uint64_t* s_inflag[kMaxOpIn];
-  __shared__ uint64_t* s_sigflag[kMaxOpOut];
-  __shared__ uint8_t s_nc[kMaxOpIn];
+  __shared__ uint64_t* s_sig[kMaxOpOut];
   __shared__ uint8_t s_every[kMaxOpOut];
-  __shared__ uint8_t s_outrank[kMaxOpOut];
-  __shared__ uint32_t s_ready[kMaxOpIn];
-  __shared__ int32_t s_inslot[kMaxOpIn];
-  __shared__ uint32_t s_entry_mask;
-  __shared__ int s_any_every;
+  __shared__ uint64_t s_e;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int lr = blockIdx.x / p.nch, ch = blockIdx.x % p.nch;
+  const int cg = ch % p.kc, cb = ch / p.kc;  // chunk group, byte part
+  const int rank = p.rank0 + lr;
+  uint64_t* const myflags = reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]);
 
   if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.ready[s], NCW);
+      mbar_init(&S.empty[s], 1);
+    }
+    S.completed_seq = 0;
+    S.q_head = S.q_tail = S.q_done = 0;
+    S.entry_mask = 1u << rank;
     s_e = p.epochs[blockIdx.x] + 1;
-    s_entry_mask = 1u << rank;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const uint64_t e = s_e;
-  uint64_t* const myflags = reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]);
-
   if (p.multiprocess)  // "rank `rank`, channel ch entered launch e"
     for (int t = tid; t < p.P; t += NT)
-      if (t != rank)
-        signal<SYS>(reinterpret_cast<uint64_t*>(p.base[t][SP_FLAGS_IDX]) + p.entry_base + rank * p.nch + ch, e);
+      if (t != rank) {
+        fence_rel<SYS>();
+        st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[t][SP_FLAGS_IDX]) + p.entry_base + rank * p.nch + ch, e);
+      }
 
   const uint32_t ob = p.prog[rank], oe = p.prog[rank + 1];
+  uint32_t it = 0;   // stage-use counter (same sequence in every role)
+  uint32_t seq = 0;  // tile sequence number (for local read-after-write)
+
+  // storer FIFO of committed tiles awaiting read-release / completion
+  uint32_t f_stage[FIFO], f_op[FIFO], f_seq[FIFO];
+  uint64_t f_end[FIFO];
+  uint8_t f_last[FIFO];
+  uint32_t f_head = 0, f_tail = 0, f_rel = 0;  // [f_head, f_tail) pending completion; [f_rel, f_tail) pending release
+
+  // storer, lane 0: tile k of the FIFO is complete (its bulk group retired).
+  // Counter releases are handed to the signaler warp so the storer never
+  // sits in the release fence while it could be issuing stores.
+  auto signal_entry = [&](uint32_t k) {
+    const uint32_t x = k % FIFO;
+    fence_proxy_async_global();  // async-proxy writes -> generic observers
+    const DevOp op = p.ops[f_op[x]];
+    bool need = false;
+    for (int o = 0; o < op.nout && !need; ++o) {
+      const DevOut d = p.outs[op.out_begin + o];
+      need = d.flag >= 0 && (d.every_tile || f_last[x]);
+    }
+    if (need) {
+      const uint32_t h = S.q_head;
+      while (h - ld_acquire_cta(&S.q_tail) >= SIGQ) __nanosleep(20);
+      S.q[h % SIGQ] = SigEntry{f_op[x], f_last[x], f_end[x]};
+      st_release_cta(&S.q_head, h + 1);
+    }
+    S.completed_seq = f_seq[x] + 1;
+  };
+  auto drain = [&]() {  // storer: retire everything in flight
+    bulk_wait<0>();
+    while (f_rel != f_tail) mbar_arrive(&S.empty[f_stage[(f_rel++) % FIFO]]);
+    while (f_head != f_tail) signal_entry(f_head++);
+  };
+
   for (uint32_t oi = ob; oi < oe; ++oi) {
     const DevOp op = p.ops[oi];
     if (op.kind == 2) {  // end-of-program waits: every receipt has landed
-      for (int i = tid; i < op.nin; i += NT) {
-        const DevIn in = p.ins[op.in_begin + i];
-        const DPart q = dsplit16(int64_t(in.len), p.nch, ch);
-        const uint64_t nt = (q.len + p.tile - 1) / p.tile;
-        if (nt) wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, e * nt, p, rank, ch, int(oi - ob), in.flag);
-      }
-      __syncthreads();
+      if (warp == 0)
+        for (int i = lane; i < op.nin; i += 32) {
+          const DevIn in = p.ins[op.in_begin + i];
+          if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
+          const DPart q = dsplit16(int64_t(in.len), p.kb, cb);
+          if (q.len) wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, e * uint64_t(q.len), p, rank, ch,
+                                  int(oi - ob), in.flag);
+        }
       continue;
     }
-    const DPart q = dsplit16(int64_t(op.len), p.nch, ch);
-    const uint32_t ntiles = uint32_t((q.len + p.tile - 1) / p.tile);
-    if (ntiles == 0) continue;  // empty sub-range: nothing sent, nothing awaited
-    if (tid < op.nin) {
-      const DevIn in = p.ins[op.in_begin + tid];
-      s_inp[tid] = p.base[in.rank][in.space] + in.off;
-      s_nc[tid] = (in.space == 0 && p.send_readonly) ? 1 : 0;
-      s_inslot[tid] = in.flag;
-      s_inflag[tid] = in.flag >= 0 ? myflags + uint64_t(in.flag) * p.nch + ch : nullptr;
-      s_ready[tid] = 0;
-    }
-    if (tid == 0) s_any_every = 0;
-    __syncthreads();
-    if (tid < op.nout) {
-      const DevOut o = p.outs[op.out_begin + tid];
-      s_outp[tid] = p.base[o.rank][o.space] + o.off;
-      s_every[tid] = o.every_tile;
-      s_outrank[tid] = o.rank;
-      s_sigflag[tid] = o.flag >= 0 ? reinterpret_cast<uint64_t*>(p.base[o.rank][SP_FLAGS_IDX]) + uint64_t(o.flag) * p.nch + ch
-                                   : nullptr;
-      if (o.flag >= 0 && o.every_tile) s_any_every = 1;
-      if (p.multiprocess && o.rank != rank && !(s_entry_mask & (1u << o.rank))) {
-        wait_ge<SYS>(myflags + p.entry_base + o.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
-        atomicOr(&s_entry_mask, 1u << o.rank);
-      }
-    }
-    __syncthreads();
-    const bool any_every = s_any_every != 0;
-    const uint64_t base = (e - 1) * uint64_t(ntiles);
+    if (int(op.chunk % uint32_t(p.kc)) != cg) continue;  // another channel's chunk group
+    const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
+    if (q.len == 0) continue;  // empty sub-range: nothing sent, nothing awaited
+    const uint64_t fbase = (e - 1) * uint64_t(q.len);
 
-    for (uint32_t t = 0; t < ntiles; ++t) {
-      if (tid < op.nin && s_inflag[tid] && s_ready[tid] <= t) {
-        uint64_t v = wait_ge<SYS>(s_inflag[tid], base + t + 1, p, rank, ch, int(oi - ob), s_inslot[tid]);
-        uint64_t r = v - base;
-        s_ready[tid] = uint32_t(r > ntiles ? ntiles : r);
+    if (!op.vec) {
+      // ---- unaligned op: whole CTA (but the signaler), element-wise, synchronous ----
+      if (warp == 2) continue;
+      const int ptid = warp < 2 ? tid : tid - 32;
+      if (warp == 1 && lane == 0) drain();
+      named_sync(1);
+      if (tid < op.nin) {
+        const DevIn in = p.ins[op.in_begin + tid];
+        s_inp[tid] = p.base[in.rank][in.space] + in.off;
+        if (in.flag >= 0)
+          wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, fbase + uint64_t(q.len), p, rank, ch, int(oi - ob),
+                       in.flag);
       }
-      __syncthreads();
-      const int64_t off = q.off + int64_t(t) * p.tile;
-      const int64_t nb = min(int64_t(p.tile), q.len - int64_t(t) * p.tile);
-      const int64_t nvb = op.vec ? (nb & ~int64_t(15)) : 0;
-      if (nvb) {
-        if (op.kind == 0) copy_tile(s_inp[0], s_nc[0], s_outp, op.nout, off, nvb);
-        else reduce_tile<DT>(s_inp, s_nc, op.nin, s_outp, op.nout, off, nvb);
+      if (tid < op.nout) {
+        const DevOut d = p.outs[op.out_begin + tid];
+        s_outp[tid] = p.base[d.rank][d.space] + d.off;
+        if (p.multiprocess && d.rank != rank && !(atomicOr(&S.entry_mask, 0u) & (1u << d.rank))) {
+          wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
+          atomicOr(&S.entry_mask, 1u << d.rank);
+        }
       }
-      if (nb > nvb) {
-        if (op.kind == 0) elem_op<0>(s_inp, s_nc, 1, s_outp, op.nout, off + nvb, nb - nvb, tid, NT);
-        else elem_op<DT>(s_inp, s_nc, op.nin, s_outp, op.nout, off + nvb, nb - nvb, tid, NT);
+      named_sync(1);
+      if (op.kind == 0) elem_op<0>(s_inp, 1, s_outp, op.nout, q.off, q.len, ptid, NPART);
+      else elem_op<DT>(s_inp, op.nin, s_outp, op.nout, q.off, q.len, ptid, NPART);
+      named_sync(1);
+      if (warp == 1 && lane == 0) {
+        fence_rel<SYS>();
+        for (int o = 0; o < op.nout; ++o) {
+          const DevOut d = p.outs[op.out_begin + o];
+          if (d.flag >= 0)
+            st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
+                            fbase + uint64_t(q.len));
+        }
+        S.completed_seq = seq + 1;
       }
-      const bool last = t + 1 == ntiles;
-      if (last || any_every) {
-        __syncthreads();
-        if (tid < op.nout && s_sigflag[tid] && (last || s_every[tid])) signal<SYS>(s_sigflag[tid], base + t + 1);
+      named_sync(1);
+      ++seq;
+      continue;
+    }
+
+    // ---- pipelined op ----
+    const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
+    const uint32_t ntiles = uint32_t((q.len + T - 1) / T);
+
+    if (warp == 0) {
+      // ================= producer =================
+      uint64_t ready = 0;  // lane k tracks input k's counter (k < 32)
+      const char* src = nullptr;
+      int32_t flag = -1;
+      if (lane < op.nin) {
+        const DevIn in = p.ins[op.in_begin + lane];
+        src = p.base[in.rank][in.space] + in.off + q.off;
+        flag = in.flag;
+      }
+      if (op.raw && lane == 0)  // input written by an earlier op of this CTA: the storer drains first
+        while (S.completed_seq < seq) __nanosleep(32);
+      __syncwarp();
+      for (uint32_t t = 0; t < ntiles; ++t, ++it) {
+        const uint32_t s = it % NSTAGE, ph = (it / NSTAGE) & 1;
+        const uint64_t lo = uint64_t(t) * T;
+        const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
+        const uint32_t nv = n & ~15u;
+        if (flag >= 0) {
+          const uint64_t need = fbase + lo + n;
+          if (ready < need) ready = wait_ge<SYS>(myflags + uint64_t(flag) * p.nch + ch, need, p, rank, ch, int(oi - ob), flag);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_wait(&S.empty[s], ph ^ 1);
+          mbar_arrive_tx(&S.full[s], nv * op.nin);
+        }
+        __syncwarp();
+        if (lane < op.nin && nv) {
+          fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
+          bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, &S.full[s]);
+        }
+      }
+    } else if (warp == 2) {
+      // signaler: runs its own loop below
+    } else if (warp >= CW0) {
+      // ================= compute (REDUCE only; others just pass) =================
+      for (uint32_t t = 0; t < ntiles; ++t, ++it) {
+        const uint32_t s = it % NSTAGE, ph = (it / NSTAGE) & 1;
+        mbar_wait(&S.full[s], ph);
+        if (op.kind == 1) {
+          const uint64_t lo = uint64_t(t) * T;
+          const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
+          uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
+          for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
+            Vec<DT> acc;
+            acc.init(b0[v]);
+            for (int k = 1; k < op.nin; ++k) acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T)[v]);
+            b0[v] = acc.out();
+          }
+          fence_proxy_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.ready[s]);
+      }
+    } else {
+      // ================= storer (warp 1, lane 0) =================
+      if (lane == 0) {
+        if (op.raw) drain();  // the producer waits for every earlier tile to be written
+        for (int o = 0; o < op.nout; ++o) {
+          const DevOut d = p.outs[op.out_begin + o];
+          s_outp[o] = p.base[d.rank][d.space] + d.off + q.off;
+          if (p.multiprocess && d.rank != rank && !(S.entry_mask & (1u << d.rank))) {
+            drain();  // never block while holding completed-but-unsignalled tiles
+            wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
+            S.entry_mask |= 1u << d.rank;
+          }
+        }
+        for (uint32_t t = 0; t < ntiles; ++t, ++it, ++seq) {
+          const uint32_t s = it % NSTAGE, ph = (it / NSTAGE) & 1;
+          const uint64_t lo = uint64_t(t) * T;
+          const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
+          const uint32_t nv = n & ~15u;
+          if (!mbar_try(&S.ready[s], ph)) {
+            // Not ready.  A short wait is the producer catching up; a long
+            // one may be a peer dependency that itself waits for our
+            // pending tiles -- retire and signal everything before blocking.
+            const uint64_t t0 = globaltimer();
+            bool ok = false;
+            while (!(ok = mbar_try(&S.ready[s], ph)) && globaltimer() - t0 < kStorerPatienceNs) {
+            }
+            if (!ok) {
+              drain();
+              mbar_wait(&S.ready[s], ph);
+            }
+          }
+          if (n > nv) {  // < 16 B chunk tail: element-wise, global -> global
+            const char* in[kMaxOpIn];
+            for (int k = 0; k < op.nin; ++k) {
+              const DevIn x = p.ins[op.in_begin + k];
+              in[k] = p.base[x.rank][x.space] + x.off + q.off;
+            }
+            if (op.kind == 0) elem_op<0>(in, 1, s_outp, op.nout, int64_t(lo + nv), n - nv, 0, 1);
+            else elem_op<DT>(in, op.nin, s_outp, op.nout, int64_t(lo + nv), n - nv, 0, 1);
+          }
+          if (nv)
+            for (int o = 0; o < op.nout; ++o) bulk_store(s_outp[o] + lo, bufs + size_t(s) * STAGE, nv);
+          bulk_commit();
+          const uint32_t x = f_tail % FIFO;
+          f_stage[x] = s;
+          f_op[x] = oi;
+          f_seq[x] = seq;
+          f_end[x] = lo + n;
+          f_last[x] = t + 1 == ntiles;
+          ++f_tail;
+          // smem of all but the newest group has been read: release stages
+          bulk_wait_read<1>();
+          while (f_tail - f_rel > 1) mbar_arrive(&S.empty[f_stage[(f_rel++) % FIFO]]);
+          // all but the newest sig_lag groups are complete: release counters
+          if (f_tail - f_head > uint32_t(p.sig_lag)) {
+            switch (p.sig_lag) {
+              case 0: bulk_wait<0>(); break;
+              case 1: bulk_wait<1>(); break;
+              case 2: bulk_wait<2>(); break;
+              case 3: bulk_wait<3>(); break;
+              case 4: bulk_wait<4>(); break;
+              case 5: bulk_wait<5>(); break;
+              default: bulk_wait<6>(); break;
+            }
+            while (f_tail - f_head > uint32_t(p.sig_lag)) signal_entry(f_head++);
+          }
+        }
+      } else {
+        it += ntiles;
+        seq += ntiles;
       }
     }
-    __syncthreads();
+    if (warp != 1) seq += ntiles;
   }
+  if (warp == 1 && lane == 0) {
+    drain();
+    st_release_cta(&S.q_done, 1);
+  }
+  if (warp == 2 && lane == 0) {
+    // ================= signaler =================
+    // release the counters of completed tiles: one fence per batch, then
+    // relaxed stores of the (monotone) byte counts
+    uint32_t tail = 0;
+    for (;;) {
+      uint32_t h = ld_acquire_cta(&S.q_head);
+      if (h == tail) {
+        if (ld_acquire_cta(&S.q_done) && ld_acquire_cta(&S.q_head) == tail) break;
+        __nanosleep(20);
+        continue;
+      }
+      fence_rel<SYS>();
+      for (; tail != h; ++tail) {
+        const SigEntry en = S.q[tail % SIGQ];
+        const DevOp op = p.ops[en.op];
+        const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
+        const uint64_t v = (e - 1) * uint64_t(q.len) + en.end;
+        for (int o = 0; o < op.nout; ++o) {
+          const DevOut d = p.outs[op.out_begin + o];
+          if (d.flag >= 0 && (d.every_tile || en.last))
+            st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
+                            v);
+        }
+      }
+      st_release_cta(&S.q_tail, tail);
+    }
+  }
+  __syncthreads();
   if (tid == 0) p.epochs[blockIdx.x] = e;
 }
 
 template <int DT>
-cudaError_t launch_dt(const KParams& p, bool sys, cudaStream_t st) {
-  dim3 grid(p.nranks_launch * p.nch), block(NT);
-  if (sys) exec_kernel<DT, true><<<grid, block, 0, st>>>(p);
-  else exec_kernel<DT, false><<<grid, block, 0, st>>>(p);
-  return cudaGetLastError();
+const void* kernel_ptr(bool sys) {
+  return sys ? reinterpret_cast<const void*>(exec_kernel<DT, true>) : reinterpret_cast<const void*>(exec_kernel<DT, false>);
+}
+
+const void* kernel_for(int dtype, bool sys) {
+  switch (dtype) {
+    case 0: return kernel_ptr<0>(sys);
+    case 1: return kernel_ptr<1>(sys);
+    case 2: return kernel_ptr<2>(sys);
+    case 3: return kernel_ptr<3>(sys);
+    case 4: return kernel_ptr<4>(sys);
+  }
+  return nullptr;
+}
+
+cudaError_t prepare(const void* f) {
+  // once per kernel instantiation (10 of them; the driver call is not free)
+  static const void* done[16] = {};
+  for (auto& d : done)
+    if (d == f) return cudaSuccess;
+  cudaError_t err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes(kMaxTile)));
+  if (err == cudaSuccess)
+    for (auto& d : done)
+      if (!d) {
+        d = f;
+        break;
+      }
+  return err;
 }
 
 }  // namespace
@@ -405,32 +671,22 @@ cudaError_t launch_dt(const KParams& p, bool sys, cudaStream_t st) {
 int exec_threads() { return NT; }
 
 cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st) {
-  switch (dtype) {
-    case 0: return launch_dt<0>(p, sys, st);
-    case 1: return launch_dt<1>(p, sys, st);
-    case 2: return launch_dt<2>(p, sys, st);
-    case 3: return launch_dt<3>(p, sys, st);
-    case 4: return launch_dt<4>(p, sys, st);
-  }
-  return cudaErrorInvalidValue;
+  const void* f = kernel_for(dtype, sys);
+  if (!f) return cudaErrorInvalidValue;
+  cudaError_t err = prepare(f);
+  if (err != cudaSuccess) return err;
+  void* args[] = {const_cast<KParams*>(&p)};
+  return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(NT), args, smem_bytes(p.tile), st);
 }
 
-cudaError_t exec_occupancy(int dtype, bool sys, int* blocks_per_sm) {
-  const void* f = nullptr;
-#define SCCL_F(D)                                                                                   \
-  case D:                                                                                           \
-    f = sys ? reinterpret_cast<const void*>(exec_kernel<D, true>) : reinterpret_cast<const void*>(exec_kernel<D, false>); \
-    break;
-  switch (dtype) {
-    SCCL_F(0)
-    SCCL_F(1)
-    SCCL_F(2)
-    SCCL_F(3)
-    SCCL_F(4)
-    default: return cudaErrorInvalidValue;
-  }
-#undef SCCL_F
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, NT, 0);
+size_t exec_smem_bytes(int tile) { return smem_bytes(tile); }
+
+cudaError_t exec_occupancy(int dtype, bool sys, int tile, int* blocks_per_sm) {
+  const void* f = kernel_for(dtype, sys);
+  if (!f) return cudaErrorInvalidValue;
+  cudaError_t err = prepare(f);
+  if (err != cudaSuccess) return err;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, NT, smem_bytes(tile));
 }
 
 }  // namespace sccl

@@ -11,12 +11,17 @@ constexpr int kMaxRanks = 16;   // pointer table width (kernel parameter space)
 constexpr int kMaxOpIn = 32;    // inputs of one copy/reduce op (staged in smem)
 constexpr int kMaxOpOut = 32;   // destinations of one op
 constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
+constexpr int kMaxTile = 32768; // one TMA pipeline stage
+constexpr int kStages = 6;      // pipeline depth
+constexpr int kThreads = 352;   // producer, storer and signaler warps + 8 compute warps
 
 struct DevIn {
   uint64_t off;   // byte offset of the chunk start in (rank, space)
   uint64_t len;   // chunk length (used by WAIT ops; equal to op len otherwise)
   int32_t flag;   // receipt slot at the executing rank, -1 = none
+  uint32_t chunk; // chunk id (WAIT ops filter by chunk group)
   uint8_t rank, space, pad0, pad1;
+  uint32_t pad2;
 };
 
 struct DevOut {
@@ -27,11 +32,14 @@ struct DevOut {
 
 struct DevOp {
   uint64_t len;   // chunk length in bytes
+  uint32_t chunk; // chunk id: CTA channel (g, b) runs ops with chunk % kc == g
+  uint32_t pad2;
   uint32_t in_begin, out_begin;
   uint16_t nin, nout;
   uint8_t kind;   // 0 copy, 1 reduce, 2 wait
-  uint8_t vec;    // all offsets 16-byte aligned -> 16 B vector path
-  uint8_t pad0, pad1;
+  uint8_t vec;    // all offsets 16-byte aligned -> TMA bulk path
+  uint8_t raw;    // reads a location an earlier op of this rank wrote (no flag)
+  uint8_t pad1;
 };
 
 enum ErrCode : int { ERR_NONE = 0, ERR_TIMEOUT = 5 };
@@ -46,7 +54,9 @@ struct KParams {
   int* errinfo;          // host-mapped watchdog record
   long long timeout_ns;
   int P, nch, rank0, nranks_launch;
-  int tile;              // bytes per tile (multiple of 16)
+  int kc, kb;            // nch = kc * kb: chunk groups x byte parts per chunk
+  int tile;              // copy tile = pipeline stage bytes (<= kMaxTile); reduce tiles tile/nin
+  int sig_lag;           // bulk groups the storer keeps in flight before retiring (0..6)
   int entry_base;        // index of the entry-handshake flags in FLAGS
   int multiprocess;      // 1: peers are other processes (entry handshake)
   int send_readonly;     // 1: SEND does not alias RECV (non-coherent loads ok)

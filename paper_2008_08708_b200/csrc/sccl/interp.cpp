@@ -95,7 +95,7 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
     g_ierr = "needs a loopback plan";
     return SCCL_INVALID_ARGUMENT;
   }
-  const int P = p->nranks, nch = p->nch;
+  const int P = p->nranks, nch = p->nch, kc = p->kc, kb = p->kb;
   const int64_t tile = p->tile;
   const size_t nflags = size_t(p->entry_base + P * nch);
   std::vector<std::vector<std::atomic<uint64_t>>> flags(P);
@@ -127,19 +127,25 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
   };
 
   auto run = [&](int rank, int ch) {
+    const int cg = ch % kc, cb = ch / kc;  // same channel map as the kernel
     for (uint32_t oi = p->prog[rank]; oi < p->prog[rank + 1]; ++oi) {
       const DevOp& op = p->ops[oi];
       if (op.kind == OP_WAIT) {
         for (int i = 0; i < op.nin; ++i) {
           const DevIn& in = p->ins[op.in_begin + i];
-          Part q = split16(int64_t(in.len), nch, ch);
-          uint64_t nt = uint64_t((q.len + tile - 1) / tile);
-          if (nt) wait_ge(flags[rank][size_t(in.flag) * nch + ch], e * nt);
+          if (int(in.chunk % uint32_t(kc)) != cg) continue;
+          Part q = split16(int64_t(in.len), kb, cb);
+          if (q.len) wait_ge(flags[rank][size_t(in.flag) * nch + ch], e * uint64_t(q.len));
         }
         continue;
       }
-      Part q = split16(int64_t(op.len), nch, ch);
-      uint64_t ntiles = uint64_t((q.len + tile - 1) / tile);
+      if (int(op.chunk % uint32_t(kc)) != cg) continue;
+      Part q = split16(int64_t(op.len), kb, cb);
+      if (q.len == 0) continue;
+      // same tiling rule as the kernel: copy tiles of `tile`, reduce tiles
+      // of tile/nin; counters count bytes so the two sides may differ
+      const int64_t T = op.kind == OP_COPY ? tile : std::max<int64_t>(16, (tile / op.nin) & ~int64_t(15));
+      const int64_t ntiles = (q.len + T - 1) / T;
       std::vector<const char*> inp(op.nin);
       std::vector<char*> outp(op.nout);
       for (int i = 0; i < op.nin; ++i) {
@@ -150,22 +156,21 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
         const DevOut& out = p->outs[op.out_begin + o];
         outp[o] = base(out.rank, out.space) + out.off;
       }
-      const uint64_t b0 = (e - 1) * ntiles;
-      for (uint64_t t = 0; t < ntiles; ++t) {
+      const uint64_t b0 = (e - 1) * uint64_t(q.len);
+      for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t lo = t * T, nb = std::min<int64_t>(T, q.len - lo);
         for (int i = 0; i < op.nin; ++i) {
           const DevIn& in = p->ins[op.in_begin + i];
-          if (in.flag >= 0) wait_ge(flags[rank][size_t(in.flag) * nch + ch], b0 + t + 1);
+          if (in.flag >= 0) wait_ge(flags[rank][size_t(in.flag) * nch + ch], b0 + uint64_t(lo + nb));
         }
         if (failed.load()) return;
-        int64_t off = q.off + int64_t(t) * tile;
-        int64_t nb = std::min<int64_t>(tile, q.len - int64_t(t) * tile);
         elem_range(op.kind == OP_COPY ? 0 : p->dtype, inp.data(), op.kind == OP_COPY ? 1 : op.nin, outp.data(),
-                   op.nout, off, nb);
+                   op.nout, q.off + lo, nb);
         bool last = t + 1 == ntiles;
         for (int o = 0; o < op.nout; ++o) {
           const DevOut& out = p->outs[op.out_begin + o];
           if (out.flag >= 0 && (last || out.every_tile))
-            flags[out.rank][size_t(out.flag) * nch + ch].store(b0 + t + 1, std::memory_order_release);
+            flags[out.rank][size_t(out.flag) * nch + ch].store(b0 + uint64_t(lo + nb), std::memory_order_release);
         }
       }
     }

@@ -40,7 +40,7 @@ struct Builder {
     op.key = key;
     op.chunk = c;
     op.len = pg.geo[c].len;
-    op.ins.push_back({src.loc, src.flag, op.len});
+    op.ins.push_back({src.loc, src.flag, op.len, c});
     op.outs.push_back({dst, slot, false});
     pg.ranks[rank].ops.push_back(std::move(op));
   }
@@ -150,8 +150,8 @@ Program lower(const Schedule& s, int64_t nbytes, int esize) {
           op.chunk = c;
           op.len = pg.geo[c].len;
           Cur& x = b.cur[c * P + n];
-          if (x.valid) op.ins.push_back({x.loc, x.flag, op.len});
-          for (auto& r : rs) op.ins.push_back({r.loc, r.slot, op.len});
+          if (x.valid) op.ins.push_back({x.loc, x.flag, op.len, c});
+          for (auto& r : rs) op.ins.push_back({r.loc, r.slot, op.len, c});
           Loc acc;
           if (s.kind == Kind::Allreduce || post[c * P + n]) {
             acc = b.out_loc(c, n);
@@ -260,7 +260,7 @@ Program lower(const Schedule& s, int64_t nbytes, int esize) {
     for (int r = 0; r < P; ++r)
       for (auto& op : pg.ranks[r].ops)
         for (auto& o : op.outs)
-          if (o.flag >= 0 && o.loc.rank == d && !consumed[o.flag]) w.ins.push_back({o.loc, o.flag, op.len});
+          if (o.flag >= 0 && o.loc.rank == d && !consumed[o.flag]) w.ins.push_back({o.loc, o.flag, op.len, op.chunk});
     std::sort(w.ins.begin(), w.ins.end(), [](const OpIn& a, const OpIn& z) { return a.flag < z.flag; });
     if (!w.ins.empty()) pg.ranks[d].ops.push_back(std::move(w));
   }

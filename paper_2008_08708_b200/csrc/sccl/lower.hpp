@@ -35,6 +35,7 @@ struct OpIn {
   Loc loc;
   int flag = -1;  // receipt slot at loc.rank whose counter gates this input, or -1
   int64_t len = 0;
+  int chunk = -1;
   bool operator==(const OpIn& o) const { return loc == o.loc && flag == o.flag && len == o.len; }
 };
 

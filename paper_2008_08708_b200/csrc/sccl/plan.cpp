@@ -12,7 +12,7 @@
 
 namespace sccl {
 cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st);
-cudaError_t exec_occupancy(int dtype, bool sys, int* blocks_per_sm);
+cudaError_t exec_occupancy(int dtype, bool sys, int tile, int* blocks_per_sm);
 int exec_threads();
 }  // namespace sccl
 
@@ -69,7 +69,7 @@ int esize_of(int dtype) {
 struct IpcBlob {
   char magic[8];
   char fingerprint[24];
-  int32_t rank, nranks, nch, tile;
+  int32_t rank, nranks, nch, kc, kb, tile;
   uint64_t region_bytes;
   cudaIpcMemHandle_t handle;
 };
@@ -79,7 +79,7 @@ struct IpcBlob {
 namespace sccl {
 
 void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks, int64_t bytes, int dtype,
-                     int redop, int device, int nch, int tile, int64_t timeout_ms, bool loopback) {
+                     int redop, int device, const ChannelRequest& req, int64_t timeout_ms, bool loopback) {
   if (redop != SCCL_SUM) throw invalid_argument_error("only SCCL_SUM is supported");
   const int es = esize_of(dtype);
   p.sched = parse_schedule(json);
@@ -98,19 +98,45 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   p.host_only = device < 0;
   p.timeout_ns = timeout_ms < 0 ? 0 : (timeout_ms == 0 ? 10000LL : timeout_ms) * 1000000LL;
 
-  // channels: enough CTAs to cover the GPU in loopback, NVLink-sized in
-  // multi-process mode, and no channel below 32 KiB of the largest chunk
+  // ---- channels (CTAs per rank) and tile (= one TMA pipeline stage) ----
+  // channel j = (chunk group j % kc, byte part j / kc).  Large chunks are cut
+  // into byte parts so every SM streams; small chunks are spread over chunk
+  // groups so independent chunks travel in parallel instead of queueing
+  // behind each other in one CTA (latency).
   int64_t maxlen = 0;
   for (auto& g : p.pg.geo) maxlen = std::max(maxlen, g.len);
-  if (nch <= 0) {
-    int cap = loopback ? std::max(1, p.nch /*preset: SMs*bps*/ / p.sched.P) : 32;
-    int64_t want = (maxlen + 32767) / 32768;
-    nch = int(std::max<int64_t>(1, std::min<int64_t>(cap, want)));
+  const int G = p.pg.G;
+  int tile = req.tile;
+  if (tile <= 0) {
+    tile = kMaxTile;
+    if (maxlen < kMaxTile) {
+      tile = 1024;
+      while (tile < maxlen) tile *= 2;
+    }
   }
-  p.nch = nch;
-  if (tile <= 0) tile = 65536;
-  if (tile % 16) throw invalid_argument_error("tile_bytes must be a multiple of 16");
+  if (tile % 16 || tile > kMaxTile || tile < 256)
+    throw invalid_argument_error("tile_bytes must be a multiple of 16 in [256, 32768]");
+  int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, tile)
+                              : std::max(1, std::min(2048 / kThreads, int((227 << 10) / (kStages * tile + 256))));
+  const int resident = std::max(1, req.sms * std::max(1, bps));
+  const int cap = loopback ? std::max(1, resident / p.sched.P) : 32;
+  int kb, kc;
+  if (req.nchannels > 0) {
+    kb = req.nchannels;
+    kc = req.chunk_groups > 0 ? req.chunk_groups : 1;
+  } else {
+    kb = int(std::max<int64_t>(1, std::min<int64_t>(cap, (maxlen + kMaxTile - 1) / kMaxTile)));
+    kc = req.chunk_groups > 0 ? req.chunk_groups : std::max(1, std::min(G, cap / kb));
+  }
+  if (kc < 1 || kb < 1) throw invalid_argument_error("channels must be positive");
+  p.kc = kc;
+  p.kb = kb;
+  p.nch = kc * kb;
   p.tile = tile;
+  // small tiles: signal every tile at once (latency); large: keep 3 bulk
+  // groups in flight (bandwidth; FIFO depth 8 in the kernel)
+  p.sig_lag = tile >= 16384 ? 6 : 0;
+  p.resident_cap = loopback ? resident : 0;
 
   // device encoding
   const int P = p.sched.P;
@@ -125,6 +151,7 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
         throw invalid_argument_error("op fan-in/fan-out exceeds executor limits (32)");
       DevOp d{};
       d.len = uint64_t(op.len);
+      d.chunk = uint32_t(std::max(0, op.chunk));
       d.kind = uint8_t(op.kind);
       d.in_begin = uint32_t(p.ins.size());
       d.out_begin = uint32_t(p.outs.size());
@@ -137,9 +164,11 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
         x.off = uint64_t(in.loc.off);
         x.len = uint64_t(in.len);
         x.flag = in.flag;
+        x.chunk = uint32_t(std::max(0, in.chunk));
         x.rank = uint8_t(in.loc.rank);
         x.space = uint8_t(in.loc.space);
         vec &= in.loc.off % 16 == 0;
+        if (in.flag < 0 && in.loc.space != SP_SEND) d.raw = 1;
         p.ins.push_back(x);
       }
       for (auto& o : op.outs) {
@@ -203,13 +232,15 @@ void plan_device_setup(sccl_plan& p) {
   }
 }
 
-int auto_channels_cap(int device, int dtype) {
-  // loopback: CTAs resident at once (all ranks' programs must be co-resident)
-  cudaDeviceProp prop{};
-  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+struct OccCtx {
+  int dtype;
+  bool sys;
+};
+int occ_fn(void* ctx, int tile) {
+  auto* c = static_cast<OccCtx*>(ctx);
   int bps = 0;
-  cuda_check(exec_occupancy(dtype, false, &bps), "occupancy");
-  return prop.multiProcessorCount * std::max(1, std::min(bps, 2));
+  cuda_check(exec_occupancy(c->dtype, c->sys, tile, &bps), "occupancy");
+  return bps;
 }
 
 void check_aligned(const void* p, const char* what) {
@@ -232,7 +263,10 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.timeout_ns = p.timeout_ns;
   k.P = p.nranks;
   k.nch = p.nch;
+  k.kc = p.kc;
+  k.kb = p.kb;
   k.tile = p.tile;
+  k.sig_lag = p.sig_lag;
   k.entry_base = p.entry_base;
 }
 
@@ -244,6 +278,7 @@ void sccl_plan_opts_init(sccl_plan_opts* o) {
   if (!o) return;
   o->device = 0;
   o->nchannels = 0;
+  o->chunk_groups = 0;
   o->tile_bytes = 0;
   o->timeout_ms = 0;
 }
@@ -301,18 +336,23 @@ static int create_common(const char* json, int rank, int nranks, size_t bytes, i
     if (opts) o = *opts;
     auto* p = new sccl_plan();
     try {
-      int nch = o.nchannels;
-      if (loopback && nch <= 0) {
-        // cap derived from the device when there is one (nch preset = SMs*bps)
-        p->nch = (o.device >= 0) ? auto_channels_cap(o.device, dtype) : 296;
+      ChannelRequest req;
+      req.nchannels = o.nchannels;
+      req.chunk_groups = o.chunk_groups;
+      req.tile = o.tile_bytes;
+      OccCtx occ{dtype, !loopback};
+      if (o.device >= 0) {
+        cudaDeviceProp prop{};
+        cuda_check(cudaGetDeviceProperties(&prop, o.device), "cudaGetDeviceProperties");
+        cuda_check(cudaSetDevice(o.device), "cudaSetDevice");
+        req.sms = prop.multiProcessorCount;
+        req.blocks_per_sm = occ_fn;
+        req.ctx = &occ;
       }
-      plan_build_host(*p, json, rank, nranks, int64_t(bytes), dtype, redop, o.device, nch, o.tile_bytes,
-                      o.timeout_ms, loopback);
-      if (loopback && o.device >= 0) {
-        int cap = auto_channels_cap(o.device, dtype);
-        if (p->nch * p->nranks > cap)
-          throw invalid_argument_error("loopback needs P*nchannels <= resident CTAs (" + std::to_string(cap) + ")");
-      }
+      plan_build_host(*p, json, rank, nranks, int64_t(bytes), dtype, redop, o.device, req, o.timeout_ms, loopback);
+      if (loopback && p->nch * p->nranks > p->resident_cap)
+        throw invalid_argument_error("loopback needs P*nchannels <= resident CTAs (" +
+                                     std::to_string(p->resident_cap) + ")");
       if (!p->host_only) plan_device_setup(*p);
     } catch (...) {
       sccl_plan_destroy(p);
@@ -347,6 +387,8 @@ int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
     b.rank = p->rank;
     b.nranks = p->nranks;
     b.nch = p->nch;
+    b.kc = p->kc;
+    b.kb = p->kb;
     b.tile = p->tile;
     b.region_bytes = p->region_bytes;
     if (!p->host_only) {
@@ -374,7 +416,7 @@ int sccl_plan_bind_peers(sccl_plan* p, const void* const* blobs, size_t blob_len
         throw invalid_argument_error("blob " + std::to_string(r) + " has rank/nranks mismatch");
       if (std::strncmp(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1))
         throw invalid_argument_error("rank " + std::to_string(r) + " lowered a different program (fingerprint mismatch)");
-      if (b.nch != p->nch || b.tile != p->tile || b.region_bytes != p->region_bytes)
+      if (b.nch != p->nch || b.kc != p->kc || b.kb != p->kb || b.tile != p->tile || b.region_bytes != p->region_bytes)
         throw invalid_argument_error("rank " + std::to_string(r) + " uses different channels/tile/region size");
     }
     if (!p->host_only) {
@@ -479,7 +521,8 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
   return guarded([&] {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
-    o << "{\"nchannels\":" << p->nch << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+    o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
+      << ",\"sig_lag\":" << p->sig_lag << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

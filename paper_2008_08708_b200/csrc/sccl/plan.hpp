@@ -17,7 +17,8 @@ struct sccl_plan {
   int rank = 0, nranks = 0;
   bool loopback = false, host_only = false;
   int device = -1, dtype = 0, redop = 0;
-  int nch = 1, tile = 65536;
+  int nch = 1, kc = 1, kb = 1, tile = 32768, sig_lag = 3;
+  int resident_cap = 0;  // loopback: CTAs that fit on the device at once
   long long timeout_ns = 0;
 
   // host copy of the device program (also used by the CPU interpreter)
@@ -49,7 +50,16 @@ struct sccl_plan {
 namespace sccl {
 
 // host-side construction (no CUDA calls)
+// Channel policy inputs: user overrides (0 = auto) and the resident-CTA
+// capacity per SM as a function of the tile (shared-memory stage) size.
+struct ChannelRequest {
+  int nchannels = 0, chunk_groups = 0, tile = 0;
+  int sms = 148;
+  int (*blocks_per_sm)(void* ctx, int tile) = nullptr;
+  void* ctx = nullptr;
+};
+
 void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks, int64_t bytes, int dtype,
-                     int redop, int device, int nch, int tile, int64_t timeout_ms, bool loopback);
+                     int redop, int device, const ChannelRequest& req, int64_t timeout_ms, bool loopback);
 
 }  // namespace sccl

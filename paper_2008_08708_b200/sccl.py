@@ -39,8 +39,8 @@ class PeerTimeoutError(SCCLError):
 
 
 class _Opts(ctypes.Structure):
-    _fields_ = [("device", ctypes.c_int), ("nchannels", ctypes.c_int), ("tile_bytes", ctypes.c_int),
-                ("timeout_ms", ctypes.c_int64)]
+    _fields_ = [("device", ctypes.c_int), ("nchannels", ctypes.c_int), ("chunk_groups", ctypes.c_int),
+                ("tile_bytes", ctypes.c_int), ("timeout_ms", ctypes.c_int64)]
 
 
 _lib = None
@@ -142,8 +142,8 @@ def version() -> str:
 
 
 # ---------------------------------------------------------------- plans
-def _opts(device: int, nchannels: int, tile_bytes: int, timeout_ms: int) -> _Opts:
-    return _Opts(device, nchannels, tile_bytes, timeout_ms)
+def _opts(device: int, nchannels: int, tile_bytes: int, timeout_ms: int, chunk_groups: int = 0) -> _Opts:
+    return _Opts(device, nchannels, chunk_groups, tile_bytes, timeout_ms)
 
 
 def _ptr(x) -> int:
@@ -194,9 +194,9 @@ class LoopbackPlan(_PlanBase):
     """Every rank of the schedule on one GPU; one launch runs them all."""
 
     def __init__(self, schedule, bytes_per_rank: int, dtype: int = U8, device: int = 0,
-                 nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0):
+                 nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0, chunk_groups: int = 0):
         super().__init__()
-        o = _opts(device, nchannels, tile_bytes, timeout_ms)
+        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups)
         rc = lib().sccl_plan_create_loopback(_text(schedule), bytes_per_rank, dtype, SUM,
                                              ctypes.byref(o), ctypes.byref(self._h))
         _raise(rc)
@@ -226,9 +226,10 @@ class Plan(_PlanBase):
     """One rank of a one-process-per-GPU execution (peers over CUDA IPC)."""
 
     def __init__(self, schedule, rank: int, nranks: int, bytes_per_rank: int, dtype: int = U8,
-                 device: int = 0, nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0):
+                 device: int = 0, nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0,
+                 chunk_groups: int = 0):
         super().__init__()
-        o = _opts(device, nchannels, tile_bytes, timeout_ms)
+        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups)
         rc = lib().sccl_plan_create(_text(schedule), rank, nranks, bytes_per_rank, dtype, SUM,
                                     ctypes.byref(o), ctypes.byref(self._h))
         _raise(rc)

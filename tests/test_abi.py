@@ -64,6 +64,8 @@ def test_bad_arguments():
         sccl.LoopbackPlan(S.allreduce_from(S.one_shot_allgather(4)), 4098, sccl.F32, device=-1)
     with pytest.raises(sccl.InvalidArgumentError, match="tile"):
         sccl.LoopbackPlan(js, 4096, sccl.U8, device=-1, tile_bytes=100)
+    with pytest.raises(sccl.InvalidArgumentError, match="tile"):
+        sccl.LoopbackPlan(js, 4096, sccl.U8, device=-1, tile_bytes=65536)
 
 
 def test_blob_exchange_single_process():

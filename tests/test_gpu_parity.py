@@ -106,7 +106,7 @@ def test_parity_u8_and_float(name, nbytes):
         run_gpu(js, nbytes, dt)
 
 
-@pytest.mark.parametrize("nch,tile", [(1, 256), (3, 4096), (7, 65536), (0, 0)])
+@pytest.mark.parametrize("nch,tile", [(1, 256), (3, 4096), (7, 32768), (0, 0)])
 @pytest.mark.parametrize("name", ["ag_777", "ag_b7_ring8", "ar_56_14_14", "ar_ring", "rs_ring8", "a2a_b5"])
 def test_channels_and_tiles(name, nch, tile):
     js = SCHED[name]

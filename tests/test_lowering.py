@@ -56,7 +56,7 @@ def test_interpreter_matches_oracle(name, nbytes):
         run_interp(js, nbytes, dt, nch=2, tile=256)
 
 
-@pytest.mark.parametrize("nch,tile", [(1, 16), (3, 64), (5, 4096)])
+@pytest.mark.parametrize("nch,tile", [(1, 256), (3, 272), (5, 4096)])
 def test_interpreter_channels_tiles(nch, tile):
     for name in ("ham8", "ar_ham", "rs_ring", "a2a_k2"):
         js = CASES[name]
@@ -103,3 +103,32 @@ def test_fingerprint_stable_across_ranks():
     assert a.info()["program"]["fingerprint"] == b.info()["program"]["fingerprint"]
     c = sccl.Plan(CASES["ham8"], 5, 8, 1 << 21, sccl.U8, device=-1)
     assert c.info()["program"]["fingerprint"] != a.info()["program"]["fingerprint"]
+
+
+@pytest.mark.parametrize("kc,kb", [(3, 1), (2, 3), (56, 1), (7, 2)])
+def test_interpreter_chunk_groups(kc, kb):
+    """channel j = (chunk group j % kc, byte part j / kc): independent chunks
+    on different CTAs, each chunk's ops still in program order."""
+    plan_js = [CASES["ham8"], CASES["ar_ham"], CASES["b5"], CASES["reduce"]]
+    for js in plan_js:
+        d = json.loads(js)
+        kind = d["collective"]
+        dt = O.BF16 if kind in ("allreduce", "reducescatter", "reduce") else O.U8
+        nbytes = 8 * 600
+        ins = O.seeded_inputs(kind, d["P"], nbytes, dt, 3)
+        ref = O.execute(d, ins, nbytes, dt)
+        plan = sccl.LoopbackPlan(js, nbytes, dt, device=-1, nchannels=kb, chunk_groups=kc, tile_bytes=256)
+        info = plan.info()
+        assert info["chunk_groups"] == kc and info["byte_parts"] == kb
+        outs = [np.zeros_like(r) for r in ref]
+        plan.interpret_on_cpu(ins, outs)
+        assert all(np.array_equal(a, b) for a, b in zip(outs, ref))
+
+
+def test_auto_channel_policy():
+    """Small chunks spread over chunk groups (latency); large chunks cut into
+    byte parts (bandwidth)."""
+    small = sccl.LoopbackPlan(CASES["ham8"], 1024, sccl.U8, device=-1).info()
+    assert small["chunk_groups"] > 1 and small["byte_parts"] == 1 and small["sig_lag"] == 0
+    large = sccl.LoopbackPlan(CASES["ham8"], 64 << 20, sccl.U8, device=-1).info()
+    assert large["byte_parts"] > 1 and large["tile_bytes"] == 32768 and large["sig_lag"] == 6
