@@ -44,6 +44,7 @@ typedef struct {
   int nchannels;      /* byte parts per chunk (CTAs per rank per chunk group); 0 = auto              */
   int chunk_groups;   /* chunk groups (independent chunks run on different CTAs); 0 = auto          */
   int tile_bytes;     /* pipeline stage / copy tile bytes, multiple of 16 in [256, 32768]; 0 = auto  */
+  int protocol;       /* 0 = auto, 1 = simple (TMA bulk + counters), 2 = LL (flag in data)          */
   int64_t timeout_ms; /* peer-wait watchdog; 0 = default (10 s), <0 = disabled                        */
 } sccl_plan_opts;
 

@@ -635,18 +635,239 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KPa
   if (tid == 0) p.epochs[blockIdx.x] = e;
 }
 
+
+// ============================================================================
+// LL protocol (small messages).  Every receipt slot holds (4 data bytes,
+// 4 flag bytes) words; the sender stores data and the launch epoch together
+// with one 8-byte-atomic half of a 16-byte store, the receiver polls the
+// words themselves.  No counters, no fences, per-word pipelining across
+// hops; 2x the bytes, so only for small chunks.
+// ============================================================================
+constexpr int LL_NT = kLLThreads;
+
 template <int DT>
-const void* kernel_ptr(bool sys) {
+struct Acc8;  // 8 data bytes, same arithmetic as Vec<DT>
+template <>
+struct Acc8<0> {
+  uint32_t a[2];
+  __device__ void init(uint2 v) { a[0] = v.x, a[1] = v.y; }
+  __device__ void add(uint2 v) { a[0] = __vadd4(a[0], v.x), a[1] = __vadd4(a[1], v.y); }
+  __device__ uint2 out() const { return make_uint2(a[0], a[1]); }
+};
+template <>
+struct Acc8<1> {
+  uint32_t a[2];
+  __device__ void init(uint2 v) { a[0] = v.x, a[1] = v.y; }
+  __device__ void add(uint2 v) { a[0] += v.x, a[1] += v.y; }
+  __device__ uint2 out() const { return make_uint2(a[0], a[1]); }
+};
+template <>
+struct Acc8<2> {
+  float a[2];
+  __device__ void init(uint2 v) { a[0] = __uint_as_float(v.x), a[1] = __uint_as_float(v.y); }
+  __device__ void add(uint2 v) {
+    a[0] = __fadd_rn(a[0], __uint_as_float(v.x));
+    a[1] = __fadd_rn(a[1], __uint_as_float(v.y));
+  }
+  __device__ uint2 out() const { return make_uint2(__float_as_uint(a[0]), __float_as_uint(a[1])); }
+};
+template <>
+struct Acc8<3> {
+  float a[4];
+  __device__ void init(uint2 v) {
+    a[0] = __uint_as_float(v.x << 16), a[1] = __uint_as_float(v.x & 0xffff0000u);
+    a[2] = __uint_as_float(v.y << 16), a[3] = __uint_as_float(v.y & 0xffff0000u);
+  }
+  __device__ void add(uint2 v) {
+    a[0] = __fadd_rn(a[0], __uint_as_float(v.x << 16));
+    a[1] = __fadd_rn(a[1], __uint_as_float(v.x & 0xffff0000u));
+    a[2] = __fadd_rn(a[2], __uint_as_float(v.y << 16));
+    a[3] = __fadd_rn(a[3], __uint_as_float(v.y & 0xffff0000u));
+  }
+  __device__ uint2 out() const {
+    auto b = [](float f) { return uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(f))); };
+    return make_uint2(b(a[0]) | (b(a[1]) << 16), b(a[2]) | (b(a[3]) << 16));
+  }
+};
+template <>
+struct Acc8<4> {
+  float a[4];
+  __device__ static float h(uint32_t w, int hi) { return __half2float(__ushort_as_half(uint16_t(hi ? w >> 16 : w))); }
+  __device__ void init(uint2 v) { a[0] = h(v.x, 0), a[1] = h(v.x, 1), a[2] = h(v.y, 0), a[3] = h(v.y, 1); }
+  __device__ void add(uint2 v) {
+    a[0] = __fadd_rn(a[0], h(v.x, 0));
+    a[1] = __fadd_rn(a[1], h(v.x, 1));
+    a[2] = __fadd_rn(a[2], h(v.y, 0));
+    a[3] = __fadd_rn(a[3], h(v.y, 1));
+  }
+  __device__ uint2 out() const {
+    auto b = [](float f) { return uint32_t(__half_as_ushort(__float2half_rn(f))); };
+    return make_uint2(b(a[0]) | (b(a[1]) << 16), b(a[2]) | (b(a[3]) << 16));
+  }
+};
+
+__device__ __forceinline__ uint4 ld_ll(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_ll(void* p, uint2 d, uint32_t f) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(d.x), "r"(f), "r"(d.y), "r"(f)
+               : "memory");
+}
+
+// 8 data bytes of an LL slot at pair index; waits for the epoch flag of
+// every valid word
+template <bool SYS>
+__device__ uint2 ll_read(const char* slot, int64_t pair, bool two, uint32_t ef, const KParams& p, int rank, int ch,
+                         int op) {
+  const char* a = slot + pair * 16;
+  uint4 v = ld_ll(a);
+  if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  for (;;) {
+    v = ld_ll(a);
+    if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
+    if (++spins > 32) __nanosleep(20);
+    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+      volatile int* e = p.errinfo;
+      if (e && atomicCAS(p.errinfo, 0, -1) == 0) {
+        e[1] = rank;
+        e[2] = ch;
+        e[3] = op;
+        e[4] = -3;
+        e[5] = int(ef);
+        e[6] = int(v.y);
+        __threadfence_system();
+        e[0] = ERR_TIMEOUT;
+        __threadfence_system();
+      }
+      __trap();
+    }
+  }
+}
+
+// plain 8 bytes (n valid, rest zero)
+__device__ __forceinline__ uint2 ld_plain8(const char* a, int n, bool aligned) {
+  if (n == 8 && aligned) {
+    uint2 v;
+    asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a) : "memory");
+    return v;
+  }
+  uint32_t w[2] = {0, 0};
+  for (int i = 0; i < n; ++i) w[i >> 2] |= uint32_t(*(const volatile uint8_t*)(a + i)) << (8 * (i & 3));
+  return make_uint2(w[0], w[1]);
+}
+__device__ __forceinline__ void st_plain8(char* a, uint2 v, int n, bool aligned) {
+  if (n == 8 && aligned) {
+    asm volatile("st.volatile.global.v2.u32 [%0], {%1,%2};" ::"l"(a), "r"(v.x), "r"(v.y) : "memory");
+    return;
+  }
+  const uint32_t w[2] = {v.x, v.y};
+  for (int i = 0; i < n; ++i) *(volatile uint8_t*)(a + i) = uint8_t(w[i >> 2] >> (8 * (i & 3)));
+}
+
+template <int DT, bool SYS>
+__global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ KParams p) {
+  const int tid = threadIdx.x;
+  const int lr = blockIdx.x / p.nch, ch = blockIdx.x % p.nch;
+  const int cg = ch % p.kc, cb = ch / p.kc;
+  const int rank = p.rank0 + lr;
+  __shared__ uint64_t s_e;
+  __shared__ uint32_t s_entry_mask;
+  __shared__ const char* s_inp[kMaxOpIn];
+  __shared__ char* s_outp[kMaxOpOut];
+  __shared__ uint8_t s_inll[kMaxOpIn], s_outll[kMaxOpOut];
+  if (tid == 0) {
+    s_e = p.epochs[blockIdx.x] + 1;
+    s_entry_mask = 1u << rank;
+  }
+  __syncthreads();
+  const uint64_t e = s_e;
+  const uint32_t ef = uint32_t(e);
+  uint64_t* const myflags = reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]);
+  if (p.multiprocess)
+    for (int t = tid; t < p.P; t += LL_NT)
+      if (t != rank) {
+        fence_rel<SYS>();
+        st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[t][SP_FLAGS_IDX]) + p.entry_base + rank * p.nch + ch, e);
+      }
+
+  const uint32_t ob = p.prog[rank], oe = p.prog[rank + 1];
+  for (uint32_t oi = ob; oi < oe; ++oi) {
+    const DevOp op = p.ops[oi];
+    if (op.kind == 2) {  // receipts nobody forwards: consume them
+      for (int i = 0; i < op.nin; ++i) {
+        const DevIn in = p.ins[op.in_begin + i];
+        if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
+        const DPart q = dsplit16(int64_t(in.len), p.kb, cb);
+        const char* slot = p.base[in.rank][in.space] + in.off + 2 * q.off;
+        const int64_t npair = (q.len + 7) / 8;
+        for (int64_t k = tid; k < npair; k += LL_NT)
+          ll_read<SYS>(slot, k, q.len - 8 * k > 4, ef, p, rank, ch, int(oi - ob));
+      }
+      continue;
+    }
+    if (int(op.chunk % uint32_t(p.kc)) != cg) continue;
+    const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
+    if (q.len == 0) continue;
+    if (tid < op.nin) {
+      const DevIn in = p.ins[op.in_begin + tid];
+      s_inll[tid] = in.flag >= 0;
+      s_inp[tid] = p.base[in.rank][in.space] + in.off + (in.flag >= 0 ? 2 * q.off : q.off);
+    }
+    if (tid < op.nout) {
+      const DevOut d = p.outs[op.out_begin + tid];
+      s_outll[tid] = d.flag >= 0;
+      s_outp[tid] = p.base[d.rank][d.space] + d.off + (d.flag >= 0 ? 2 * q.off : q.off);
+      if (p.multiprocess && d.rank != rank && !(atomicOr(&s_entry_mask, 0u) & (1u << d.rank))) {
+        wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
+        atomicOr(&s_entry_mask, 1u << d.rank);
+      }
+    }
+    __syncthreads();
+    const int64_t npair = (q.len + 7) / 8;
+    for (int64_t k = tid; k < npair; k += LL_NT) {
+      const int n = int(min(int64_t(8), q.len - 8 * k));
+      const bool two = n > 4;
+      uint2 v = s_inll[0] ? ll_read<SYS>(s_inp[0], k, two, ef, p, rank, ch, int(oi - ob))
+                          : ld_plain8(s_inp[0] + 8 * k, n, op.vec);
+      if (op.kind == 1) {
+        Acc8<DT> acc;
+        acc.init(v);
+        for (int i = 1; i < op.nin; ++i)
+          acc.add(s_inll[i] ? ll_read<SYS>(s_inp[i], k, two, ef, p, rank, ch, int(oi - ob))
+                            : ld_plain8(s_inp[i] + 8 * k, n, op.vec));
+        v = acc.out();
+      }
+      for (int o = 0; o < op.nout; ++o) {
+        if (s_outll[o]) st_ll(s_outp[o] + 16 * k, v, ef);
+        else st_plain8(s_outp[o] + 8 * k, v, n, op.vec);
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) p.epochs[blockIdx.x] = e;
+}
+
+template <int DT>
+const void* kernel_ptr(bool sys, bool ll) {
+  if (ll)
+    return sys ? reinterpret_cast<const void*>(exec_ll_kernel<DT, true>)
+               : reinterpret_cast<const void*>(exec_ll_kernel<DT, false>);
   return sys ? reinterpret_cast<const void*>(exec_kernel<DT, true>) : reinterpret_cast<const void*>(exec_kernel<DT, false>);
 }
 
-const void* kernel_for(int dtype, bool sys) {
+const void* kernel_for(int dtype, bool sys, bool ll) {
   switch (dtype) {
-    case 0: return kernel_ptr<0>(sys);
-    case 1: return kernel_ptr<1>(sys);
-    case 2: return kernel_ptr<2>(sys);
-    case 3: return kernel_ptr<3>(sys);
-    case 4: return kernel_ptr<4>(sys);
+    case 0: return kernel_ptr<0>(sys, ll);
+    case 1: return kernel_ptr<1>(sys, ll);
+    case 2: return kernel_ptr<2>(sys, ll);
+    case 3: return kernel_ptr<3>(sys, ll);
+    case 4: return kernel_ptr<4>(sys, ll);
   }
   return nullptr;
 }
@@ -671,19 +892,22 @@ cudaError_t prepare(const void* f) {
 int exec_threads() { return NT; }
 
 cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st) {
-  const void* f = kernel_for(dtype, sys);
+  const void* f = kernel_for(dtype, sys, p.ll != 0);
   if (!f) return cudaErrorInvalidValue;
+  void* args[] = {const_cast<KParams*>(&p)};
+  if (p.ll) return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(LL_NT), args, 0, st);
   cudaError_t err = prepare(f);
   if (err != cudaSuccess) return err;
-  void* args[] = {const_cast<KParams*>(&p)};
   return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(NT), args, smem_bytes(p.tile), st);
 }
 
 size_t exec_smem_bytes(int tile) { return smem_bytes(tile); }
 
 cudaError_t exec_occupancy(int dtype, bool sys, int tile, int* blocks_per_sm) {
-  const void* f = kernel_for(dtype, sys);
+  // tile == 0: the LL kernel (no dynamic shared memory)
+  const void* f = kernel_for(dtype, sys, tile == 0);
   if (!f) return cudaErrorInvalidValue;
+  if (tile == 0) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, LL_NT, 0);
   cudaError_t err = prepare(f);
   if (err != cudaSuccess) return err;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, NT, smem_bytes(tile));

@@ -14,6 +14,9 @@ constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
 constexpr int kMaxTile = 32768; // one TMA pipeline stage
 constexpr int kStages = 6;      // pipeline depth
 constexpr int kThreads = 352;   // producer, storer and signaler warps + 8 compute warps
+constexpr int kLLThreads = 256; // LL kernel
+constexpr int64_t kLLMaxChunk = 16384;  // auto protocol: LL up to this chunk size
+constexpr int64_t kLLPart = 4096;       // LL: bytes of a chunk one CTA owns
 
 struct DevIn {
   uint64_t off;   // byte offset of the chunk start in (rank, space)
@@ -60,6 +63,7 @@ struct KParams {
   int entry_base;        // index of the entry-handshake flags in FLAGS
   int multiprocess;      // 1: peers are other processes (entry handshake)
   int send_readonly;     // 1: SEND does not alias RECV (non-coherent loads ok)
+  int ll;                // 1: low-latency protocol (receipts are LL slots)
 };
 
 }  // namespace sccl

@@ -126,6 +126,33 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
     return v;
   };
 
+  const uint32_t ef = uint32_t(e);
+  // LL word pair k of a slot: two 8-byte words (data | flag << 32)
+  auto ll_read = [&](const char* slot, int64_t k, bool two, char* out8) {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(slot + 16 * k);
+    uint64_t a, b = 0;
+    for (;;) {
+      a = __atomic_load_n(w, __ATOMIC_ACQUIRE);
+      if (two) b = __atomic_load_n(w + 1, __ATOMIC_ACQUIRE);
+      if (uint32_t(a >> 32) == ef && (!two || uint32_t(b >> 32) == ef)) break;
+      if (failed.load()) return;
+      if (std::chrono::steady_clock::now() > deadline) {
+        failed.store(1);
+        return;
+      }
+      std::this_thread::yield();
+    }
+    uint32_t d[2] = {uint32_t(a), uint32_t(b)};
+    std::memcpy(out8, d, 8);
+  };
+  auto ll_write = [&](char* slot, int64_t k, const char* in8) {
+    uint32_t d[2];
+    std::memcpy(d, in8, 8);
+    uint64_t* w = reinterpret_cast<uint64_t*>(slot + 16 * k);
+    __atomic_store_n(w, uint64_t(d[0]) | (uint64_t(ef) << 32), __ATOMIC_RELEASE);
+    __atomic_store_n(w + 1, uint64_t(d[1]) | (uint64_t(ef) << 32), __ATOMIC_RELEASE);
+  };
+
   auto run = [&](int rank, int ch) {
     const int cg = ch % kc, cb = ch / kc;  // same channel map as the kernel
     for (uint32_t oi = p->prog[rank]; oi < p->prog[rank + 1]; ++oi) {
@@ -135,27 +162,58 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
           const DevIn& in = p->ins[op.in_begin + i];
           if (int(in.chunk % uint32_t(kc)) != cg) continue;
           Part q = split16(int64_t(in.len), kb, cb);
-          if (q.len) wait_ge(flags[rank][size_t(in.flag) * nch + ch], e * uint64_t(q.len));
+          if (p->ll) {
+            char tmp[8];
+            for (int64_t k = 0; k < (q.len + 7) / 8; ++k)
+              ll_read(base(in.rank, in.space) + in.off + 2 * q.off, k, q.len - 8 * k > 4, tmp);
+          } else if (q.len) {
+            wait_ge(flags[rank][size_t(in.flag) * nch + ch], e * uint64_t(q.len));
+          }
         }
         continue;
       }
       if (int(op.chunk % uint32_t(kc)) != cg) continue;
       Part q = split16(int64_t(op.len), kb, cb);
       if (q.len == 0) continue;
-      // same tiling rule as the kernel: copy tiles of `tile`, reduce tiles
-      // of tile/nin; counters count bytes so the two sides may differ
-      const int64_t T = op.kind == OP_COPY ? tile : std::max<int64_t>(16, (tile / op.nin) & ~int64_t(15));
-      const int64_t ntiles = (q.len + T - 1) / T;
       std::vector<const char*> inp(op.nin);
       std::vector<char*> outp(op.nout);
       for (int i = 0; i < op.nin; ++i) {
         const DevIn& in = p->ins[op.in_begin + i];
-        inp[i] = base(in.rank, in.space) + in.off;
+        inp[i] = base(in.rank, in.space) + in.off + (p->ll && in.flag >= 0 ? 2 * q.off : q.off);
       }
       for (int o = 0; o < op.nout; ++o) {
         const DevOut& out = p->outs[op.out_begin + o];
-        outp[o] = base(out.rank, out.space) + out.off;
+        outp[o] = base(out.rank, out.space) + out.off + (p->ll && out.flag >= 0 ? 2 * q.off : q.off);
       }
+      if (p->ll) {  // LL: 8 data bytes at a time, flags in the data
+        const int dt = op.kind == OP_COPY ? 0 : p->dtype;
+        const int nin = op.kind == OP_COPY ? 1 : op.nin;
+        std::vector<char> ibuf(8 * size_t(nin));
+        std::vector<const char*> ip(nin);
+        char obuf[8];
+        char* op8[1] = {obuf};
+        for (int64_t k = 0; k < (q.len + 7) / 8; ++k) {
+          const int n = int(std::min<int64_t>(8, q.len - 8 * k));
+          for (int i = 0; i < nin; ++i) {
+            char* b8 = ibuf.data() + 8 * i;
+            std::memset(b8, 0, 8);
+            if (p->ins[op.in_begin + i].flag >= 0) ll_read(inp[i], k, n > 4, b8);
+            else std::memcpy(b8, inp[i] + 8 * k, n);
+            ip[i] = b8;
+          }
+          if (failed.load()) return;
+          elem_range(dt, ip.data(), nin, op8, 1, 0, 8);
+          for (int o = 0; o < op.nout; ++o) {
+            if (p->outs[op.out_begin + o].flag >= 0) ll_write(outp[o], k, obuf);
+            else std::memcpy(outp[o] + 8 * k, obuf, n);
+          }
+        }
+        continue;
+      }
+      // same tiling rule as the kernel: copy tiles of `tile`, reduce tiles
+      // of tile/nin; counters count bytes so the two sides may differ
+      const int64_t T = op.kind == OP_COPY ? tile : std::max<int64_t>(16, (tile / op.nin) & ~int64_t(15));
+      const int64_t ntiles = (q.len + T - 1) / T;
       const uint64_t b0 = (e - 1) * uint64_t(q.len);
       for (int64_t t = 0; t < ntiles; ++t) {
         const int64_t lo = t * T, nb = std::min<int64_t>(T, q.len - lo);
@@ -165,7 +223,7 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
         }
         if (failed.load()) return;
         elem_range(op.kind == OP_COPY ? 0 : p->dtype, inp.data(), op.kind == OP_COPY ? 1 : op.nin, outp.data(),
-                   op.nout, q.off + lo, nb);
+                   op.nout, lo, nb);
         bool last = t + 1 == ntiles;
         for (int o = 0; o < op.nout; ++o) {
           const DevOut& out = p->outs[op.out_begin + o];

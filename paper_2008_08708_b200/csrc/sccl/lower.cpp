@@ -31,8 +31,8 @@ struct Builder {
     return off;
   }
   int new_slot(int rank) { return pg.ranks[rank].nslots++; }
-  Loc out_loc(int c, int n) const { return {n, SP_RECV, pg.geo[c].out_off}; }
-  Loc in_loc(int c, int n) const { return {n, SP_SEND, pg.geo[c].in_off}; }
+  Loc out_loc(int c, int n) const { return {n, SP_RECV, pg.geo[c].out_off, c}; }
+  Loc in_loc(int c, int n) const { return {n, SP_SEND, pg.geo[c].in_off, c}; }
 
   void add_copy(int rank, int key, int c, const Cur& src, Loc dst, int slot) {
     Op op;
@@ -54,7 +54,7 @@ bool writes_loc(const Op& op, const Loc& L) {
 
 }  // namespace
 
-Program lower(const Schedule& s, int64_t nbytes, int esize) {
+Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
   auto viol = verify(s);
   if (!viol.empty())
     throw invalid_argument_error("executing an unverified schedule is rejected (SPEC.md:420): " + viol[0].str() +
@@ -70,6 +70,7 @@ Program lower(const Schedule& s, int64_t nbytes, int esize) {
     throw invalid_argument_error("alltoall needs bytes_per_rank divisible by P * element size");
 
   Program pg;
+  pg.ll = ll;
   pg.kind = s.kind;
   pg.P = P;
   pg.G = G;
@@ -116,8 +117,9 @@ Program lower(const Schedule& s, int64_t nbytes, int esize) {
           const Cur& src = b.cur[t.chunk * P + t.src];
           if (!src.valid) throw invalid_argument_error("internal: sender lacks chunk after verification");
           Loc dst;
-          if (last && fpost[t.chunk * P + t.dst]) dst = b.out_loc(t.chunk, t.dst);
-          else dst = {t.dst, SP_SCRATCH, b.scratch_alloc(t.dst, pg.geo[t.chunk].len)};
+          const int64_t len = pg.geo[t.chunk].len;
+          if (!ll && last && fpost[t.chunk * P + t.dst]) dst = b.out_loc(t.chunk, t.dst);
+          else dst = {t.dst, SP_SCRATCH, b.scratch_alloc(t.dst, ll ? ll_bytes(len) : len), t.chunk};
           int slot = b.new_slot(t.dst);
           b.add_copy(t.src, 2 * (step_base + st), t.chunk, src, dst, slot);
           upd.push_back({t.chunk, t.dst, dst, slot});
@@ -135,7 +137,8 @@ Program lower(const Schedule& s, int64_t nbytes, int esize) {
           if (t.step != st) continue;
           const Cur& src = b.cur[t.chunk * P + t.src];
           if (!src.valid) throw invalid_argument_error("internal: sender holds no contribution after verification");
-          Loc dst{t.dst, SP_SCRATCH, b.scratch_alloc(t.dst, pg.geo[t.chunk].len)};
+          const int64_t len = pg.geo[t.chunk].len;
+          Loc dst{t.dst, SP_SCRATCH, b.scratch_alloc(t.dst, ll ? ll_bytes(len) : len), t.chunk};
           int slot = b.new_slot(t.dst);
           b.add_copy(t.src, 2 * (step_base + st), t.chunk, src, dst, slot);
           recv[{t.dst, t.chunk}].push_back({t.src, slot, dst});
@@ -158,7 +161,7 @@ Program lower(const Schedule& s, int64_t nbytes, int esize) {
           } else {
             int64_t& off = acc_scratch_off[c * P + n];
             if (off < 0) off = b.scratch_alloc(n, op.len);
-            acc = {n, SP_SCRATCH, off};
+            acc = {n, SP_SCRATCH, off, c};
           }
           op.outs.push_back({acc, -1, false});
           pg.ranks[n].ops.push_back(std::move(op));
@@ -270,7 +273,7 @@ Program lower(const Schedule& s, int64_t nbytes, int esize) {
     pg.scratch_bytes = std::max(pg.scratch_bytes, rp.scratch_bytes);
   }
   // fingerprint: every rank must lower the identical program
-  std::string text = serialize(s) + "|" + std::to_string(nbytes) + "|" + std::to_string(esize);
+  std::string text = serialize(s) + "|" + std::to_string(nbytes) + "|" + std::to_string(esize) + (ll ? "|ll" : "");
   uint64_t h = 0xcbf29ce484222325ull;
   for (unsigned char ch : text) {
     h ^= ch;
@@ -286,7 +289,8 @@ std::string Program::summary_json() const {
   std::ostringstream o;
   o << "{\"collective\":\"" << kind_name(kind) << "\",\"P\":" << P << ",\"G\":" << G << ",\"bytes\":" << nbytes
     << ",\"send_bytes\":" << send_bytes << ",\"recv_bytes\":" << recv_bytes << ",\"max_slots\":" << max_slots
-    << ",\"scratch_bytes\":" << scratch_bytes << ",\"fingerprint\":\"" << fingerprint << "\",\"ranks\":[";
+    << ",\"scratch_bytes\":" << scratch_bytes << ",\"protocol\":\"" << (ll ? "ll" : "simple")
+    << "\",\"fingerprint\":\"" << fingerprint << "\",\"ranks\":[";
   static const char* sp[] = {"send", "recv", "scratch", "flags"};
   for (int r = 0; r < P; ++r) {
     o << (r ? "," : "") << "{\"nslots\":" << ranks[r].nslots << ",\"ops\":[";

@@ -28,7 +28,10 @@ enum Space : int { SP_SEND = 0, SP_RECV = 1, SP_SCRATCH = 2, SP_FLAGS = 3, NSPAC
 struct Loc {
   int rank = -1, space = -1;
   int64_t off = 0;
-  bool operator==(const Loc& o) const { return rank == o.rank && space == o.space && off == o.off; }
+  int chunk = -1;  // owner chunk: zero-length chunks share offsets, so identity includes it
+  bool operator==(const Loc& o) const {
+    return rank == o.rank && space == o.space && off == o.off && chunk == o.chunk;
+  }
 };
 
 struct OpIn {
@@ -71,13 +74,20 @@ struct Program {
   std::vector<RankProgram> ranks;
   int max_slots = 0;
   int64_t scratch_bytes = 0;  // symmetric per-rank scratch size
-  std::string fingerprint;    // hash of (canonical schedule, sizes, dtype)
+  bool ll = false;            // low-latency protocol: every receipt is an LL slot in scratch
+  std::string fingerprint;    // hash of (canonical schedule, sizes, dtype, protocol)
 
   std::string summary_json() const;
 };
 
 // Throws invalid_argument_error for unverified schedules or
-// inconsistent sizes.
-Program lower(const Schedule& s, int64_t nbytes, int esize);
+// inconsistent sizes.  ll = low-latency protocol: every receipt lands in a
+// scratch slot encoded as (4 data bytes, 4 flag bytes) words (2x the chunk),
+// so the receiver polls the data itself; post entries then get a local
+// unpacking copy, fused with the forward of the same receipt.
+Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll = false);
+
+// bytes of an LL slot for a chunk of len bytes
+inline int64_t ll_bytes(int64_t len) { return 2 * ((len + 15) / 16 * 16); }
 
 }  // namespace sccl

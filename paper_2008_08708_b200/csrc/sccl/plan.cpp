@@ -9,6 +9,7 @@
 
 #include "../../../include/sccl_exec.h"
 #include "error.hpp"
+#include "layout.hpp"
 
 namespace sccl {
 cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st);
@@ -88,7 +89,17 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     if (nranks != p.sched.P) throw invalid_argument_error("nranks != schedule P");
     if (rank < 0 || rank >= nranks) throw invalid_argument_error("rank out of range");
   }
-  p.pg = lower(p.sched, bytes, es);
+  // protocol: LL (flag-in-data, no fences, 2x bytes) for small chunks,
+  // pipelined TMA bulk copies with counter flags otherwise
+  int64_t maxlen = 0;
+  {
+    const auto phases = p.sched.flat();
+    for (auto& g : chunk_geometry(p.sched.kind, p.sched.P, phases.back()->G, bytes)) maxlen = std::max(maxlen, g.len);
+  }
+  bool ll = req.protocol == 2 || (req.protocol == 0 && maxlen <= kLLMaxChunk);
+  if (req.protocol < 0 || req.protocol > 2) throw invalid_argument_error("protocol must be 0 (auto), 1 (simple), 2 (ll)");
+  p.pg = lower(p.sched, bytes, es, ll);
+  p.ll = ll;
   p.rank = loopback ? 0 : rank;
   p.nranks = p.sched.P;
   p.loopback = loopback;
@@ -103,8 +114,6 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   // into byte parts so every SM streams; small chunks are spread over chunk
   // groups so independent chunks travel in parallel instead of queueing
   // behind each other in one CTA (latency).
-  int64_t maxlen = 0;
-  for (auto& g : p.pg.geo) maxlen = std::max(maxlen, g.len);
   const int G = p.pg.G;
   int tile = req.tile;
   if (tile <= 0) {
@@ -116,16 +125,18 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   }
   if (tile % 16 || tile > kMaxTile || tile < 256)
     throw invalid_argument_error("tile_bytes must be a multiple of 16 in [256, 32768]");
-  int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, tile)
-                              : std::max(1, std::min(2048 / kThreads, int((227 << 10) / (kStages * tile + 256))));
+  int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, ll ? 0 : tile)
+            : ll ? 2048 / kLLThreads
+                 : std::max(1, std::min(2048 / kThreads, int((227 << 10) / (kStages * tile + 2048))));
   const int resident = std::max(1, req.sms * std::max(1, bps));
   const int cap = loopback ? std::max(1, resident / p.sched.P) : 32;
+  const int64_t part = ll ? kLLPart : kMaxTile;  // bytes one CTA should own per chunk
   int kb, kc;
   if (req.nchannels > 0) {
     kb = req.nchannels;
     kc = req.chunk_groups > 0 ? req.chunk_groups : 1;
   } else {
-    kb = int(std::max<int64_t>(1, std::min<int64_t>(cap, (maxlen + kMaxTile - 1) / kMaxTile)));
+    kb = int(std::max<int64_t>(1, std::min<int64_t>(cap, (maxlen + part - 1) / part)));
     kc = req.chunk_groups > 0 ? req.chunk_groups : std::max(1, std::min(G, cap / kb));
   }
   if (kc < 1 || kb < 1) throw invalid_argument_error("channels must be positive");
@@ -133,7 +144,7 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   p.kb = kb;
   p.nch = kc * kb;
   p.tile = tile;
-  // small tiles: signal every tile at once (latency); large: keep 3 bulk
+  // small tiles: retire every bulk group at once (latency); large: keep 6
   // groups in flight (bandwidth; FIFO depth 8 in the kernel)
   p.sig_lag = tile >= 16384 ? 6 : 0;
   p.resident_cap = loopback ? resident : 0;
@@ -267,6 +278,7 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.kb = p.kb;
   k.tile = p.tile;
   k.sig_lag = p.sig_lag;
+  k.ll = p.ll ? 1 : 0;
   k.entry_base = p.entry_base;
 }
 
@@ -280,6 +292,7 @@ void sccl_plan_opts_init(sccl_plan_opts* o) {
   o->nchannels = 0;
   o->chunk_groups = 0;
   o->tile_bytes = 0;
+  o->protocol = 0;
   o->timeout_ms = 0;
 }
 
@@ -340,6 +353,7 @@ static int create_common(const char* json, int rank, int nranks, size_t bytes, i
       req.nchannels = o.nchannels;
       req.chunk_groups = o.chunk_groups;
       req.tile = o.tile_bytes;
+      req.protocol = o.protocol;
       OccCtx occ{dtype, !loopback};
       if (o.device >= 0) {
         cudaDeviceProp prop{};
@@ -522,7 +536,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"sig_lag\":" << p->sig_lag << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"sig_lag\":" << p->sig_lag << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

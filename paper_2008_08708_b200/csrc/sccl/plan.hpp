@@ -19,6 +19,7 @@ struct sccl_plan {
   int device = -1, dtype = 0, redop = 0;
   int nch = 1, kc = 1, kb = 1, tile = 32768, sig_lag = 3;
   int resident_cap = 0;  // loopback: CTAs that fit on the device at once
+  bool ll = false;       // low-latency protocol
   long long timeout_ns = 0;
 
   // host copy of the device program (also used by the CPU interpreter)
@@ -53,7 +54,7 @@ namespace sccl {
 // Channel policy inputs: user overrides (0 = auto) and the resident-CTA
 // capacity per SM as a function of the tile (shared-memory stage) size.
 struct ChannelRequest {
-  int nchannels = 0, chunk_groups = 0, tile = 0;
+  int nchannels = 0, chunk_groups = 0, tile = 0, protocol = 0;
   int sms = 148;
   int (*blocks_per_sm)(void* ctx, int tile) = nullptr;
   void* ctx = nullptr;

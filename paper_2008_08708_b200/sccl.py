@@ -40,7 +40,7 @@ class PeerTimeoutError(SCCLError):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("nchannels", ctypes.c_int), ("chunk_groups", ctypes.c_int),
-                ("tile_bytes", ctypes.c_int), ("timeout_ms", ctypes.c_int64)]
+                ("tile_bytes", ctypes.c_int), ("protocol", ctypes.c_int), ("timeout_ms", ctypes.c_int64)]
 
 
 _lib = None
@@ -142,8 +142,12 @@ def version() -> str:
 
 
 # ---------------------------------------------------------------- plans
-def _opts(device: int, nchannels: int, tile_bytes: int, timeout_ms: int, chunk_groups: int = 0) -> _Opts:
-    return _Opts(device, nchannels, chunk_groups, tile_bytes, timeout_ms)
+PROTOCOLS = {"auto": 0, "simple": 1, "ll": 2}
+
+
+def _opts(device: int, nchannels: int, tile_bytes: int, timeout_ms: int, chunk_groups: int = 0,
+          protocol: str = "auto") -> _Opts:
+    return _Opts(device, nchannels, chunk_groups, tile_bytes, PROTOCOLS[protocol], timeout_ms)
 
 
 def _ptr(x) -> int:
@@ -194,9 +198,10 @@ class LoopbackPlan(_PlanBase):
     """Every rank of the schedule on one GPU; one launch runs them all."""
 
     def __init__(self, schedule, bytes_per_rank: int, dtype: int = U8, device: int = 0,
-                 nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0, chunk_groups: int = 0):
+                 nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0, chunk_groups: int = 0,
+                 protocol: str = "auto"):
         super().__init__()
-        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups)
+        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol)
         rc = lib().sccl_plan_create_loopback(_text(schedule), bytes_per_rank, dtype, SUM,
                                              ctypes.byref(o), ctypes.byref(self._h))
         _raise(rc)
@@ -227,9 +232,9 @@ class Plan(_PlanBase):
 
     def __init__(self, schedule, rank: int, nranks: int, bytes_per_rank: int, dtype: int = U8,
                  device: int = 0, nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0,
-                 chunk_groups: int = 0):
+                 chunk_groups: int = 0, protocol: str = "auto"):
         super().__init__()
-        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups)
+        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol)
         rc = lib().sccl_plan_create(_text(schedule), rank, nranks, bytes_per_rank, dtype, SUM,
                                     ctypes.byref(o), ctypes.byref(self._h))
         _raise(rc)

@@ -51,10 +51,11 @@ def _schedules():
 SCHED = _schedules()
 
 
-def run_gpu(js, nbytes, dtype, seed=3, mode="random", nch=0, tile=0, repeats=1):
+def run_gpu(js, nbytes, dtype, seed=3, mode="random", nch=0, tile=0, repeats=1, protocol="auto", kc=0):
     d = json.loads(js)
     kind, P = d["collective"], d["P"]
-    plan = sccl.LoopbackPlan(js, nbytes, dtype, device=0, nchannels=nch, tile_bytes=tile)
+    plan = sccl.LoopbackPlan(js, nbytes, dtype, device=0, nchannels=nch, tile_bytes=tile, protocol=protocol,
+                             chunk_groups=kc)
     try:
         for it in range(repeats):
             ins = O.seeded_inputs(kind, P, nbytes, dtype, seed + it, mode)
@@ -205,3 +206,24 @@ def test_unverified_schedule_rejected_on_gpu():
     d["sends"] = d["sends"][1:]
     with pytest.raises(sccl.InvalidArgumentError):
         sccl.LoopbackPlan(d, 4096, O.U8, device=0)
+
+
+@pytest.mark.parametrize("protocol", ["ll", "simple"])
+@pytest.mark.parametrize("name", sorted(SCHED))
+def test_both_protocols(name, protocol):
+    """LL (flag-in-data) and simple (TMA bulk + counters) on the same cases."""
+    js = SCHED[name]
+    kind = json.loads(js)["collective"]
+    dts = [O.U8] if kind not in ("reduce", "reducescatter", "allreduce") else [O.BF16, O.F32, O.I32]
+    for nbytes in (8, 4096 + 48, 40000):
+        for dt in dts:
+            if nbytes % O.ESIZE[dt] or (kind == "alltoall" and nbytes % (json.loads(js)["P"] * O.ESIZE[dt])):
+                continue
+            run_gpu(js, nbytes, dt, protocol=protocol, repeats=2)
+
+
+@pytest.mark.parametrize("kc,kb", [(3, 2), (56, 1), (7, 3)])
+def test_chunk_groups_gpu(kc, kb):
+    run_gpu(SCHED["ag_777"], 3 * 65536 + 1024, O.U8, nch=kb, kc=kc)
+    run_gpu(SCHED["ar_56_14_14"], 3 * 65536 + 1024, O.BF16, nch=kb, kc=kc)
+    run_gpu(SCHED["ar_56_14_14"], 24000, O.BF16, nch=kb, kc=kc, protocol="ll", repeats=3)
