@@ -190,11 +190,17 @@ def run_loopback(args):
     want = torch.cat(send)
     assert all(torch.equal(r, want) for r in recv), "bench: allgather result wrong"
 
-    n0 = plan.launch_count
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_all = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
+        # untimed soak under the sampler so the clock record sees this load
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < 0.6:
+            for _ in range(8):
+                plan.launch(send, recv, stream)
+            stream.synchronize()
+        n0 = plan.launch_count
         t_all[0].record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
@@ -221,26 +227,52 @@ def run_loopback(args):
         except Exception:
             traffic = None
 
-    # latency sweep (small/medium sizes) and the one-shot schedule at full size
+    def time_us(p2, s2, r2, iters):
+        for _ in range(3):
+            p2.launch(s2, r2, stream)
+        stream.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(iters):
+            p2.launch(s2, r2, stream)
+        b.record(stream)
+        stream.synchronize()
+        p2.check()
+        return a.elapsed_time(b) * 1e3 / iters
+
+    # latency sweep: the (7,7,7) schedule and the one-shot (1,1,1) per size
+    from paper_2008_08708_b200 import schedules as S
     sweep = []
     if not args.no_sweep:
-        for sz in (1 << 10, 64 << 10, 1 << 20, 16 << 20):
-            p2 = sccl.LoopbackPlan(js, sz, sccl.U8, device=0)
-            s2 = [x[:sz] for x in send]
-            r2 = [x[:P * sz] for x in recv]
-            for _ in range(5):
-                p2.launch(s2, r2, stream)
-            stream.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            it = 50
-            a.record(stream)
-            for _ in range(it):
-                p2.launch(s2, r2, stream)
-            b.record(stream)
-            stream.synchronize()
-            us = a.elapsed_time(b) * 1e3 / it
-            sweep.append({"bytes_per_rank": sz, "us": round(us, 2),
-                          "busbw_per_rank_GBps": round((P - 1) * sz / (us * 1e-6) / 1e9, 2)})
+        one = S.to_json(S.one_shot_allgather(P))
+        for sz in (1 << 10, 8 << 10, 64 << 10, 1 << 20, 16 << 20):
+            row = {"bytes_per_rank": sz}
+            for tag, sj in (("777", js), ("oneshot", one)):
+                p2 = sccl.LoopbackPlan(sj, sz, sccl.U8, device=0)
+                us = time_us(p2, [x[:sz] for x in send], [x[:P * sz] for x in recv], 50 if sz < (1 << 20) else 10)
+                row[f"{tag}_us"] = round(us, 2)
+                row[f"{tag}_busbw_per_rank_GBps"] = round((P - 1) * sz / (us * 1e-6) / 1e9, 2)
+                row[f"{tag}_protocol"] = p2.info()["protocol"]
+                p2.close()
+            sweep.append(row)
+
+    # BASELINE configs 3 and 4 on the same device (loopback, 64 MiB per rank)
+    extra = {}
+    if not args.no_sweep:
+        M = 64 << 20
+        xs = [x[:M] for x in send]
+        ys = [x[:M] for x in recv]
+        ag = S.hamiltonian_allgather(P)
+        for tag, sj, dt in (("allreduce_56_14_14_bf16", S.allreduce_from(ag), sccl.BF16),
+                            ("allreduce_8_2_2_bf16", S.allreduce_from(S.one_shot_allgather(P)), sccl.BF16),
+                            ("alltoall_8_1_1_u8", S.to_json(S.direct_alltoall(P)), sccl.U8)):
+            p2 = sccl.LoopbackPlan(sj, M, dt, device=0)
+            us = time_us(p2, xs, ys, 10)
+            busb = (2 * (P - 1) * M // P) if tag.startswith("allreduce") else ((P - 1) * M // P)
+            extra[tag] = {"bytes_per_rank": M, "us": round(us, 1),
+                          "busbw_per_rank_GBps": round(busb / (us * 1e-6) / 1e9, 1),
+                          "hbm_GBps": round(hbm_bytes_per_launch(p2) / (us * 1e-6) / 1e9, 1),
+                          "hbm_frac": round(hbm_bytes_per_launch(p2) / (us * 1e-6) / 1e9 / _peaks()[0]["hbm_gbs"], 3)}
             p2.close()
 
     # e2e: through the public API with host buffers (pinned) both ways
@@ -297,6 +329,7 @@ def run_loopback(args):
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "latency_sweep": sweep,
+        "other_collectives": extra,
     }
     print(json.dumps(line), flush=True)
 
