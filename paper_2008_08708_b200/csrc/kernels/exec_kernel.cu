@@ -329,6 +329,7 @@ struct Smem {
   SigEntry q[SIGQ];                 // completed tiles whose counters must be released
   uint32_t q_head, q_tail, q_done;  // storer pushes, signaler pops (release/acquire, cta)
   volatile uint32_t completed_seq;  // storer: tiles < completed_seq fully written
+  volatile uint32_t producer_blocked;  // producer spins on a peer's counter
   uint32_t entry_mask;
 };
 static_assert(sizeof(Smem) <= SMEM_HDR, "smem header");
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KPa
     }
     S.completed_seq = 0;
     S.q_head = S.q_tail = S.q_done = 0;
+    S.producer_blocked = 0;
     S.entry_mask = 1u << rank;
     s_e = p.epochs[blockIdx.x] + 1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -490,8 +492,15 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KPa
         const uint32_t nv = n & ~15u;
         if (flag >= 0) {
           const uint64_t need = fbase + lo + n;
-          if (ready < need) ready = wait_ge<SYS>(myflags + uint64_t(flag) * p.nch + ch, need, p, rank, ch, int(oi - ob), flag);
+          const uint64_t* f = myflags + uint64_t(flag) * p.nch + ch;
+          if (ready < need) ready = ld_acquire<SYS>(f);
+          if (ready < need) {  // a peer is behind: let the storer publish what it holds
+            S.producer_blocked = 1;
+            ready = wait_ge<SYS>(f, need, p, rank, ch, int(oi - ob), flag);
+          }
         }
+        __syncwarp();
+        if (lane == 0) S.producer_blocked = 0;
         __syncwarp();
         if (lane == 0) {
           mbar_wait(&S.empty[s], ph ^ 1);
@@ -549,7 +558,8 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KPa
             // pending tiles -- retire and signal everything before blocking.
             const uint64_t t0 = globaltimer();
             bool ok = false;
-            while (!(ok = mbar_try(&S.ready[s], ph)) && globaltimer() - t0 < kStorerPatienceNs) {
+            while (!(ok = mbar_try(&S.ready[s], ph)) && !S.producer_blocked &&
+                   globaltimer() - t0 < kStorerPatienceNs) {
             }
             if (!ok) {
               drain();

@@ -222,8 +222,15 @@ def test_both_protocols(name, protocol):
             run_gpu(js, nbytes, dt, protocol=protocol, repeats=2)
 
 
-@pytest.mark.parametrize("kc,kb", [(3, 2), (56, 1), (7, 3)])
+@pytest.mark.parametrize("kc,kb", [(3, 2), (7, 2)])
 def test_chunk_groups_gpu(kc, kb):
     run_gpu(SCHED["ag_777"], 3 * 65536 + 1024, O.U8, nch=kb, kc=kc)
     run_gpu(SCHED["ar_56_14_14"], 3 * 65536 + 1024, O.BF16, nch=kb, kc=kc)
     run_gpu(SCHED["ar_56_14_14"], 24000, O.BF16, nch=kb, kc=kc, protocol="ll", repeats=3)
+
+
+def test_many_chunk_groups_small():
+    """one CTA per chunk (56 chunk groups x 8 ranks = 448 CTAs, small tiles)"""
+    run_gpu(SCHED["ag_777"], 20000, O.U8, nch=1, kc=56, protocol="simple", repeats=2)
+    run_gpu(SCHED["ar_56_14_14"], 20000, O.F32, nch=1, kc=56, protocol="simple", repeats=2)
+    run_gpu(SCHED["ag_777"], 20000, O.U8, nch=1, kc=56, protocol="ll", repeats=2)
