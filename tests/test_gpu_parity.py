@@ -234,3 +234,17 @@ def test_many_chunk_groups_small():
     run_gpu(SCHED["ag_777"], 20000, O.U8, nch=1, kc=56, protocol="simple", repeats=2)
     run_gpu(SCHED["ar_56_14_14"], 20000, O.F32, nch=1, kc=56, protocol="simple", repeats=2)
     run_gpu(SCHED["ag_777"], 20000, O.U8, nch=1, kc=56, protocol="ll", repeats=2)
+
+
+SYN = sorted(__import__("glob").glob(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden",
+                                                                     "schedules", "*.json")))
+
+
+@pytest.mark.parametrize("path", SYN, ids=[p.split("/")[-1][:-5] for p in SYN])
+@pytest.mark.parametrize("protocol", ["ll", "simple"])
+def test_synthesized_schedules_gpu(path, protocol):
+    js = open(path).read().strip()
+    kind = json.loads(js)["collective"]
+    for nb in (8 * 1000, 8 * 65536 + 64):
+        for dt in ([O.BF16, O.I32] if kind == "allreduce" else [O.U8]):
+            run_gpu(js, nb, dt, protocol=protocol)

@@ -1,0 +1,74 @@
+"""Schedules produced by the SMT synthesizer (tools/make_synth_schedules.py,
+committed as files: models are not unique) run through the
+host verifier, the oracle, and the lowering interpreter."""
+import glob
+import json
+import os
+import shutil
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2008_08708_b200 import sccl
+
+FILES = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "schedules", "*.json")))
+NAMES = [os.path.basename(f)[:-5] for f in FILES]
+
+
+def _load(name):
+    return open(os.path.join(os.path.dirname(__file__), "golden", "schedules", name + ".json")).read().strip()
+
+
+def test_files_present():
+    assert len(FILES) >= 9
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_canonical_and_verified(name):
+    js = _load(name)
+    assert sccl.canonicalize(js) == js
+    assert sccl.verify(js) == []
+    assert O.verify(json.loads(js)) == []
+
+
+def test_table4_allreduce_tuples():
+    """SPEC.md:360 / Table 4: DGX-1 AG (1,2,2) -> AR (8,4,4); (2,2,3) -> (16,4,6)."""
+    a = json.loads(_load("ar_from_dgx1_1_2_2"))
+    b = json.loads(_load("ar_from_dgx1_2_2_3"))
+    assert (a["C"], a["S"], a["R"]) == (8, 4, 4)
+    assert (b["C"], b["S"], b["R"]) == (16, 4, 6)
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("protocol", ["ll", "simple"])
+def test_interpreter_on_synthesized(name, protocol):
+    js = _load(name)
+    d = json.loads(js)
+    kind = d["collective"]
+    dt = O.I32 if kind == "allreduce" else O.U8
+    nb = 8 * 1000
+    ins = O.seeded_inputs(kind, d["P"], nb, dt, 13)
+    ref = O.execute(d, ins, nb, dt)
+    p = sccl.LoopbackPlan(js, nb, dt, device=-1, protocol=protocol, tile_bytes=256 if protocol == "simple" else 0)
+    outs = [np.zeros_like(r) for r in ref]
+    p.interpret_on_cpu(ins, outs)
+    for a, b in zip(outs, ref):
+        assert np.array_equal(a, b)
+    if kind == "allreduce":  # exact integer sums (acceptance :641)
+        want = np.sum([x.view(np.int32).astype(np.int64) for x in ins], axis=0).astype(np.int32)
+        assert all(np.array_equal(o.view(np.int32), want) for o in ref)
+
+
+@pytest.mark.skipif(shutil.which(os.environ.get("SCCL_SOLVER", "z3")) is None, reason="no SMT solver")
+def test_synth_small_instances():
+    """Encoding C1-C6 + solver driver: ring(4) needs 2
+    steps (diameter); (1,2,2) on DGX-1 is SAT (Table 4 row 1)."""
+    from paper_2008_08708_b200 import synth
+    assert synth.synthesize("allgather", "ring:4", 1, 1, 1)[0] == "unsat"
+    st, js, _ = synth.synthesize("allgather", "ring:4", 1, 2, 2)
+    assert st == "sat" and sccl.verify(js) == []
+    st, js, _ = synth.synthesize("allgather", "dgx1", 1, 2, 2)
+    assert st == "sat" and json.loads(js)["S"] == 2
+    st, js, _ = synth.synthesize("broadcast", "ring:4", 2, 3, 3, root=0)
+    assert st == "sat" and sccl.verify(js) == []
