@@ -43,11 +43,11 @@ static_assert(NT == (3 + NCW) * 32, "thread layout");
 constexpr int CW0 = 3;               // first compute warp
 constexpr int NPART = NT - 32;       // threads of the unaligned path (all but the signaler)
 constexpr int SIGQ = 64;             // storer -> signaler queue entries
-constexpr int NSTAGE = kStages;      // stage size = KParams::tile (runtime)
+constexpr int NSTAGE = kMaxStages;   // barrier sets; stages in use = KParams::nstage
 constexpr int FIFO = 8;              // storer's in-flight tile records (> max sig_lag)
 constexpr uint64_t kStorerPatienceNs = 3000;  // storer spins this long before draining
 constexpr size_t SMEM_HDR = 2048;    // mbarriers, signal queue, control words, ahead of the stages
-__host__ __device__ constexpr size_t smem_bytes(int tile) { return SMEM_HDR + size_t(NSTAGE) * tile; }
+__host__ __device__ constexpr size_t smem_bytes(int tile, int nstage) { return SMEM_HDR + size_t(nstage) * tile; }
 
 struct DPart {
   int64_t off, len;
@@ -335,11 +335,12 @@ struct Smem {
 static_assert(sizeof(Smem) <= SMEM_HDR, "smem header");
 
 template <int DT, bool SYS>
-__global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   uint8_t* const bufs = smem_raw + SMEM_HDR;
   const size_t STAGE = size_t(p.tile);
+  const uint32_t NST = uint32_t(p.nstage);
   __shared__ const char* s_inp[kMaxOpIn];
   __shared__ char* s_outp[kMaxOpOut];
   __shared__ uint64_t* s_sig[kMaxOpOut];
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KPa
   uint64_t* const myflags = reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]);
 
   if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) {
+    for (int s = 0; s < p.nstage; ++s) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.ready[s], NCW);
       mbar_init(&S.empty[s], 1);
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KPa
         while (S.completed_seq < seq) __nanosleep(32);
       __syncwarp();
       for (uint32_t t = 0; t < ntiles; ++t, ++it) {
-        const uint32_t s = it % NSTAGE, ph = (it / NSTAGE) & 1;
+        const uint32_t s = it % NST, ph = (it / NST) & 1;
         const uint64_t lo = uint64_t(t) * T;
         const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
         const uint32_t nv = n & ~15u;
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KPa
     } else if (warp >= CW0) {
       // ================= compute (REDUCE only; others just pass) =================
       for (uint32_t t = 0; t < ntiles; ++t, ++it) {
-        const uint32_t s = it % NSTAGE, ph = (it / NSTAGE) & 1;
+        const uint32_t s = it % NST, ph = (it / NST) & 1;
         mbar_wait(&S.full[s], ph);
         if (op.kind == 1) {
           const uint64_t lo = uint64_t(t) * T;
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(const __grid_constant__ KPa
           }
         }
         for (uint32_t t = 0; t < ntiles; ++t, ++it, ++seq) {
-          const uint32_t s = it % NSTAGE, ph = (it / NSTAGE) & 1;
+          const uint32_t s = it % NST, ph = (it / NST) & 1;
           const uint64_t lo = uint64_t(t) * T;
           const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
           const uint32_t nv = n & ~15u;
@@ -887,7 +888,7 @@ cudaError_t prepare(const void* f) {
   static const void* done[16] = {};
   for (auto& d : done)
     if (d == f) return cudaSuccess;
-  cudaError_t err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes(kMaxTile)));
+  cudaError_t err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_HDR + kStageBudget));
   if (err == cudaSuccess)
     for (auto& d : done)
       if (!d) {
@@ -908,19 +909,19 @@ cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st) 
   if (p.ll) return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(LL_NT), args, 0, st);
   cudaError_t err = prepare(f);
   if (err != cudaSuccess) return err;
-  return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(NT), args, smem_bytes(p.tile), st);
+  return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(NT), args, smem_bytes(p.tile, p.nstage), st);
 }
 
-size_t exec_smem_bytes(int tile) { return smem_bytes(tile); }
+size_t exec_smem_bytes(int tile, int nstage) { return smem_bytes(tile, nstage); }
 
-cudaError_t exec_occupancy(int dtype, bool sys, int tile, int* blocks_per_sm) {
+cudaError_t exec_occupancy(int dtype, bool sys, int tile, int nstage, int* blocks_per_sm) {
   // tile == 0: the LL kernel (no dynamic shared memory)
   const void* f = kernel_for(dtype, sys, tile == 0);
   if (!f) return cudaErrorInvalidValue;
   if (tile == 0) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, LL_NT, 0);
   cudaError_t err = prepare(f);
   if (err != cudaSuccess) return err;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, NT, smem_bytes(tile));
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, NT, smem_bytes(tile, nstage));
 }
 
 }  // namespace sccl

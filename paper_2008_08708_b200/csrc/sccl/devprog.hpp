@@ -11,8 +11,9 @@ constexpr int kMaxRanks = 16;   // pointer table width (kernel parameter space)
 constexpr int kMaxOpIn = 32;    // inputs of one copy/reduce op (staged in smem)
 constexpr int kMaxOpOut = 32;   // destinations of one op
 constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
-constexpr int kMaxTile = 32768; // one TMA pipeline stage
-constexpr int kStages = 6;      // pipeline depth
+constexpr int kMaxTile = 65536; // one TMA pipeline stage (bytes)
+constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
+constexpr int kStageBudget = 196608;  // bytes of stages per CTA (nstage * tile)
 constexpr int kThreads = 352;   // producer, storer and signaler warps + 8 compute warps
 constexpr int kLLThreads = 256; // LL kernel
 constexpr int64_t kLLMaxChunk = 16384;  // auto protocol: LL up to this chunk size
@@ -59,6 +60,7 @@ struct KParams {
   int P, nch, rank0, nranks_launch;
   int kc, kb;            // nch = kc * kb: chunk groups x byte parts per chunk
   int tile;              // copy tile = pipeline stage bytes (<= kMaxTile); reduce tiles tile/nin
+  int nstage;            // pipeline stages (<= kMaxStages)
   int sig_lag;           // bulk groups the storer keeps in flight before retiring (0..6)
   int entry_base;        // index of the entry-handshake flags in FLAGS
   int multiprocess;      // 1: peers are other processes (entry handshake)

@@ -13,7 +13,7 @@
 
 namespace sccl {
 cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st);
-cudaError_t exec_occupancy(int dtype, bool sys, int tile, int* blocks_per_sm);
+cudaError_t exec_occupancy(int dtype, bool sys, int tile, int nstage, int* blocks_per_sm);
 int exec_threads();
 }  // namespace sccl
 
@@ -115,22 +115,32 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   // groups so independent chunks travel in parallel instead of queueing
   // behind each other in one CTA (latency).
   const int G = p.pg.G;
+  int max_fanin = 1;
+  for (auto& rp : p.pg.ranks)
+    for (auto& op : rp.ops)
+      if (op.kind == OP_REDUCE) max_fanin = std::max(max_fanin, int(op.ins.size()));
+  // stage (= copy tile) size and pipeline depth, within kStageBudget bytes:
+  // bulk streaming 6 x 32 KiB; wide reductions 3 x 64 KiB (reduce tiles are
+  // stage / fan-in); small chunks: the smallest power of two that holds one
   int tile = req.tile;
   if (tile <= 0) {
-    tile = kMaxTile;
-    if (maxlen < kMaxTile) {
+    tile = max_fanin >= 4 ? kMaxTile : 32768;
+    if (maxlen < tile) {
       tile = 1024;
       while (tile < maxlen) tile *= 2;
     }
   }
   if (tile % 16 || tile > kMaxTile || tile < 256)
-    throw invalid_argument_error("tile_bytes must be a multiple of 16 in [256, 32768]");
-  int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, ll ? 0 : tile)
+    throw invalid_argument_error("tile_bytes must be a multiple of 16 in [256, 65536]");
+  const int nstage = std::max(2, std::min(6, kStageBudget / tile));
+  int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, ll ? 0 : tile, nstage)
             : ll ? 2048 / kLLThreads
-                 : std::max(1, std::min(2048 / kThreads, int((227 << 10) / (kStages * tile + 2048))));
+                 : std::max(1, std::min(2, int((227 << 10) / (nstage * tile + 2048))));
   const int resident = std::max(1, req.sms * std::max(1, bps));
   const int cap = loopback ? std::max(1, resident / p.sched.P) : 32;
-  const int64_t part = ll ? kLLPart : kMaxTile;  // bytes one CTA should own per chunk
+  // bytes of a chunk one CTA should own: enough to pipeline (256 KiB for
+  // the bulk protocol), small for LL (latency)
+  const int64_t part = ll ? kLLPart : std::max<int64_t>(tile, 256 << 10);
   int kb, kc;
   if (req.nchannels > 0) {
     kb = req.nchannels;
@@ -144,6 +154,7 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   p.kb = kb;
   p.nch = kc * kb;
   p.tile = tile;
+  p.nstage = nstage;
   // small tiles: retire every bulk group at once (latency); large: keep 6
   // groups in flight (bandwidth; FIFO depth 8 in the kernel)
   p.sig_lag = tile >= 16384 ? 6 : 0;
@@ -247,10 +258,10 @@ struct OccCtx {
   int dtype;
   bool sys;
 };
-int occ_fn(void* ctx, int tile) {
+int occ_fn(void* ctx, int tile, int nstage) {
   auto* c = static_cast<OccCtx*>(ctx);
   int bps = 0;
-  cuda_check(exec_occupancy(c->dtype, c->sys, tile, &bps), "occupancy");
+  cuda_check(exec_occupancy(c->dtype, c->sys, tile, nstage, &bps), "occupancy");
   return bps;
 }
 
@@ -277,6 +288,7 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.kc = p.kc;
   k.kb = p.kb;
   k.tile = p.tile;
+  k.nstage = p.nstage;
   k.sig_lag = p.sig_lag;
   k.ll = p.ll ? 1 : 0;
   k.entry_base = p.entry_base;
@@ -536,7 +548,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"sig_lag\":" << p->sig_lag << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"sig_lag\":" << p->sig_lag << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

@@ -65,7 +65,7 @@ def test_bad_arguments():
     with pytest.raises(sccl.InvalidArgumentError, match="tile"):
         sccl.LoopbackPlan(js, 4096, sccl.U8, device=-1, tile_bytes=100)
     with pytest.raises(sccl.InvalidArgumentError, match="tile"):
-        sccl.LoopbackPlan(js, 4096, sccl.U8, device=-1, tile_bytes=65536)
+        sccl.LoopbackPlan(js, 4096, sccl.U8, device=-1, tile_bytes=131072)
 
 
 def test_blob_exchange_single_process():

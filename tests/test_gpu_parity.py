@@ -230,9 +230,9 @@ def test_chunk_groups_gpu(kc, kb):
 
 
 def test_many_chunk_groups_small():
-    """one CTA per chunk (56 chunk groups x 8 ranks = 448 CTAs, small tiles)"""
-    run_gpu(SCHED["ag_777"], 20000, O.U8, nch=1, kc=56, protocol="simple", repeats=2)
-    run_gpu(SCHED["ar_56_14_14"], 20000, O.F32, nch=1, kc=56, protocol="simple", repeats=2)
+    """many chunk groups (28 x 8 ranks = 224 CTAs, small tiles; 56 with LL)"""
+    run_gpu(SCHED["ag_777"], 20000, O.U8, nch=1, kc=28, protocol="simple", repeats=2)
+    run_gpu(SCHED["ar_56_14_14"], 20000, O.F32, nch=1, kc=28, protocol="simple", repeats=2)
     run_gpu(SCHED["ag_777"], 20000, O.U8, nch=1, kc=56, protocol="ll", repeats=2)
 
 
