@@ -138,9 +138,10 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
                  : std::max(1, std::min(2, int((227 << 10) / (nstage * tile + 2048))));
   const int resident = std::max(1, req.sms * std::max(1, bps));
   const int cap = loopback ? std::max(1, resident / p.sched.P) : 32;
-  // bytes of a chunk one CTA should own: enough to pipeline (256 KiB for
-  // the bulk protocol), small for LL (latency)
-  const int64_t part = ll ? kLLPart : std::max<int64_t>(tile, 256 << 10);
+  // bytes of a chunk one CTA should own: one stage for the bulk protocol
+  // (measured: fewer, longer byte parts lose more to idle SMs than they
+  // gain in pipelining), small for LL (latency)
+  const int64_t part = ll ? kLLPart : tile;
   int kb, kc;
   if (req.nchannels > 0) {
     kb = req.nchannels;

@@ -248,3 +248,10 @@ def test_synthesized_schedules_gpu(path, protocol):
     for nb in (8 * 1000, 8 * 65536 + 64):
         for dt in ([O.BF16, O.I32] if kind == "allreduce" else [O.U8]):
             run_gpu(js, nb, dt, protocol=protocol)
+
+
+def test_topology_discovery_gpu():
+    from paper_2008_08708_b200 import topology
+    info = topology.discover()
+    assert info["devices"] >= 1 and info["target"] != "unknown"
+    print("topology:", info)
