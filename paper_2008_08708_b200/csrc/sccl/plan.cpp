@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -96,7 +97,12 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     const auto phases = p.sched.flat();
     for (auto& g : chunk_geometry(p.sched.kind, p.sched.P, phases.back()->G, bytes)) maxlen = std::max(maxlen, g.len);
   }
-  bool ll = req.protocol == 2 || (req.protocol == 0 && maxlen <= kLLMaxChunk);
+  // multi-hop schedules pay the bulk path's per-hop latency S times, so
+  // they keep LL up to larger chunks (measured crossover, tools/tune.py)
+  int total_steps = 0;
+  for (auto* ph : p.sched.flat()) total_steps += ph->S;
+  const int64_t ll_max = total_steps >= 2 ? 4 * kLLMaxChunk : kLLMaxChunk;
+  bool ll = req.protocol == 2 || (req.protocol == 0 && maxlen <= ll_max);
   if (req.protocol < 0 || req.protocol > 2) throw invalid_argument_error("protocol must be 0 (auto), 1 (simple), 2 (ll)");
   p.pg = lower(p.sched, bytes, es, ll);
   p.ll = ll;
@@ -132,7 +138,14 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   }
   if (tile % 16 || tile > kMaxTile || tile < 256)
     throw invalid_argument_error("tile_bytes must be a multiple of 16 in [256, 65536]");
-  const int nstage = std::max(2, std::min(6, kStageBudget / tile));
+  // stage budget: 192 KiB = 1 CTA/SM with a deep ring; SCCL_STAGE_BUDGET
+  // (bytes) trades depth for CTAs per SM (96 KiB -> 2 CTAs/SM)
+  // streaming copies / 2-input reductions: 3 x 32 KiB at 2 CTAs per SM;
+  // wide reductions: 3 x 64 KiB at 1 CTA per SM (tools/tune.py sweep)
+  int budget = max_fanin >= 4 ? kStageBudget : kStageBudget / 2;
+  if (const char* env = std::getenv("SCCL_STAGE_BUDGET")) budget = std::max(2 * 256, std::min(kStageBudget, std::atoi(env)));
+  if (req.stage_budget > 0) budget = std::min(kStageBudget, req.stage_budget);
+  const int nstage = std::max(2, std::min(6, budget / tile));
   int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, ll ? 0 : tile, nstage)
             : ll ? 2048 / kLLThreads
                  : std::max(1, std::min(2, int((227 << 10) / (nstage * tile + 2048))));

@@ -54,7 +54,7 @@ namespace sccl {
 // Channel policy inputs: user overrides (0 = auto) and the resident-CTA
 // capacity per SM as a function of the tile (shared-memory stage) size.
 struct ChannelRequest {
-  int nchannels = 0, chunk_groups = 0, tile = 0, protocol = 0;
+  int nchannels = 0, chunk_groups = 0, tile = 0, protocol = 0, stage_budget = 0;
   int sms = 148;
   int (*blocks_per_sm)(void* ctx, int tile, int nstage) = nullptr;
   void* ctx = nullptr;

@@ -1,0 +1,72 @@
+#!/usr/bin/env python3
+"""Loopback tuning matrix on one GPU: for each (schedule, size, knob set)
+time the executor (CUDA events) and print one JSON line.  Knobs: tile,
+stage budget (env SCCL_STAGE_BUDGET), chunk groups, byte parts, protocol."""
+import itertools
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_2008_08708_b200 import sccl  # noqa: E402
+from paper_2008_08708_b200 import schedules as S  # noqa: E402
+
+
+def time_plan(plan, send, recv, iters):
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        plan.launch(send, recv, st)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(iters):
+        plan.launch(send, recv, st)
+    b.record(st)
+    torch.cuda.synchronize()
+    plan.check()
+    return a.elapsed_time(b) * 1e3 / iters
+
+
+def main():
+    P = 8
+    ag = S.hamiltonian_allgather(P)
+    scheds = {"ag777": (S.to_json(ag), sccl.U8), "ag111": (S.to_json(S.one_shot_allgather(P)), sccl.U8),
+              "ar822": (S.allreduce_from(S.one_shot_allgather(P)), sccl.BF16),
+              "ar56": (S.allreduce_from(ag), sccl.BF16)}
+    grid = json.loads(sys.argv[1]) if len(sys.argv) > 1 else {}
+    sizes = grid.get("sizes", [128 << 20])
+    names = grid.get("scheds", list(scheds))
+    knobs = grid.get("knobs", [{}])
+    maxb = max(sizes)
+    send = [torch.randint(0, 256, (maxb,), dtype=torch.uint8, device="cuda") for _ in range(P)]
+    recv = [torch.empty(P * maxb, dtype=torch.uint8, device="cuda") for _ in range(P)]
+    for name, sz, kn in itertools.product(names, sizes, knobs):
+        js, dt = scheds[name]
+        if "budget" in kn:
+            os.environ["SCCL_STAGE_BUDGET"] = str(kn["budget"])
+        else:
+            os.environ.pop("SCCL_STAGE_BUDGET", None)
+        try:
+            plan = sccl.LoopbackPlan(js, sz, dt, device=0, nchannels=kn.get("kb", 0), chunk_groups=kn.get("kc", 0),
+                                     tile_bytes=kn.get("tile", 0), protocol=kn.get("protocol", "auto"))
+        except sccl.SCCLError as e:
+            print(json.dumps({"sched": name, "bytes": sz, "knobs": kn, "error": str(e)[:100]}), flush=True)
+            continue
+        rb = plan.recv_bytes
+        us = time_plan(plan, [x[:sz] for x in send], [x[:rb] for x in recv], 20 if sz >= (16 << 20) else 100)
+        info = plan.info()
+        prog = info["program"]
+        hbm = sum(op["len"] * (len(op["ins"]) + len(op["outs"])) for rk in prog["ranks"] for op in rk["ops"]
+                  if op["kind"] != "wait")
+        print(json.dumps({"sched": name, "bytes": sz, "knobs": kn, "us": round(us, 2),
+                          "hbm_TBps": round(hbm / us / 1e6, 3), "kc": info["chunk_groups"], "kb": info["byte_parts"],
+                          "tile": info["tile_bytes"], "nstage": info["nstage"], "proto": info["protocol"],
+                          "grid": info["grid"]}), flush=True)
+        plan.close()
+
+
+if __name__ == "__main__":
+    main()
