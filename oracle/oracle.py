@@ -540,6 +540,29 @@ def seeded_inputs(kind: str, P: int, nbytes: int, dtype: int, seed: int,
     return out
 
 
+def cli_payload(nbytes: int, seed: int, rank: int) -> np.ndarray:
+    """Input bytes the C++ CLI (sccl-exec exec) generates: little-endian
+    bytes of splitmix64((seed << 40) ^ (rank << 32) ^ word)."""
+    M = 0xFFFFFFFFFFFFFFFF
+    nw = (nbytes + 7) // 8
+    x = ((np.uint64(seed) << np.uint64(40)) ^ (np.uint64(rank) << np.uint64(32))
+         ^ np.arange(nw, dtype=np.uint64))
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9e3779b97f4a7c15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+        x = x ^ (x >> np.uint64(31))
+    return x.view(np.uint8)[:nbytes].copy()
+
+
+def fnv1a(b: np.ndarray) -> str:
+    h = 0xcbf29ce484222325
+    for c in np.ascontiguousarray(b).view(np.uint8).tobytes():
+        h ^= c
+        h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
 def digest(bufs: Sequence[np.ndarray]) -> str:
     h = hashlib.sha256()
     for b in bufs:

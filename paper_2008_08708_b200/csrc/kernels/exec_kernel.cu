@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[t][SP_FLAGS_IDX]) + p.entry_base + rank * p.nch + ch, e);
       }
 
-  const uint32_t ob = p.prog[rank], oe = p.prog[rank + 1];
+  const uint32_t ob = p.prog[rank * p.kc + cg], oe = p.prog[rank * p.kc + cg + 1];
   uint32_t it = 0;   // stage-use counter (same sequence in every role)
   uint32_t seq = 0;  // tile sequence number (for local read-after-write)
 
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
         st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[t][SP_FLAGS_IDX]) + p.entry_base + rank * p.nch + ch, e);
       }
 
-  const uint32_t ob = p.prog[rank], oe = p.prog[rank + 1];
+  const uint32_t ob = p.prog[rank * p.kc + cg], oe = p.prog[rank * p.kc + cg + 1];
   for (uint32_t oi = ob; oi < oe; ++oi) {
     const DevOp op = p.ops[oi];
     if (op.kind == 2) {  // receipts nobody forwards: consume them

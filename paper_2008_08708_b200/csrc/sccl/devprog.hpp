@@ -53,7 +53,7 @@ struct KParams {
   const DevOp* ops;
   const DevIn* ins;
   const DevOut* outs;
-  const uint32_t* prog;  // [P+1] op ranges per rank
+  const uint32_t* prog;  // [P*kc+1] op ranges per (rank, chunk group)
   uint64_t* epochs;      // [nranks_launch * nch] per-CTA launch counters
   int* errinfo;          // host-mapped watchdog record
   long long timeout_ns;

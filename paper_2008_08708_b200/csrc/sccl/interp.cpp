@@ -155,7 +155,7 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
 
   auto run = [&](int rank, int ch) {
     const int cg = ch % kc, cb = ch / kc;  // same channel map as the kernel
-    for (uint32_t oi = p->prog[rank]; oi < p->prog[rank + 1]; ++oi) {
+    for (uint32_t oi = p->prog[size_t(rank) * kc + cg]; oi < p->prog[size_t(rank) * kc + cg + 1]; ++oi) {
       const DevOp& op = p->ops[oi];
       if (op.kind == OP_WAIT) {
         for (int i = 0; i < op.nin; ++i) {

@@ -179,49 +179,63 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   p.ops.clear();
   p.ins.clear();
   p.outs.clear();
-  p.prog.assign(P + 1, 0);
-  for (int r = 0; r < P; ++r) {
-    p.prog[r] = uint32_t(p.ops.size());
-    for (const Op& op : p.pg.ranks[r].ops) {
-      if (op.kind != OP_WAIT && (op.ins.size() > size_t(kMaxOpIn) || op.outs.size() > size_t(kMaxOpOut)))
-        throw invalid_argument_error("op fan-in/fan-out exceeds executor limits (32)");
-      DevOp d{};
-      d.len = uint64_t(op.len);
-      d.chunk = uint32_t(std::max(0, op.chunk));
-      d.kind = uint8_t(op.kind);
-      d.in_begin = uint32_t(p.ins.size());
-      d.out_begin = uint32_t(p.outs.size());
-      d.nin = uint16_t(op.ins.size());
-      d.nout = uint16_t(op.outs.size());
-      bool vec = true;
-      for (auto& in : op.ins) {
-        if (in.loc.rank != r) throw invalid_argument_error("internal: op reads remote memory");
-        DevIn x{};
-        x.off = uint64_t(in.loc.off);
-        x.len = uint64_t(in.len);
-        x.flag = in.flag;
-        x.chunk = uint32_t(std::max(0, in.chunk));
-        x.rank = uint8_t(in.loc.rank);
-        x.space = uint8_t(in.loc.space);
-        vec &= in.loc.off % 16 == 0;
-        if (in.flag < 0 && in.loc.space != SP_SEND) d.raw = 1;
-        p.ins.push_back(x);
-      }
-      for (auto& o : op.outs) {
-        DevOut x{};
-        x.off = uint64_t(o.loc.off);
-        x.flag = o.flag;
-        x.rank = uint8_t(o.loc.rank);
-        x.space = uint8_t(o.loc.space);
-        x.every_tile = o.every_tile ? 1 : 0;
-        vec &= o.loc.off % 16 == 0;
-        p.outs.push_back(x);
-      }
-      d.vec = vec ? 1 : 0;
-      p.ops.push_back(d);
+  // one op list per (rank, chunk group): a CTA walks only its own ops
+  // (ops of different chunks never depend on each other within a rank);
+  // end-of-program waits are split by chunk group the same way
+  p.prog.assign(size_t(P) * p.kc + 1, 0);
+  auto encode = [&](int r, const Op& op, const std::vector<OpIn>& ins) {
+    if (op.kind != OP_WAIT && (ins.size() > size_t(kMaxOpIn) || op.outs.size() > size_t(kMaxOpOut)))
+      throw invalid_argument_error("op fan-in/fan-out exceeds executor limits (32)");
+    DevOp d{};
+    d.len = uint64_t(op.len);
+    d.chunk = uint32_t(std::max(0, op.chunk));
+    d.kind = uint8_t(op.kind);
+    d.in_begin = uint32_t(p.ins.size());
+    d.out_begin = uint32_t(p.outs.size());
+    d.nin = uint16_t(ins.size());
+    d.nout = uint16_t(op.outs.size());
+    bool vec = true;
+    for (auto& in : ins) {
+      if (in.loc.rank != r) throw invalid_argument_error("internal: op reads remote memory");
+      DevIn x{};
+      x.off = uint64_t(in.loc.off);
+      x.len = uint64_t(in.len);
+      x.flag = in.flag;
+      x.chunk = uint32_t(std::max(0, in.chunk));
+      x.rank = uint8_t(in.loc.rank);
+      x.space = uint8_t(in.loc.space);
+      vec &= in.loc.off % 16 == 0;
+      if (in.flag < 0 && in.loc.space != SP_SEND) d.raw = 1;
+      p.ins.push_back(x);
     }
-  }
-  p.prog[P] = uint32_t(p.ops.size());
+    for (auto& o : op.outs) {
+      DevOut x{};
+      x.off = uint64_t(o.loc.off);
+      x.flag = o.flag;
+      x.rank = uint8_t(o.loc.rank);
+      x.space = uint8_t(o.loc.space);
+      x.every_tile = o.every_tile ? 1 : 0;
+      vec &= o.loc.off % 16 == 0;
+      p.outs.push_back(x);
+    }
+    d.vec = vec ? 1 : 0;
+    p.ops.push_back(d);
+  };
+  for (int r = 0; r < P; ++r)
+    for (int cg = 0; cg < p.kc; ++cg) {
+      p.prog[size_t(r) * p.kc + cg] = uint32_t(p.ops.size());
+      for (const Op& op : p.pg.ranks[r].ops) {
+        if (op.kind == OP_WAIT) {
+          std::vector<OpIn> mine;
+          for (auto& in : op.ins)
+            if (std::max(0, in.chunk) % p.kc == cg) mine.push_back(in);
+          if (!mine.empty()) encode(r, op, mine);
+        } else if (std::max(0, op.chunk) % p.kc == cg) {
+          encode(r, op, op.ins);
+        }
+      }
+    }
+  p.prog[size_t(P) * p.kc] = uint32_t(p.ops.size());
 
   // memory layout of one rank's region
   auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };

@@ -26,7 +26,7 @@ struct sccl_plan {
   std::vector<sccl::DevOp> ops;
   std::vector<sccl::DevIn> ins;
   std::vector<sccl::DevOut> outs;
-  std::vector<uint32_t> prog;  // [P+1]
+  std::vector<uint32_t> prog;  // [P*kc+1]: op range per (rank, chunk group)
 
   // device program
   sccl::DevOp* d_ops = nullptr;
