@@ -1,0 +1,73 @@
+"""Multi-process path on ONE GPU: two processes, one rank each, both on
+cuda:0.  Exercises exactly what an 8xB200 run uses -- CUDA-IPC export /
+bind of the plan regions through torch.distributed (gloo), sys-scope
+counters, the per-(peer, channel) entry handshake, the registered receive
+buffer and its copy-out -- except that the peer is the same device (the
+contexts time-slice instead of running concurrently, so this checks
+correctness, not speed)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r"""
+import json, os, sys
+sys.path[:0] = [{root!r}, {oracle!r}]
+import numpy as np, torch, torch.distributed as dist
+import oracle as O
+from paper_2008_08708_b200 import sccl, schedules as S
+rank = int(sys.argv[1])
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=2)
+torch.cuda.set_device(0)
+cases = [
+    (S.to_json(S.one_shot_allgather(2)), 1 << 16, O.U8, "simple"),
+    (S.to_json(S.one_shot_allgather(2)), 4096, O.U8, "ll"),
+    (S.allreduce_from(S.one_shot_allgather(2)), 1 << 18, O.BF16, "simple"),
+    (S.allreduce_from(S.one_shot_allgather(2)), 2048, O.F32, "ll"),
+]
+for js, nb, dt, proto in cases:
+    d = json.loads(js)
+    ins = O.seeded_inputs(d["collective"], 2, nb, dt, 17)
+    ref = O.execute(d, ins, nb, dt)
+    plan = sccl.Plan(js, rank, 2, nb, dt, device=0, protocol=proto, timeout_ms=60000)
+    plan.bind_with()
+    send = torch.from_numpy(ins[rank]).cuda()
+    for it in range(3):  # back-to-back launches: entry handshake + epochs
+        recv = torch.zeros(ref[rank].size, dtype=torch.uint8, device="cuda")
+        plan.launch(send, recv)
+        torch.cuda.synchronize()
+        plan.check()
+        assert np.array_equal(recv.cpu().numpy(), ref[rank]), (d["collective"], proto, it)
+        dist.barrier()
+    plan.close()
+    print("OK", rank, d["collective"], proto, flush=True)
+dist.destroy_process_group()
+"""
+
+
+def test_two_processes_one_gpu(tmp_path):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = tmp_path / "w.py"
+    script.write_text(WORKER.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"), port=port))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    procs = [subprocess.Popen([sys.executable, str(script), str(r)], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True, env=env) for r in range(2)]
+    try:
+        outs = [p.communicate(timeout=600) for p in procs]
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, (o, e[-3000:])
+    text = "".join(o for o, _ in outs)
+    assert text.count("OK") == 8, text

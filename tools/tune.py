@@ -16,16 +16,22 @@ from paper_2008_08708_b200 import schedules as S  # noqa: E402
 
 
 def time_plan(plan, send, recv, iters):
-    st = torch.cuda.current_stream()
+    st = torch.cuda.Stream()
     for _ in range(3):
         plan.launch(send, recv, st)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st)
-    for _ in range(iters):
-        plan.launch(send, recv, st)
-    b.record(st)
-    torch.cuda.synchronize()
+    st.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for _ in range(iters):
+            plan.launch(send, recv, st)
+    with torch.cuda.stream(st):  # replay() launches on the current stream
+        g.replay()
+        st.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        g.replay()
+        b.record(st)
+    st.synchronize()
     plan.check()
     return a.elapsed_time(b) * 1e3 / iters
 
