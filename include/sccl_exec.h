@@ -97,6 +97,13 @@ int sccl_launch(sccl_plan* plan, const void* sendbuf, void* recvbuf, void* strea
 /* Loopback launch: sendbufs[r]/recvbufs[r] for r < P, all on the plan's device. */
 int sccl_launch_loopback(sccl_plan* plan, const void* const* sendbufs, void* const* recvbufs, void* stream);
 
+/* Comparison backend: the same
+ * lowered program executed as one cudaMemcpyAsync per send in step order
+ * (copy engines / driver copies).  Non-combining schedules, simple protocol.
+ * Not the hot path; bench.py reports it beside the kernel. */
+int sccl_launch_loopback_copy_engine(sccl_plan* plan, const void* const* sendbufs, void* const* recvbufs,
+                                     void* stream);
+
 /* After the stream is synchronized: SCCL_PEER_TIMEOUT if the watchdog fired
  * (details in sccl_last_error), else SCCL_OK. */
 int sccl_plan_check(sccl_plan* plan);

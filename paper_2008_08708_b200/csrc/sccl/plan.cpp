@@ -559,6 +559,43 @@ int sccl_launch_loopback(sccl_plan* p, const void* const* sendbufs, void* const*
   });
 }
 
+int sccl_launch_loopback_copy_engine(sccl_plan* p, const void* const* sendbufs, void* const* recvbufs,
+                                     void* stream) {
+  return guarded([&] {
+    if (!p || !sendbufs || !recvbufs) throw invalid_argument_error("NULL argument");
+    if (!p->loopback || p->host_only) throw invalid_argument_error("needs a device loopback plan");
+    if (p->ll) throw invalid_argument_error("copy-engine baseline needs the simple protocol's program");
+    // the paper's per-step cudaMemcpy lowering:
+    // every send of the lowered program becomes one stream-ordered
+    // device-to-device copy, steps in order -- a comparison point, not the
+    // hot path (no reductions: combining schedules need the kernel)
+    std::vector<std::pair<int, std::pair<int, const Op*>>> order;
+    for (int r = 0; r < p->nranks; ++r)
+      for (const Op& op : p->pg.ranks[r].ops) {
+        if (op.kind == OP_REDUCE) throw invalid_argument_error("copy-engine baseline: combining schedules unsupported");
+        if (op.kind == OP_COPY) order.push_back({op.key, {r, &op}});
+      }
+    std::stable_sort(order.begin(), order.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    auto base = [&](int rank, int space) -> char* {
+      if (space == SP_SEND) return const_cast<char*>(static_cast<const char*>(sendbufs[rank]));
+      if (space == SP_RECV) return static_cast<char*>(recvbufs[rank]);
+      return p->d_region + size_t(rank) * p->region_bytes + p->scratch_off;
+    };
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+    for (auto& e : order) {
+      const Op& op = *e.second.second;
+      if (op.len == 0) continue;
+      const char* src = base(op.ins[0].loc.rank, op.ins[0].loc.space) + op.ins[0].loc.off;
+      for (auto& o : op.outs)
+        cuda_check(cudaMemcpyAsync(base(o.loc.rank, o.loc.space) + o.loc.off, src, size_t(op.len),
+                                   cudaMemcpyDeviceToDevice, st),
+                   "cudaMemcpyAsync");
+    }
+  });
+}
+
 int sccl_plan_check(sccl_plan* p) {
   return guarded([&] {
     if (!p) throw invalid_argument_error("NULL plan");

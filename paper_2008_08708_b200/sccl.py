@@ -68,6 +68,7 @@ def lib():
         L.sccl_plan_recv_buffer.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_sz)]
         L.sccl_launch.argtypes = [c_p, c_p, c_p, c_p]
         L.sccl_launch_loopback.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
+        L.sccl_launch_loopback_copy_engine.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
         L.sccl_plan_check.argtypes = [c_p]
         L.sccl_plan_info.argtypes = [c_p, c_p, ctypes.POINTER(c_sz)]
         L.sccl_plan_launch_count.argtypes = [c_p]
@@ -215,6 +216,13 @@ class LoopbackPlan(_PlanBase):
         s = (ctypes.c_void_p * P)(*[_ptr(x) for x in sendbufs])
         r = (ctypes.c_void_p * P)(*[_ptr(x) for x in recvbufs])
         _raise(lib().sccl_launch_loopback(self._h, s, r, ctypes.c_void_p(_stream_ptr(stream))))
+
+    def launch_copy_engine(self, sendbufs: Sequence, recvbufs: Sequence, stream=None):
+        """Comparison backend: one cudaMemcpyAsync per send, steps in order."""
+        P = self.nranks
+        s = (ctypes.c_void_p * P)(*[_ptr(x) for x in sendbufs])
+        r = (ctypes.c_void_p * P)(*[_ptr(x) for x in recvbufs])
+        _raise(lib().sccl_launch_loopback_copy_engine(self._h, s, r, ctypes.c_void_p(_stream_ptr(stream))))
 
     def interpret_on_cpu(self, sendbufs: Sequence, recvbufs: Sequence, timeout_s: float = 30.0):
         """TEST HOOK (sccl_debug.h): run the lowered program on CPU threads

@@ -255,3 +255,21 @@ def test_topology_discovery_gpu():
     info = topology.discover()
     assert info["devices"] >= 1 and info["target"] != "unknown"
     print("topology:", info)
+
+
+@pytest.mark.parametrize("name", ["ag_777", "ag_b7_ring8", "a2a_b5", "bcast_chain"])
+def test_copy_engine_baseline_matches(name):
+    """The copy-engine comparison backend runs the same lowered program."""
+    js = SCHED[name]
+    d = json.loads(js)
+    nb = 1 << 20
+    ins = O.seeded_inputs(d["collective"], d["P"], nb, O.U8, 21)
+    ref = O.execute(d, ins, nb, O.U8)
+    plan = sccl.LoopbackPlan(js, nb, O.U8, device=0, protocol="simple")
+    send = [torch.from_numpy(x).to(DEV) for x in ins]
+    recv = [torch.zeros(r.size, dtype=torch.uint8, device=DEV) for r in ref]
+    plan.launch_copy_engine(send, recv)
+    torch.cuda.synchronize()
+    for r, (a, b) in enumerate(zip(recv, ref)):
+        got = np.where(_covered(d, nb, r, b.size), a.cpu().numpy(), 0)
+        assert np.array_equal(got, b)
