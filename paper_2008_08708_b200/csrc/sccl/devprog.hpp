@@ -16,7 +16,8 @@ constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
 constexpr int kStageBudget = 196608;  // bytes of stages per CTA (nstage * tile)
 constexpr int kThreads = 352;   // producer, storer and signaler warps + 8 compute warps
 constexpr int kLLThreads = 256; // LL kernel
-constexpr int64_t kLLMaxChunk = 16384;  // auto protocol: LL up to this chunk size
+constexpr int64_t kLLMaxChunk = 65536;         // auto protocol: LL up to this chunk size (copies)
+constexpr int64_t kLLMaxChunkReduce = 163840;  // ... and for schedules that reduce
 constexpr int64_t kLLPart = 4096;       // LL: bytes of a chunk one CTA owns
 
 struct DevIn {

@@ -97,11 +97,12 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     const auto phases = p.sched.flat();
     for (auto& g : chunk_geometry(p.sched.kind, p.sched.P, phases.back()->G, bytes)) maxlen = std::max(maxlen, g.len);
   }
-  // multi-hop schedules pay the bulk path's per-hop latency S times, so
-  // they keep LL up to larger chunks (measured crossover, tools/tune.py)
-  int total_steps = 0;
-  for (auto* ph : p.sched.flat()) total_steps += ph->S;
-  const int64_t ll_max = total_steps >= 2 ? 4 * kLLMaxChunk : kLLMaxChunk;
+  // measured crossover on B200 (tools/tune.py, loopback, round 1): LL wins
+  // up to 64 KiB chunks for copies and up to ~160 KiB when the schedule
+  // reduces (the bulk path's wide-reduce tiles are its weaker side)
+  bool combining = false;
+  for (auto* ph : p.sched.flat()) combining |= is_combining(ph->kind);
+  const int64_t ll_max = combining ? kLLMaxChunkReduce : kLLMaxChunk;
   bool ll = req.protocol == 2 || (req.protocol == 0 && maxlen <= ll_max);
   if (req.protocol < 0 || req.protocol > 2) throw invalid_argument_error("protocol must be 0 (auto), 1 (simple), 2 (ll)");
   p.pg = lower(p.sched, bytes, es, ll);
