@@ -68,7 +68,7 @@ def test_program_structure_one_shot_allgather():
     """B4 lowers to exactly one fused op per rank: read the input chunk once,
     write the own output slot and the 7 peers (PAPER.md:724 single fused
     kernel, push model PAPER.md:720), plus the end-of-program wait."""
-    plan = sccl.LoopbackPlan(CASES["b4"], 1 << 20, sccl.U8, device=-1)
+    plan = sccl.LoopbackPlan(CASES["b4"], 1 << 20, sccl.U8, device=-1, protocol="simple")
     prog = plan.info()["program"]
     for r, rk in enumerate(prog["ranks"]):
         kinds = [op["kind"] for op in rk["ops"]]
@@ -80,7 +80,7 @@ def test_program_structure_one_shot_allgather():
 def test_program_structure_fused_allreduce():
     """(8,2,2): per rank 7 pushes into peers' receipt slots, then one fused
     receive-reduce-broadcast op (8 inputs, 8 outputs)."""
-    plan = sccl.LoopbackPlan(CASES["ar_b4"], 1 << 20, sccl.BF16, device=-1)
+    plan = sccl.LoopbackPlan(CASES["ar_b4"], 1 << 20, sccl.BF16, device=-1, protocol="simple")
     for rk in plan.info()["program"]["ranks"]:
         red = [op for op in rk["ops"] if op["kind"] == "reduce"]
         assert len(red) == 1 and len(red[0]["ins"]) == 8 and len(red[0]["outs"]) == 8
