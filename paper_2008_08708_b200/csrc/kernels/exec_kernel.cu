@@ -912,7 +912,6 @@ cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st) 
   return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(NT), args, smem_bytes(p.tile, p.nstage), st);
 }
 
-size_t exec_smem_bytes(int tile, int nstage) { return smem_bytes(tile, nstage); }
 
 cudaError_t exec_occupancy(int dtype, bool sys, int tile, int nstage, int* blocks_per_sm) {
   // tile == 0: the LL kernel (no dynamic shared memory)

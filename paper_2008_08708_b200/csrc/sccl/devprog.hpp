@@ -65,7 +65,6 @@ struct KParams {
   int sig_lag;           // bulk groups the storer keeps in flight before retiring (0..6)
   int entry_base;        // index of the entry-handshake flags in FLAGS
   int multiprocess;      // 1: peers are other processes (entry handshake)
-  int send_readonly;     // 1: SEND does not alias RECV (non-coherent loads ok)
   int ll;                // 1: low-latency protocol (receipts are LL slots)
 };
 

@@ -85,7 +85,6 @@ Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
   const int root = s.root >= 0 ? s.root : (phases[0]->root >= 0 ? phases[0]->root : 0);
   Relation fpre, fpost;
   pre_post(phases.back()->kind, G, P, root, fpre, fpost);
-  std::vector<int> acc_scratch(size_t(G) * P, -1);  // scratch accumulators (RS/Reduce non-dest)
   std::vector<int64_t> acc_scratch_off(size_t(G) * P, -1);
 
   int step_base = 0;

@@ -298,10 +298,6 @@ void check_aligned(const void* p, const char* what) {
   if (reinterpret_cast<uintptr_t>(p) % 16) throw invalid_argument_error(std::string(what) + " must be 16-byte aligned");
 }
 
-bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
-  auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
-  return na && nb && x < y + nb && y < x + na;
-}
 
 void fill_common(const sccl_plan& p, KParams& k) {
   std::memset(&k, 0, sizeof k);
@@ -518,7 +514,6 @@ int sccl_launch(sccl_plan* p, const void* sendbuf, void* recvbuf, void* stream) 
     k.rank0 = p->rank;
     k.nranks_launch = 1;
     k.multiprocess = 1;
-    k.send_readonly = !overlaps(sendbuf, size_t(p->pg.send_bytes), reg, size_t(p->pg.recv_bytes));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
     cuda_check(launch_exec(k, p->dtype, true, st), "launch");
@@ -536,7 +531,6 @@ int sccl_launch_loopback(sccl_plan* p, const void* const* sendbufs, void* const*
     if (p->host_only) throw invalid_argument_error("host-only plan cannot launch (no CUDA device)");
     KParams k;
     fill_common(*p, k);
-    bool ro = true;
     for (int r = 0; r < p->nranks; ++r) {
       if (p->pg.send_bytes && !sendbufs[r]) throw invalid_argument_error("sendbuf is NULL");
       if (p->pg.recv_bytes && !recvbufs[r]) throw invalid_argument_error("recvbuf is NULL");
@@ -547,13 +541,10 @@ int sccl_launch_loopback(sccl_plan* p, const void* const* sendbufs, void* const*
       k.base[r][SP_RECV] = static_cast<char*>(recvbufs[r]);
       k.base[r][SP_SCRATCH] = reg + p->scratch_off;
       k.base[r][SP_FLAGS] = reg;
-      for (int q = 0; q < p->nranks; ++q)
-        ro &= !overlaps(sendbufs[r], size_t(p->pg.send_bytes), recvbufs[q], size_t(p->pg.recv_bytes));
     }
     k.rank0 = 0;
     k.nranks_launch = p->nranks;
     k.multiprocess = 0;
-    k.send_readonly = ro ? 1 : 0;
     cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
     cuda_check(launch_exec(k, p->dtype, false, static_cast<cudaStream_t>(stream)), "launch");
     p->launches++;

@@ -45,7 +45,6 @@ struct sccl_plan {
   int* h_err = nullptr;  // host-mapped watchdog record
   int* d_err = nullptr;
   int64_t launches = 0;
-  void* stream_hint = nullptr;
 };
 
 namespace sccl {
