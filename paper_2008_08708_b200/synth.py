@@ -27,17 +27,11 @@ from typing import Dict, List, Optional, Tuple
 
 from . import sccl
 
-TOPO_CACHE: Dict[str, dict] = {}
-
-
 def topology_edges(name: str) -> Tuple[int, List[Tuple[List[Tuple[int, int]], int]]]:
-    """(P, [(edges, bound)]) of a named topology, read back from the C++
-    builders through a canonical round trip of an empty schedule."""
-    import json as _json
-    if name not in TOPO_CACHE:
-        P = {"dgx1": 8, "amd-z52": 8}.get(name) or int(name.split(":")[1])
-        TOPO_CACHE[name] = {"P": P}
-    P = TOPO_CACHE[name]["P"]
+    """(P, [(edges, bound)]) of a named topology: the builders of
+    SPEC.md:36-71 restated (the C++ library rebuilds the same constraints
+    when it verifies the decoded schedule, so a disagreement fails loudly)."""
+    P = {"dgx1": 8, "amd-z52": 8}.get(name) or int(name.split(":")[1])
     # builders restated (SPEC.md:36-71); E and groups per PAPER.md:343-345
     if name in ("dgx1",):
         bw = {}
@@ -171,3 +165,81 @@ def synthesize(kind: str, topo: str, C: int, S: int, R: int, root: int = 0,
     if v:
         raise RuntimeError(f"decoded schedule failed verification: {v[:3]}")
     return "sat", js, dt
+
+
+# ----------------------------------------------------------------------------
+# Algorithm 1, Pareto-Synthesize
+# ----------------------------------------------------------------------------
+def diameter(topo: str) -> int:
+    """Max over node pairs of the shortest directed path over E."""
+    P, groups = topology_edges(topo)
+    E = {e for es, b in groups for e in es if b > 0}
+    best = 0
+    for s in range(P):
+        dist = {s: 0}
+        frontier = [s]
+        while frontier:
+            nxt = []
+            for u in frontier:
+                for (a, b) in E:
+                    if a == u and b not in dist:
+                        dist[b] = dist[u] + 1
+                        nxt.append(b)
+            frontier = nxt
+        if len(dist) < P:
+            raise ValueError(f"unreachable pair from node {s} in {topo}")
+        best = max(best, max(dist.values()))
+    return best
+
+
+def bandwidth_lower_bound(kind: str, topo: str) -> "Fraction":
+    """Per-node ingress bound on R/C (the paper's §2.4
+    argument): a node that must receive X chunks per per-node chunk over
+    ingress bandwidth B needs R/C >= X / B.  (The exhaustive cut bounds of
+    SPEC.md:100 are not restated; the per-node bound is sound.)"""
+    from fractions import Fraction
+    P, groups = topology_edges(topo)
+    need = {"allgather": P - 1, "alltoall": Fraction(P - 1, P), "broadcast": 1, "gather": 0,
+            "scatter": 0}[kind]
+    best = Fraction(0)
+    for n in range(P):
+        ingress = sum(b for es, b in groups for (a, d) in es if d == n and len(es) == 1)
+        for es, b in groups:  # grouped ingress constraints (switch model)
+            if len(es) > 1 and all(d == n for (_, d) in es):
+                ingress = b if ingress == 0 else min(ingress, b)
+        if need and ingress:
+            best = max(best, Fraction(need) / ingress)
+    return best
+
+
+def pareto_synthesize(kind: str, topo: str, k: int, max_steps: int = 8, timeout: float = 120.0,
+                      root: int = 0) -> List[dict]:
+    """Algorithm 1: for S = diameter.. try (R, C) with S <= R <= S+k and
+    R/C >= b_l in ascending R/C (ties: smaller R); report the first SAT per
+    S; stop once R/C reaches b_l."""
+    from fractions import Fraction
+    a_l = diameter(topo)
+    b_l = bandwidth_lower_bound(kind, topo)
+    frontier: List[dict] = []
+    best_ratio = None
+    for S in range(a_l, max_steps + 1):
+        cands = []
+        for R in range(S, S + k + 1):
+            C = 1
+            while Fraction(R, C) >= b_l:
+                if best_ratio is None or Fraction(R, C) < best_ratio:
+                    cands.append((Fraction(R, C), R, C))
+                C += 1
+        cands.sort()
+        for ratio, R, C in cands:
+            if kind == "alltoall" and C % topology_edges(topo)[0]:
+                continue
+            st, js, dt = synthesize(kind, topo, C, S, R, root, timeout)
+            if st == "sat":
+                frontier.append({"C": C, "S": S, "R": R, "ratio": str(ratio), "seconds": round(dt, 2),
+                                 "schedule": js, "bandwidth_optimal": ratio == b_l})
+                best_ratio = ratio
+                break
+        if best_ratio is not None and best_ratio == b_l:
+            break
+    return frontier
