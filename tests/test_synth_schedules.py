@@ -72,3 +72,42 @@ def test_synth_small_instances():
     assert st == "sat" and json.loads(js)["S"] == 2
     st, js, _ = synth.synthesize("broadcast", "ring:4", 2, 3, 3, root=0)
     assert st == "sat" and sccl.verify(js) == []
+
+
+PARETO = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "schedules", "pareto", "ag_*.json")))
+
+
+def test_pareto_index_matches_paper():
+    """Table 5 (PAPER.md:952-954): ring(8) k=0 frontier starts at (1,4,4);
+    k=3 reaches (2,4,7), both latency- and bandwidth-optimal."""
+    idx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "schedules", "pareto", "index.json")))
+    r8 = {(e["k"], e["C"], e["S"], e["R"]) for e in idx if e["topology"] == "ring:8"}
+    assert (0, 1, 4, 4) in r8 and (3, 2, 4, 7) in r8
+    assert all(e["bandwidth_optimal"] for e in idx if e["topology"].startswith("full"))
+
+
+@pytest.mark.parametrize("path", PARETO, ids=[os.path.basename(p)[:-5] for p in PARETO])
+def test_pareto_files_verified_and_executable(path):
+    js = open(path).read().strip()
+    assert sccl.verify(js) == []
+    d = json.loads(js)
+    ar = sccl.compose_allreduce(sccl.invert(js), js)
+    for sched, dt in ((js, O.U8), (ar, O.BF16)):
+        dd = json.loads(sched)
+        nb = 8 * 300
+        ins = O.seeded_inputs(dd["collective"], d["P"], nb, dt, 4)
+        ref = O.execute(dd, ins, nb, dt)
+        p = sccl.LoopbackPlan(sched, nb, dt, device=-1)
+        outs = [np.zeros_like(r) for r in ref]
+        p.interpret_on_cpu(ins, outs)
+        assert all(np.array_equal(a, b) for a, b in zip(outs, ref))
+
+
+@pytest.mark.skipif(shutil.which(os.environ.get("SCCL_SOLVER", "z3")) is None, reason="no SMT solver")
+def test_pareto_synthesize_small():
+    from paper_2008_08708_b200 import synth
+    assert synth.diameter("ring:8") == 4 and synth.diameter("dgx1") == 2
+    from fractions import Fraction
+    assert synth.bandwidth_lower_bound("allgather", "dgx1") == Fraction(7, 6)  # PAPER §2.4
+    fr = synth.pareto_synthesize("allgather", "ring:4", 1, max_steps=4, timeout=60)
+    assert [(e["C"], e["S"], e["R"]) for e in fr] == [(2, 2, 3)]
