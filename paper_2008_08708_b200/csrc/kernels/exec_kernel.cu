@@ -791,40 +791,13 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
   __shared__ const char* s_inp[kMaxOpIn];
   __shared__ char* s_outp[kMaxOpOut];
   __shared__ uint8_t s_inll[kMaxOpIn], s_outll[kMaxOpOut];
-  __shared__ uint32_t s_rng[6];
-  extern __shared__ __align__(16) uint8_t ll_prog[];  // this CTA's ops / ins / outs
-  const int pidx = rank * p.kc + cg;
   if (tid == 0) {
     s_e = p.epochs[blockIdx.x] + 1;
     s_entry_mask = 1u << rank;
-  } else if (tid <= 2) {
-    s_rng[tid - 1] = p.prog[pidx + tid - 1];
-  } else if (tid <= 6) {
-    s_rng[tid - 1] = p.progx[4 * pidx + tid - 3];
   }
   __syncthreads();
   const uint64_t e = s_e;
   const uint32_t ef = uint32_t(e);
-  const uint32_t ob = s_rng[0], oe = s_rng[1];
-  // stage the whole program in shared memory in one cooperative pass: no
-  // dependent global loads per op on the latency path
-  const DevOp* ops = p.ops;
-  const DevIn* ins = p.ins;
-  const DevOut* outs = p.outs;
-  if (p.ll_smem > 0) {
-    const uint32_t nop = oe - ob, nin = s_rng[3] - s_rng[2], nout = s_rng[5] - s_rng[4];
-    uint4* d = reinterpret_cast<uint4*>(ll_prog);
-    const uint4* so = reinterpret_cast<const uint4*>(p.ops + ob);
-    const uint4* si = reinterpret_cast<const uint4*>(p.ins + s_rng[2]);
-    const uint4* sx = reinterpret_cast<const uint4*>(p.outs + s_rng[4]);
-    const uint32_t wo = nop * (sizeof(DevOp) / 16), wi = nin * (sizeof(DevIn) / 16), wx = nout * (sizeof(DevOut) / 16);
-    for (uint32_t k = tid; k < wo + wi + wx; k += LL_NT)
-      d[k] = k < wo ? so[k] : k < wo + wi ? si[k - wo] : sx[k - wo - wi];
-    ops = reinterpret_cast<const DevOp*>(ll_prog) - ob;
-    ins = reinterpret_cast<const DevIn*>(ll_prog + wo * 16) - s_rng[2];
-    outs = reinterpret_cast<const DevOut*>(ll_prog + (wo + wi) * 16) - s_rng[4];
-    __syncthreads();
-  }
   uint64_t* const myflags = reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]);
   if (p.multiprocess)
     for (int t = tid; t < p.P; t += LL_NT)
@@ -833,11 +806,12 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
         st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[t][SP_FLAGS_IDX]) + p.entry_base + rank * p.nch + ch, e);
       }
 
+  const uint32_t ob = p.prog[rank * p.kc + cg], oe = p.prog[rank * p.kc + cg + 1];
   for (uint32_t oi = ob; oi < oe; ++oi) {
-    const DevOp op = ops[oi];
+    const DevOp op = p.ops[oi];
     if (op.kind == 2) {  // receipts nobody forwards: consume them
       for (int i = 0; i < op.nin; ++i) {
-        const DevIn in = ins[op.in_begin + i];
+        const DevIn in = p.ins[op.in_begin + i];
         if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
         const DPart q = dsplit16(int64_t(in.len), p.kb, cb);
         const char* slot = p.base[in.rank][in.space] + in.off + 2 * q.off;
@@ -851,12 +825,12 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
     const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
     if (q.len == 0) continue;
     if (tid < op.nin) {
-      const DevIn in = ins[op.in_begin + tid];
+      const DevIn in = p.ins[op.in_begin + tid];
       s_inll[tid] = in.flag >= 0;
       s_inp[tid] = p.base[in.rank][in.space] + in.off + (in.flag >= 0 ? 2 * q.off : q.off);
     }
     if (tid < op.nout) {
-      const DevOut d = outs[op.out_begin + tid];
+      const DevOut d = p.outs[op.out_begin + tid];
       s_outll[tid] = d.flag >= 0;
       s_outp[tid] = p.base[d.rank][d.space] + d.off + (d.flag >= 0 ? 2 * q.off : q.off);
       if (p.multiprocess && d.rank != rank && !(atomicOr(&s_entry_mask, 0u) & (1u << d.rank))) {
@@ -932,18 +906,12 @@ cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st) 
   const void* f = kernel_for(dtype, sys, p.ll != 0);
   if (!f) return cudaErrorInvalidValue;
   void* args[] = {const_cast<KParams*>(&p)};
-  if (p.ll) return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(LL_NT), args, size_t(p.ll_smem), st);
+  if (p.ll) return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(LL_NT), args, 0, st);
   cudaError_t err = prepare(f);
   if (err != cudaSuccess) return err;
   return cudaLaunchKernel(f, dim3(p.nranks_launch * p.nch), dim3(NT), args, smem_bytes(p.tile, p.nstage), st);
 }
 
-
-cudaError_t exec_ll_occupancy(int dtype, bool sys, int smem, int* blocks_per_sm) {
-  const void* f = kernel_for(dtype, sys, true);
-  if (!f) return cudaErrorInvalidValue;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, LL_NT, size_t(smem));
-}
 
 cudaError_t exec_occupancy(int dtype, bool sys, int tile, int nstage, int* blocks_per_sm) {
   // tile == 0: the LL kernel (no dynamic shared memory)

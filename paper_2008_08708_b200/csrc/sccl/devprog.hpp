@@ -55,8 +55,6 @@ struct KParams {
   const DevIn* ins;
   const DevOut* outs;
   const uint32_t* prog;  // [P*kc+1] op ranges per (rank, chunk group)
-  const uint32_t* progx; // [P*kc][4]: ins begin/end, outs begin/end per (rank, chunk group)
-  int ll_smem;           // LL kernel: bytes to stage a CTA's whole program in smem (0 = read global)
   uint64_t* epochs;      // [nranks_launch * nch] per-CTA launch counters
   int* errinfo;          // host-mapped watchdog record
   long long timeout_ns;

@@ -15,7 +15,6 @@
 namespace sccl {
 cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st);
 cudaError_t exec_occupancy(int dtype, bool sys, int tile, int nstage, int* blocks_per_sm);
-cudaError_t exec_ll_occupancy(int dtype, bool sys, int smem, int* blocks_per_sm);
 int exec_threads();
 }  // namespace sccl
 
@@ -238,21 +237,6 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
       }
     }
   p.prog[size_t(P) * p.kc] = uint32_t(p.ops.size());
-  // ins/outs ranges per (rank, chunk group): contiguous because they were
-  // pushed in op order; lets the LL kernel stage its program in one pass
-  p.progx.assign(size_t(P) * p.kc * 4, 0);
-  size_t maxblob = 0;
-  for (size_t i = 0; i + 1 < p.prog.size(); ++i) {
-    const uint32_t ob = p.prog[i], oe = p.prog[i + 1];
-    const uint32_t ib = ob < oe ? p.ops[ob].in_begin : 0, ie = ob < oe ? p.ops[oe - 1].in_begin + p.ops[oe - 1].nin : 0;
-    const uint32_t xb = ob < oe ? p.ops[ob].out_begin : 0, xe = ob < oe ? p.ops[oe - 1].out_begin + p.ops[oe - 1].nout : 0;
-    p.progx[4 * i + 0] = ib;
-    p.progx[4 * i + 1] = ie;
-    p.progx[4 * i + 2] = xb;
-    p.progx[4 * i + 3] = xe;
-    maxblob = std::max(maxblob, (oe - ob) * sizeof(DevOp) + (ie - ib) * sizeof(DevIn) + (xe - xb) * sizeof(DevOut));
-  }
-  p.ll_smem = maxblob <= 32768 ? int(maxblob) : 0;
 
   // memory layout of one rank's region
   auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
@@ -282,7 +266,6 @@ void plan_device_setup(sccl_plan& p) {
   upload(p.ins, &p.d_ins);
   upload(p.outs, &p.d_outs);
   upload(p.prog, &p.d_prog);
-  upload(p.progx, &p.d_progx);
   int nlaunch = p.loopback ? p.nranks : 1;
   size_t ne = size_t(nlaunch) * p.nch;
   cuda_check(cudaMalloc(&p.d_epochs, ne * sizeof(uint64_t)), "cudaMalloc(epochs)");
@@ -322,8 +305,6 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.ins = p.d_ins;
   k.outs = p.d_outs;
   k.prog = p.d_prog;
-  k.progx = p.d_progx;
-  k.ll_smem = p.ll_smem;
   k.epochs = p.d_epochs;
   k.errinfo = p.d_err;
   k.timeout_ns = p.timeout_ns;
@@ -420,12 +401,6 @@ static int create_common(const char* json, int rank, int nranks, size_t bytes, i
         req.ctx = &occ;
       }
       plan_build_host(*p, json, rank, nranks, int64_t(bytes), dtype, redop, o.device, req, o.timeout_ms, loopback);
-      if (p->ll && p->ll_smem > 0 && o.device >= 0) {
-        // staging the program in smem must not break co-residency
-        int bps = 0;
-        cuda_check(exec_ll_occupancy(dtype, !loopback, p->ll_smem, &bps), "occupancy");
-        if (loopback && p->nch * p->nranks > req.sms * bps) p->ll_smem = 0;
-      }
       if (loopback && p->nch * p->nranks > p->resident_cap)
         throw invalid_argument_error("loopback needs P*nchannels <= resident CTAs (" +
                                      std::to_string(p->resident_cap) + ")");
@@ -650,7 +625,6 @@ int sccl_plan_destroy(sccl_plan* p) {
     cudaFree(p->d_ins);
     cudaFree(p->d_outs);
     cudaFree(p->d_prog);
-    cudaFree(p->d_progx);
     cudaFree(p->d_epochs);
     cudaFree(p->d_region);
     if (p->h_err) cudaFreeHost(p->h_err);

@@ -27,15 +27,12 @@ struct sccl_plan {
   std::vector<sccl::DevIn> ins;
   std::vector<sccl::DevOut> outs;
   std::vector<uint32_t> prog;  // [P*kc+1]: op range per (rank, chunk group)
-  std::vector<uint32_t> progx; // [P*kc][4]: ins / outs ranges of the same
-  int ll_smem = 0;             // max bytes of one CTA's program (LL staging), 0 if too large
 
   // device program
   sccl::DevOp* d_ops = nullptr;
   sccl::DevIn* d_ins = nullptr;
   sccl::DevOut* d_outs = nullptr;
   uint32_t* d_prog = nullptr;
-  uint32_t* d_progx = nullptr;
   uint64_t* d_epochs = nullptr;
 
   // plan memory: per rank region = [flags | scratch | recv (multi-process)]
