@@ -304,7 +304,9 @@ def verify(sched: dict, topo: Optional[dict] = None) -> List[Tuple[str, int, int
     """Verify every phase; returns violations as (kind, step, chunk, src, dst)."""
     out = []
     for ph in _phases(sched):
-        t = topo or topology_by_name(ph["topology"]["name"])
+        tj = ph["topology"]
+        t = topo or ({"name": tj["name"], "P": ph["P"], "constraints": tj["constraints"]}
+                     if "constraints" in tj else topology_by_name(tj["name"]))
         P, G = ph["P"], ph["G"]
         kind = ph["collective"]
         a, b = pre_post(kind, G, P, ph.get("root", 0) or 0)

@@ -215,3 +215,29 @@ REGISTRY = {
     "b2": ring4_s2r2,
     "b3": dgx1_allgather_122,
 }
+
+
+def random_allgather(P: int, C: int, S: int, seed: int = 0) -> dict:
+    """A random valid allgather for fuzzing the lowering and kernels: chunk
+    i*P+n spreads from rank n along a random tree; a rank that gets the
+    chunk at step t forwards it at some later step (so multi-hop relays,
+    fan-out and uneven per-step traffic all occur).  The topology is given
+    inline as the complete digraph with a bound that admits every step."""
+    rng = random.Random(seed)
+    G = P * C
+    sends = []
+    for c in range(G):
+        have = {c % P: -1}  # rank -> step it received the chunk (-1: owner)
+        todo = [r for r in range(P) if r != c % P]
+        rng.shuffle(todo)
+        for dst in todo:
+            srcs = [r for r, t in have.items() if t < S - 1]
+            src = rng.choice(srcs)
+            step = rng.randint(have[src] + 1, S - 1)
+            have[dst] = step
+            sends.append((c, src, dst, step))
+    bound = G
+    cons = [{"edges": [[a, b]], "bound": bound} for a in range(P) for b in range(P) if a != b]
+    d = _sched("allgather", f"full:{P}", P, G, C, [1] * S, sends)
+    d["topology"] = {"name": f"dense:{P}", "constraints": cons}
+    return d
