@@ -206,6 +206,19 @@ Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
     }
     ops.swap(merged);
 
+    // within a step, send to the next rank first, then the one after, ...
+    // (rank r starts at r+1): every destination receives its first
+    // receipts at the same time instead of all ranks feeding rank 0 first,
+    // which starts every receiver's dependent work (reduce, forward) evenly
+    auto dist = [&](const Op& op) {
+      int d = P;
+      for (auto& o : op.outs)
+        if (o.loc.rank != r) d = std::min(d, (o.loc.rank - r + P) % P);
+      return d;
+    };
+    std::stable_sort(ops.begin(), ops.end(),
+                     [&](const Op& a, const Op& z) { return a.key != z.key ? a.key < z.key : dist(a) < dist(z); });
+
     // F2: fold copies that read a reduce's result into the reduce (fused
     // receive-reduce-forward, "reduce on receipt")
     for (size_t i = 0; i < ops.size(); ++i) {
