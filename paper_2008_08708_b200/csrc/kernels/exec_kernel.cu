@@ -43,7 +43,6 @@ static_assert(NT == (3 + NCW) * 32, "thread layout");
 constexpr int CW0 = 3;               // first compute warp
 constexpr int NPART = NT - 32;       // threads of the unaligned path (all but the signaler)
 constexpr int SIGQ = 64;             // storer -> signaler queue entries
-constexpr int ORDQ = 32;             // producer -> consumers op-order ring (> stages in flight)
 constexpr int NSTAGE = kMaxStages;   // barrier sets; stages in use = KParams::nstage
 constexpr int FIFO = 8;              // storer's in-flight tile records (> max sig_lag)
 constexpr uint64_t kStorerPatienceNs = 3000;  // storer spins this long before draining
@@ -150,26 +149,9 @@ __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
   return v;
 }
 
-// Watchdog: the diagnostic goes to host-mapped memory and the kernel traps
+// Spin until *f >= target; returns the value seen.  Watchdog: after
+// timeout_ns the diagnostic goes to host-mapped memory and the kernel traps
 // (the host maps it to SCCL_PEER_TIMEOUT).
-__device__ __noinline__ void watchdog_fire(const KParams& p, int rank, int ch, int op, int slot, uint64_t target,
-                                           uint64_t seen) {
-  volatile int* e = p.errinfo;
-  if (e && atomicCAS(p.errinfo, 0, -1) == 0) {
-    e[1] = rank;
-    e[2] = ch;
-    e[3] = op;
-    e[4] = slot;
-    e[5] = int(target & 0x7fffffff);
-    e[6] = int(seen & 0x7fffffff);
-    __threadfence_system();
-    e[0] = ERR_TIMEOUT;
-    __threadfence_system();
-  }
-  __trap();
-}
-
-// Spin until *f >= target; returns the value seen.  Bounded by timeout_ns.
 template <bool SYS>
 __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p, int rank, int ch, int op,
                             int slot) {
@@ -179,8 +161,21 @@ __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p
   uint32_t spins = 0;
   while ((v = ld_acquire<SYS>(f)) < target) {
     if (++spins > 64) __nanosleep(32);
-    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
-      watchdog_fire(p, rank, ch, op, slot, target, v);
+    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+      volatile int* e = p.errinfo;
+      if (e && atomicCAS(p.errinfo, 0, -1) == 0) {
+        e[1] = rank;
+        e[2] = ch;
+        e[3] = op;
+        e[4] = slot;
+        e[5] = int(target & 0x7fffffff);
+        e[6] = int(v & 0x7fffffff);
+        __threadfence_system();
+        e[0] = ERR_TIMEOUT;
+        __threadfence_system();
+      }
+      __trap();
+    }
   }
   return v;
 }
@@ -336,8 +331,6 @@ struct Smem {
   volatile uint32_t completed_seq;  // storer: tiles < completed_seq fully written
   volatile uint32_t producer_blocked;  // producer spins on a peer's counter
   uint32_t entry_mask;
-  uint32_t order[ORDQ];             // op indices in the order the producer runs them
-  uint32_t o_head;                  // producer publishes (release/acquire, cta)
 };
 static_assert(sizeof(Smem) <= SMEM_HDR, "smem header");
 
@@ -368,7 +361,6 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
     }
     S.completed_seq = 0;
     S.q_head = S.q_tail = S.q_done = 0;
-    S.o_head = 0;
     S.producer_blocked = 0;
     S.entry_mask = 1u << rank;
     s_e = p.epochs[blockIdx.x] + 1;
@@ -419,320 +411,210 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
     while (f_head != f_tail) signal_entry(f_head++);
   };
 
-  // ---------------------------------------------------------------- ops
-  struct OpGeom {
-    DevOp op;
-    DPart q;
-    uint64_t fbase;
-    uint32_t T, ntiles;
-  };
-  auto geom = [&](uint32_t oi) {
-    OpGeom g;
-    g.op = p.ops[oi];
-    g.q = dsplit16(int64_t(g.op.len), p.kb, cb);
-    g.fbase = (e - 1) * uint64_t(g.q.len);
-    g.T = g.op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / max(1, int(g.op.nin))) & ~15u);
-    g.ntiles = uint32_t((g.q.len + g.T - 1) / g.T);
-    return g;
-  };
-
-  // ---- unaligned op: whole CTA but the signaler, element-wise, synchronous
-  auto do_unaligned = [&](const OpGeom& g, uint32_t oi) {
-    const DevOp& op = g.op;
-    const int ptid = warp < 2 ? tid : tid - 32;
-    if (warp == 1 && lane == 0) drain();
-    named_sync(1);
-    if (tid < op.nin) {
-      const DevIn in = p.ins[op.in_begin + tid];
-      s_inp[tid] = p.base[in.rank][in.space] + in.off;
-      if (in.flag >= 0)
-        wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, g.fbase + uint64_t(g.q.len), p, rank, ch, int(oi - ob),
-                     in.flag);
-    }
-    if (tid < op.nout) {
-      const DevOut d = p.outs[op.out_begin + tid];
-      s_outp[tid] = p.base[d.rank][d.space] + d.off;
-      if (p.multiprocess && d.rank != rank && !(atomicOr(&S.entry_mask, 0u) & (1u << d.rank))) {
-        wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
-        atomicOr(&S.entry_mask, 1u << d.rank);
-      }
-    }
-    named_sync(1);
-    if (op.kind == 0) elem_op<0>(s_inp, 1, s_outp, op.nout, g.q.off, g.q.len, ptid, NPART);
-    else elem_op<DT>(s_inp, op.nin, s_outp, op.nout, g.q.off, g.q.len, ptid, NPART);
-    named_sync(1);
-    if (warp == 1 && lane == 0) {
-      fence_rel<SYS>();
-      for (int o = 0; o < op.nout; ++o) {
-        const DevOut d = p.outs[op.out_begin + o];
-        if (d.flag >= 0)
-          st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
-                          g.fbase + uint64_t(g.q.len));
-      }
-      S.completed_seq = seq + 1;
-    }
-    named_sync(1);
-    ++seq;
-  };
-
-  // ---- producer (warp 0): loads every input tile once its counter allows
-  auto produce = [&](const OpGeom& g, uint32_t oi) {
-    const DevOp& op = g.op;
-    uint64_t ready = 0;  // lane k tracks input k's counter (k < 32)
-    const char* src = nullptr;
-    int32_t flag = -1;
-    if (lane < op.nin) {
-      const DevIn in = p.ins[op.in_begin + lane];
-      src = p.base[in.rank][in.space] + in.off + g.q.off;
-      flag = in.flag;
-    }
-    if (op.raw && lane == 0)  // input written by an earlier op of this CTA: the storer drains first
-      while (S.completed_seq < seq) __nanosleep(32);
-    __syncwarp();
-    for (uint32_t t = 0; t < g.ntiles; ++t, ++it) {
-      const uint32_t s = it % NST, ph = (it / NST) & 1;
-      const uint64_t lo = uint64_t(t) * g.T;
-      const uint32_t n = uint32_t(min(uint64_t(g.T), uint64_t(g.q.len) - lo));
-      const uint32_t nv = n & ~15u;
-      if (flag >= 0) {
-        const uint64_t need = g.fbase + lo + n;
-        const uint64_t* f = myflags + uint64_t(flag) * p.nch + ch;
-        if (ready < need) ready = ld_acquire<SYS>(f);
-        if (ready < need) {  // a peer is behind: let the storer publish what it holds
-          S.producer_blocked = 1;
-          ready = wait_ge<SYS>(f, need, p, rank, ch, int(oi - ob), flag);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) S.producer_blocked = 0;
-      __syncwarp();
-      if (lane == 0) {
-        mbar_wait(&S.empty[s], ph ^ 1);
-        mbar_arrive_tx(&S.full[s], nv * op.nin);
-      }
-      __syncwarp();
-      if (lane < op.nin && nv) {
-        fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
-        bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * g.T, src + lo, nv, &S.full[s]);
-      }
-    }
-    seq += g.ntiles;
-  };
-
-  // ---- compute warps: REDUCE ops accumulate in smem; others just pass
-  auto compute = [&](const OpGeom& g) {
-    const DevOp& op = g.op;
-    for (uint32_t t = 0; t < g.ntiles; ++t, ++it) {
-      const uint32_t s = it % NST, ph = (it / NST) & 1;
-      mbar_wait(&S.full[s], ph);
-      if (op.kind == 1) {
-        const uint64_t lo = uint64_t(t) * g.T;
-        const uint32_t nv = uint32_t(min(uint64_t(g.T), uint64_t(g.q.len) - lo)) >> 4;
-        uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
-        for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
-          Vec<DT> acc;
-          acc.init(b0[v]);
-          for (int k = 1; k < op.nin; ++k)
-            acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * g.T)[v]);
-          b0[v] = acc.out();
-        }
-        fence_proxy_async_smem();
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.ready[s]);
-    }
-    seq += g.ntiles;
-  };
-
-  // ---- storer (warp 1, lane 0): bulk stores to every destination
-  auto store = [&](const OpGeom& g, uint32_t oi) {
-    const DevOp& op = g.op;
-    if (lane != 0) {
-      it += g.ntiles;
-      seq += g.ntiles;
-      return;
-    }
-    if (op.raw) drain();  // the producer waits for every earlier tile to be written
-    for (int o = 0; o < op.nout; ++o) {
-      const DevOut d = p.outs[op.out_begin + o];
-      s_outp[o] = p.base[d.rank][d.space] + d.off + g.q.off;
-      if (p.multiprocess && d.rank != rank && !(S.entry_mask & (1u << d.rank))) {
-        drain();  // never block while holding completed-but-unsignalled tiles
-        wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
-        S.entry_mask |= 1u << d.rank;
-      }
-    }
-    for (uint32_t t = 0; t < g.ntiles; ++t, ++it, ++seq) {
-      const uint32_t s = it % NST, ph = (it / NST) & 1;
-      const uint64_t lo = uint64_t(t) * g.T;
-      const uint32_t n = uint32_t(min(uint64_t(g.T), uint64_t(g.q.len) - lo));
-      const uint32_t nv = n & ~15u;
-      if (!mbar_try(&S.ready[s], ph)) {
-        // Not ready.  A short wait is the producer catching up; a long one
-        // may be a peer dependency that itself waits for our pending tiles
-        // -- retire and signal everything before blocking.
-        const uint64_t t0 = globaltimer();
-        bool ok = false;
-        while (!(ok = mbar_try(&S.ready[s], ph)) && !S.producer_blocked && globaltimer() - t0 < kStorerPatienceNs) {
-        }
-        if (!ok) {
-          drain();
-          mbar_wait(&S.ready[s], ph);
-        }
-      }
-      if (n > nv) {  // < 16 B chunk tail: element-wise, global -> global
-        const char* in[kMaxOpIn];
-        for (int k = 0; k < op.nin; ++k) {
-          const DevIn x = p.ins[op.in_begin + k];
-          in[k] = p.base[x.rank][x.space] + x.off + g.q.off;
-        }
-        if (op.kind == 0) elem_op<0>(in, 1, s_outp, op.nout, int64_t(lo + nv), n - nv, 0, 1);
-        else elem_op<DT>(in, op.nin, s_outp, op.nout, int64_t(lo + nv), n - nv, 0, 1);
-      }
-      if (nv)
-        for (int o = 0; o < op.nout; ++o) bulk_store(s_outp[o] + lo, bufs + size_t(s) * STAGE, nv);
-      bulk_commit();
-      const uint32_t x = f_tail % FIFO;
-      f_stage[x] = s;
-      f_op[x] = oi;
-      f_seq[x] = seq;
-      f_end[x] = lo + n;
-      f_last[x] = t + 1 == g.ntiles;
-      ++f_tail;
-      // smem of all but the newest group has been read: release stages
-      bulk_wait_read<1>();
-      while (f_tail - f_rel > 1) mbar_arrive(&S.empty[f_stage[(f_rel++) % FIFO]]);
-      // all but the newest sig_lag groups are complete: release counters
-      if (f_tail - f_head > uint32_t(p.sig_lag)) {
-        switch (p.sig_lag) {
-          case 0: bulk_wait<0>(); break;
-          case 1: bulk_wait<1>(); break;
-          case 2: bulk_wait<2>(); break;
-          case 3: bulk_wait<3>(); break;
-          case 4: bulk_wait<4>(); break;
-          case 5: bulk_wait<5>(); break;
-          default: bulk_wait<6>(); break;
-        }
-        while (f_tail - f_head > uint32_t(p.sig_lag)) signal_entry(f_head++);
-      }
-    }
-  };
-
-  constexpr uint32_t kEnd = 0xffffffffu;
-  if (warp == 0) {
-    // ================= producer: picks the order =================
-    // Ops of one group (same step, independent) run in the order their
-    // first tile becomes available, so a CTA never idles behind a slow
-    // peer while another input of the same step has already landed.  The
-    // chosen order is published to the compute warps and the storer.
-    auto publish = [&](uint32_t oi) {
-      if (lane == 0) {
-        const uint32_t h = S.o_head;
-        S.order[h % ORDQ] = oi;
-        st_release_cta(&S.o_head, h + 1);
-      }
-      __syncwarp();
-    };
-    uint32_t oi = ob;
-    while (oi < oe) {
-      const DevOp op0 = p.ops[oi];
-      if (op0.kind == 2) {  // end-of-program waits: every receipt has landed
-        for (int i = lane; i < op0.nin; i += 32) {
-          const DevIn in = p.ins[op0.in_begin + i];
+  for (uint32_t oi = ob; oi < oe; ++oi) {
+    const DevOp op = p.ops[oi];
+    if (op.kind == 2) {  // end-of-program waits: every receipt has landed
+      if (warp == 0)
+        for (int i = lane; i < op.nin; i += 32) {
+          const DevIn in = p.ins[op.in_begin + i];
+          if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
           const DPart q = dsplit16(int64_t(in.len), p.kb, cb);
           if (q.len) wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, e * uint64_t(q.len), p, rank, ch,
                                   int(oi - ob), in.flag);
         }
+      continue;
+    }
+    if (int(op.chunk % uint32_t(p.kc)) != cg) continue;  // another channel's chunk group
+    const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
+    if (q.len == 0) continue;  // empty sub-range: nothing sent, nothing awaited
+    const uint64_t fbase = (e - 1) * uint64_t(q.len);
+
+    if (!op.vec) {
+      // ---- unaligned op: whole CTA (but the signaler), element-wise, synchronous ----
+      if (warp == 2) continue;
+      const int ptid = warp < 2 ? tid : tid - 32;
+      if (warp == 1 && lane == 0) drain();
+      named_sync(1);
+      if (tid < op.nin) {
+        const DevIn in = p.ins[op.in_begin + tid];
+        s_inp[tid] = p.base[in.rank][in.space] + in.off;
+        if (in.flag >= 0)
+          wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, fbase + uint64_t(q.len), p, rank, ch, int(oi - ob),
+                       in.flag);
+      }
+      if (tid < op.nout) {
+        const DevOut d = p.outs[op.out_begin + tid];
+        s_outp[tid] = p.base[d.rank][d.space] + d.off;
+        if (p.multiprocess && d.rank != rank && !(atomicOr(&S.entry_mask, 0u) & (1u << d.rank))) {
+          wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
+          atomicOr(&S.entry_mask, 1u << d.rank);
+        }
+      }
+      named_sync(1);
+      if (op.kind == 0) elem_op<0>(s_inp, 1, s_outp, op.nout, q.off, q.len, ptid, NPART);
+      else elem_op<DT>(s_inp, op.nin, s_outp, op.nout, q.off, q.len, ptid, NPART);
+      named_sync(1);
+      if (warp == 1 && lane == 0) {
+        fence_rel<SYS>();
+        for (int o = 0; o < op.nout; ++o) {
+          const DevOut d = p.outs[op.out_begin + o];
+          if (d.flag >= 0)
+            st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
+                            fbase + uint64_t(q.len));
+        }
+        S.completed_seq = seq + 1;
+      }
+      named_sync(1);
+      ++seq;
+      continue;
+    }
+
+    // ---- pipelined op ----
+    const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
+    const uint32_t ntiles = uint32_t((q.len + T - 1) / T);
+
+    if (warp == 0) {
+      // ================= producer =================
+      uint64_t ready = 0;  // lane k tracks input k's counter (k < 32)
+      const char* src = nullptr;
+      int32_t flag = -1;
+      if (lane < op.nin) {
+        const DevIn in = p.ins[op.in_begin + lane];
+        src = p.base[in.rank][in.space] + in.off + q.off;
+        flag = in.flag;
+      }
+      if (op.raw && lane == 0)  // input written by an earlier op of this CTA: the storer drains first
+        while (S.completed_seq < seq) __nanosleep(32);
+      __syncwarp();
+      for (uint32_t t = 0; t < ntiles; ++t, ++it) {
+        const uint32_t s = it % NST, ph = (it / NST) & 1;
+        const uint64_t lo = uint64_t(t) * T;
+        const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
+        const uint32_t nv = n & ~15u;
+        if (flag >= 0) {
+          const uint64_t need = fbase + lo + n;
+          const uint64_t* f = myflags + uint64_t(flag) * p.nch + ch;
+          if (ready < need) ready = ld_acquire<SYS>(f);
+          if (ready < need) {  // a peer is behind: let the storer publish what it holds
+            S.producer_blocked = 1;
+            ready = wait_ge<SYS>(f, need, p, rank, ch, int(oi - ob), flag);
+          }
+        }
         __syncwarp();
-        ++oi;
-        continue;
-      }
-      const uint32_t gend = min(oe, max(oi + 1, op0.group_end));
-      if (gend == oi + 1) {
-        const OpGeom g = geom(oi);
-        if (g.q.len) {
-          publish(oi);
-          if (!g.op.vec) do_unaligned(g, oi);
-          else produce(g, oi);
-        }
-        ++oi;
-        continue;
-      }
-      // a group: lane j watches op oi + j
-      OpGeom mine{};
-      bool live = false;
-      if (oi + lane < gend) {
-        mine = geom(oi + lane);
-        live = mine.q.len > 0;
-      }
-      uint32_t pending = __ballot_sync(0xffffffffu, live);
-      uint64_t t0 = 0;
-      while (pending) {
-        bool rdy = false;
-        if ((pending >> lane) & 1) {
-          rdy = true;
-          const uint64_t need = mine.fbase + min(uint64_t(mine.q.len), uint64_t(mine.T));
-          for (int k = 0; k < mine.op.nin && rdy; ++k) {
-            const DevIn in = p.ins[mine.op.in_begin + k];
-            if (in.flag >= 0) rdy = ld_acquire<SYS>(myflags + uint64_t(in.flag) * p.nch + ch) >= need;
-          }
-        }
-        uint32_t rmask = __ballot_sync(0xffffffffu, rdy) & pending;
-        if (!rmask) {  // nothing landed yet: the storer may publish its tiles
-          if (lane == 0) S.producer_blocked = 1;
-          if (!t0) t0 = globaltimer();
-          else if (p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
-            const int j = __ffs(pending) - 1;  // report the first waiting op
-            if (lane == j) watchdog_fire(p, rank, ch, int(oi + j - ob), -4, 0, 0);
-          }
-          __nanosleep(64);
-          continue;
-        }
         if (lane == 0) S.producer_blocked = 0;
-        const int j = __ffs(rmask) - 1;
-        pending &= ~(1u << j);
-        OpGeom g;
-        g.op = p.ops[oi + j];
-        g.q = dsplit16(int64_t(g.op.len), p.kb, cb);
-        g.fbase = (e - 1) * uint64_t(g.q.len);
-        g.T = __shfl_sync(0xffffffffu, mine.T, j);
-        g.ntiles = __shfl_sync(0xffffffffu, mine.ntiles, j);
-        publish(oi + j);
-        produce(g, oi + j);
-        t0 = 0;
-      }
-      oi = gend;
-    }
-    publish(kEnd);
-  } else if (warp != 2) {
-    // ========== compute warps / storer: follow the producer's order ==========
-    uint32_t tail = 0;
-    for (;;) {
-      uint32_t h = ld_acquire_cta(&S.o_head);
-      if (h == tail) {
-        // the storer must not wait here holding completed, unsignalled tiles
-        if (warp == 1 && lane == 0) {
-          const uint64_t t0 = globaltimer();
-          while ((h = ld_acquire_cta(&S.o_head)) == tail && !S.producer_blocked &&
-                 globaltimer() - t0 < kStorerPatienceNs) {
-          }
-          if (h == tail) drain();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_wait(&S.empty[s], ph ^ 1);
+          mbar_arrive_tx(&S.full[s], nv * op.nin);
         }
-        while ((h = ld_acquire_cta(&S.o_head)) == tail) __nanosleep(20);
+        __syncwarp();
+        if (lane < op.nin && nv) {
+          fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
+          bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, &S.full[s]);
+        }
       }
-      const uint32_t oi = S.order[tail % ORDQ];
-      ++tail;
-      if (oi == kEnd) break;
-      const OpGeom g = geom(oi);
-      if (!g.op.vec) do_unaligned(g, oi);
-      else if (warp >= CW0) compute(g);
-      else store(g, oi);
+    } else if (warp == 2) {
+      // signaler: runs its own loop below
+    } else if (warp >= CW0) {
+      // ================= compute (REDUCE only; others just pass) =================
+      for (uint32_t t = 0; t < ntiles; ++t, ++it) {
+        const uint32_t s = it % NST, ph = (it / NST) & 1;
+        mbar_wait(&S.full[s], ph);
+        if (op.kind == 1) {
+          const uint64_t lo = uint64_t(t) * T;
+          const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
+          uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
+          for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
+            Vec<DT> acc;
+            acc.init(b0[v]);
+            for (int k = 1; k < op.nin; ++k) acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T)[v]);
+            b0[v] = acc.out();
+          }
+          fence_proxy_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.ready[s]);
+      }
+    } else {
+      // ================= storer (warp 1, lane 0) =================
+      if (lane == 0) {
+        if (op.raw) drain();  // the producer waits for every earlier tile to be written
+        for (int o = 0; o < op.nout; ++o) {
+          const DevOut d = p.outs[op.out_begin + o];
+          s_outp[o] = p.base[d.rank][d.space] + d.off + q.off;
+          if (p.multiprocess && d.rank != rank && !(S.entry_mask & (1u << d.rank))) {
+            drain();  // never block while holding completed-but-unsignalled tiles
+            wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
+            S.entry_mask |= 1u << d.rank;
+          }
+        }
+        for (uint32_t t = 0; t < ntiles; ++t, ++it, ++seq) {
+          const uint32_t s = it % NST, ph = (it / NST) & 1;
+          const uint64_t lo = uint64_t(t) * T;
+          const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
+          const uint32_t nv = n & ~15u;
+          if (!mbar_try(&S.ready[s], ph)) {
+            // Not ready.  A short wait is the producer catching up; a long
+            // one may be a peer dependency that itself waits for our
+            // pending tiles -- retire and signal everything before blocking.
+            const uint64_t t0 = globaltimer();
+            bool ok = false;
+            while (!(ok = mbar_try(&S.ready[s], ph)) && !S.producer_blocked &&
+                   globaltimer() - t0 < kStorerPatienceNs) {
+            }
+            if (!ok) {
+              drain();
+              mbar_wait(&S.ready[s], ph);
+            }
+          }
+          if (n > nv) {  // < 16 B chunk tail: element-wise, global -> global
+            const char* in[kMaxOpIn];
+            for (int k = 0; k < op.nin; ++k) {
+              const DevIn x = p.ins[op.in_begin + k];
+              in[k] = p.base[x.rank][x.space] + x.off + q.off;
+            }
+            if (op.kind == 0) elem_op<0>(in, 1, s_outp, op.nout, int64_t(lo + nv), n - nv, 0, 1);
+            else elem_op<DT>(in, op.nin, s_outp, op.nout, int64_t(lo + nv), n - nv, 0, 1);
+          }
+          if (nv)
+            for (int o = 0; o < op.nout; ++o) bulk_store(s_outp[o] + lo, bufs + size_t(s) * STAGE, nv);
+          bulk_commit();
+          const uint32_t x = f_tail % FIFO;
+          f_stage[x] = s;
+          f_op[x] = oi;
+          f_seq[x] = seq;
+          f_end[x] = lo + n;
+          f_last[x] = t + 1 == ntiles;
+          ++f_tail;
+          // smem of all but the newest group has been read: release stages
+          bulk_wait_read<1>();
+          while (f_tail - f_rel > 1) mbar_arrive(&S.empty[f_stage[(f_rel++) % FIFO]]);
+          // all but the newest sig_lag groups are complete: release counters
+          if (f_tail - f_head > uint32_t(p.sig_lag)) {
+            switch (p.sig_lag) {
+              case 0: bulk_wait<0>(); break;
+              case 1: bulk_wait<1>(); break;
+              case 2: bulk_wait<2>(); break;
+              case 3: bulk_wait<3>(); break;
+              case 4: bulk_wait<4>(); break;
+              case 5: bulk_wait<5>(); break;
+              default: bulk_wait<6>(); break;
+            }
+            while (f_tail - f_head > uint32_t(p.sig_lag)) signal_entry(f_head++);
+          }
+        }
+      } else {
+        it += ntiles;
+        seq += ntiles;
+      }
     }
-    if (warp == 1 && lane == 0) {
-      drain();
-      st_release_cta(&S.q_done, 1);
-    }
-  } else if (lane == 0) {
+    if (warp != 1) seq += ntiles;
+  }
+  if (warp == 1 && lane == 0) {
+    drain();
+    st_release_cta(&S.q_done, 1);
+  }
+  if (warp == 2 && lane == 0) {
     // ================= signaler =================
     // release the counters of completed tiles: one fence per batch, then
     // relaxed stores of the (monotone) byte counts
@@ -860,8 +742,21 @@ __device__ uint2 ll_read(const char* slot, int64_t pair, bool two, uint32_t ef, 
     v = ld_ll(a);
     if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
     if (++spins > 32) __nanosleep(20);
-    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
-      watchdog_fire(p, rank, ch, op, -3, ef, v.y);
+    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+      volatile int* e = p.errinfo;
+      if (e && atomicCAS(p.errinfo, 0, -1) == 0) {
+        e[1] = rank;
+        e[2] = ch;
+        e[3] = op;
+        e[4] = -3;
+        e[5] = int(ef);
+        e[6] = int(v.y);
+        __threadfence_system();
+        e[0] = ERR_TIMEOUT;
+        __threadfence_system();
+      }
+      __trap();
+    }
   }
 }
 

@@ -10,7 +10,6 @@ namespace sccl {
 constexpr int kMaxRanks = 16;   // pointer table width (kernel parameter space)
 constexpr int kMaxOpIn = 32;    // inputs of one copy/reduce op (staged in smem)
 constexpr int kMaxOpOut = 32;   // destinations of one op
-constexpr int kMaxGroup = 32;   // ops the producer may reorder at once (one per lane)
 constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
 constexpr int kMaxTile = 65536; // one TMA pipeline stage (bytes)
 constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
@@ -39,7 +38,7 @@ struct DevOut {
 struct DevOp {
   uint64_t len;   // chunk length in bytes
   uint32_t chunk; // chunk id: CTA channel (g, b) runs ops with chunk % kc == g
-  uint32_t group_end;  // ops [this, group_end) are independent (same step): any order
+  uint32_t pad2;
   uint32_t in_begin, out_begin;
   uint16_t nin, nout;
   uint8_t kind;   // 0 copy, 1 reduce, 2 wait

@@ -184,9 +184,7 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   // (ops of different chunks never depend on each other within a rank);
   // end-of-program waits are split by chunk group the same way
   p.prog.assign(size_t(P) * p.kc + 1, 0);
-  std::vector<int> keys;  // op key per encoded op (grouping below)
   auto encode = [&](int r, const Op& op, const std::vector<OpIn>& ins) {
-    keys.push_back(op.key);
     if (op.kind != OP_WAIT && (ins.size() > size_t(kMaxOpIn) || op.outs.size() > size_t(kMaxOpOut)))
       throw invalid_argument_error("op fan-in/fan-out exceeds executor limits (32)");
     DevOp d{};
@@ -239,22 +237,6 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
       }
     }
   p.prog[size_t(P) * p.kc] = uint32_t(p.ops.size());
-  // reorderable groups: consecutive ops of one (rank, chunk group) list with
-  // the same step key are independent; the kernel's producer may run them in
-  // the order their inputs arrive.  WAIT, unaligned and local-RAW ops stay
-  // singletons (program order).
-  for (size_t g = 0; g + 1 < p.prog.size(); ++g) {
-    const uint32_t b = p.prog[g], e = p.prog[g + 1];
-    uint32_t i = b;
-    while (i < e) {
-      auto groupable = [&](uint32_t k) { return p.ops[k].kind != OP_WAIT && p.ops[k].vec && !p.ops[k].raw; };
-      uint32_t j = i + 1;
-      if (groupable(i))
-        while (j < e && j - i < uint32_t(kMaxGroup) && groupable(j) && keys[j] == keys[i]) ++j;
-      for (uint32_t k = i; k < j; ++k) p.ops[k].group_end = j;
-      i = j;
-    }
-  }
 
   // memory layout of one rank's region
   auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
