@@ -149,9 +149,26 @@ __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
   return v;
 }
 
-// Spin until *f >= target; returns the value seen.  Watchdog: after
-// timeout_ns the diagnostic goes to host-mapped memory and the kernel traps
+// Watchdog: the diagnostic goes to host-mapped memory and the kernel traps
 // (the host maps it to SCCL_PEER_TIMEOUT).
+__device__ __noinline__ void watchdog_fire(const KParams& p, int rank, int ch, int op, int slot, uint64_t target,
+                                           uint64_t seen) {
+  volatile int* e = p.errinfo;
+  if (e && atomicCAS(p.errinfo, 0, -1) == 0) {
+    e[1] = rank;
+    e[2] = ch;
+    e[3] = op;
+    e[4] = slot;
+    e[5] = int(target & 0x7fffffff);
+    e[6] = int(seen & 0x7fffffff);
+    __threadfence_system();
+    e[0] = ERR_TIMEOUT;
+    __threadfence_system();
+  }
+  __trap();
+}
+
+// Spin until *f >= target; returns the value seen.  Bounded by timeout_ns.
 template <bool SYS>
 __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p, int rank, int ch, int op,
                             int slot) {
@@ -161,21 +178,8 @@ __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p
   uint32_t spins = 0;
   while ((v = ld_acquire<SYS>(f)) < target) {
     if (++spins > 64) __nanosleep(32);
-    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
-      volatile int* e = p.errinfo;
-      if (e && atomicCAS(p.errinfo, 0, -1) == 0) {
-        e[1] = rank;
-        e[2] = ch;
-        e[3] = op;
-        e[4] = slot;
-        e[5] = int(target & 0x7fffffff);
-        e[6] = int(v & 0x7fffffff);
-        __threadfence_system();
-        e[0] = ERR_TIMEOUT;
-        __threadfence_system();
-      }
-      __trap();
-    }
+    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
+      watchdog_fire(p, rank, ch, op, slot, target, v);
   }
   return v;
 }
@@ -742,21 +746,8 @@ __device__ uint2 ll_read(const char* slot, int64_t pair, bool two, uint32_t ef, 
     v = ld_ll(a);
     if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
     if (++spins > 32) __nanosleep(20);
-    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
-      volatile int* e = p.errinfo;
-      if (e && atomicCAS(p.errinfo, 0, -1) == 0) {
-        e[1] = rank;
-        e[2] = ch;
-        e[3] = op;
-        e[4] = -3;
-        e[5] = int(ef);
-        e[6] = int(v.y);
-        __threadfence_system();
-        e[0] = ERR_TIMEOUT;
-        __threadfence_system();
-      }
-      __trap();
-    }
+    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
+      watchdog_fire(p, rank, ch, op, -3, ef, v.y);
   }
 }
 

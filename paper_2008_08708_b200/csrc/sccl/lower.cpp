@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <map>
 #include <sstream>
 
@@ -187,6 +188,10 @@ Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
       b.add_copy(n, key, c, x, o, -1);
     }
 
+  // SCCL_SEND_ORDER=canonical keeps (step, chunk, src, dst) order within a
+  // step (A/B switch for the rotation below)
+  const char* order_env = std::getenv("SCCL_SEND_ORDER");
+  const bool canonical_order = order_env && std::string(order_env) == "canonical";
   for (int r = 0; r < P; ++r) {
     auto& ops = pg.ranks[r].ops;
     std::stable_sort(ops.begin(), ops.end(), [](const Op& a, const Op& z) { return a.key < z.key; });
@@ -216,8 +221,9 @@ Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
         if (o.loc.rank != r) d = std::min(d, (o.loc.rank - r + P) % P);
       return d;
     };
-    std::stable_sort(ops.begin(), ops.end(),
-                     [&](const Op& a, const Op& z) { return a.key != z.key ? a.key < z.key : dist(a) < dist(z); });
+    if (!canonical_order)
+      std::stable_sort(ops.begin(), ops.end(),
+                       [&](const Op& a, const Op& z) { return a.key != z.key ? a.key < z.key : dist(a) < dist(z); });
 
     // F2: fold copies that read a reduce's result into the reduce (fused
     // receive-reduce-forward, "reduce on receipt")

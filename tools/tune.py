@@ -51,6 +51,10 @@ def main():
     recv = [torch.empty(P * maxb, dtype=torch.uint8, device="cuda") for _ in range(P)]
     for name, sz, kn in itertools.product(names, sizes, knobs):
         js, dt = scheds[name]
+        if "order" in kn:
+            os.environ["SCCL_SEND_ORDER"] = kn["order"]
+        else:
+            os.environ.pop("SCCL_SEND_ORDER", None)
         if "budget" in kn:
             os.environ["SCCL_STAGE_BUDGET"] = str(kn["budget"])
         else:
