@@ -213,8 +213,10 @@ class LoopbackPlan(_PlanBase):
 
     def launch(self, sendbufs: Sequence, recvbufs: Sequence, stream=None):
         P = self.nranks
-        s = (ctypes.c_void_p * P)(*[_ptr(x) for x in sendbufs])
-        r = (ctypes.c_void_p * P)(*[_ptr(x) for x in recvbufs])
+        if len(sendbufs) < P or len(recvbufs) < P:
+            raise InvalidArgumentError(INVALID_ARGUMENT, f"need {P} send and recv buffers")
+        s = (ctypes.c_void_p * P)(*[_ptr(x) for x in sendbufs[:P]])
+        r = (ctypes.c_void_p * P)(*[_ptr(x) for x in recvbufs[:P]])
         _raise(lib().sccl_launch_loopback(self._h, s, r, ctypes.c_void_p(_stream_ptr(stream))))
 
     def launch_copy_engine(self, sendbufs: Sequence, recvbufs: Sequence, stream=None):
