@@ -46,8 +46,6 @@ constexpr int SIGQ = 64;             // storer -> signaler queue entries
 constexpr int NSTAGE = kMaxStages;   // barrier sets; stages in use = KParams::nstage
 constexpr int FIFO = 8;              // storer's in-flight tile records (> max sig_lag)
 constexpr uint64_t kStorerPatienceNs = 3000;  // storer spins this long before draining
-constexpr int kReduceTile = 16384;  // reduce output tile (registers hold it across the fan-in)
-constexpr int kReduceVPT = kReduceTile / 16 / (NCW * 32);  // 16 B vectors per compute thread
 constexpr size_t SMEM_HDR = 2048;    // mbarriers, signal queue, control words, ahead of the stages
 __host__ __device__ constexpr size_t smem_bytes(int tile, int nstage) { return SMEM_HDR + size_t(nstage) * tile; }
 
@@ -476,14 +474,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
     }
 
     // ---- pipelined op ----
-    // A copy tile uses one stage.  A reduce tile of T output bytes uses nin
-    // consecutive stages, one per input in the fixed order; the compute warps
-    // accumulate in f32 registers across them and write the result into the
-    // last input's stage, which the storer stores.  So the reduce tile does
-    // not shrink with the fan-in.
-    const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : min(uint32_t(p.tile), uint32_t(kReduceTile));
+    const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
     const uint32_t ntiles = uint32_t((q.len + T - 1) / T);
-    const uint32_t uses = op.kind == 1 ? uint32_t(op.nin) : 1u;
 
     if (warp == 0) {
       // ================= producer =================
@@ -498,68 +490,54 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       if (op.raw && lane == 0)  // input written by an earlier op of this CTA: the storer drains first
         while (S.completed_seq < seq) __nanosleep(32);
       __syncwarp();
-      for (uint32_t t = 0; t < ntiles; ++t) {
+      for (uint32_t t = 0; t < ntiles; ++t, ++it) {
+        const uint32_t s = it % NST, ph = (it / NST) & 1;
         const uint64_t lo = uint64_t(t) * T;
         const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
         const uint32_t nv = n & ~15u;
-        for (uint32_t u = 0; u < uses; ++u, ++it) {
-          const uint32_t s = it % NST, ph = (it / NST) & 1;
-          if (lane == int(u) && flag >= 0) {
-            const uint64_t need = fbase + lo + n;
-            const uint64_t* f = myflags + uint64_t(flag) * p.nch + ch;
-            if (ready < need) ready = ld_acquire<SYS>(f);
-            if (ready < need) {  // a peer is behind: let the storer publish what it holds
-              S.producer_blocked = 1;
-              ready = wait_ge<SYS>(f, need, p, rank, ch, int(oi - ob), flag);
-              S.producer_blocked = 0;
-            }
+        if (flag >= 0) {
+          const uint64_t need = fbase + lo + n;
+          const uint64_t* f = myflags + uint64_t(flag) * p.nch + ch;
+          if (ready < need) ready = ld_acquire<SYS>(f);
+          if (ready < need) {  // a peer is behind: let the storer publish what it holds
+            S.producer_blocked = 1;
+            ready = wait_ge<SYS>(f, need, p, rank, ch, int(oi - ob), flag);
           }
-          __syncwarp();
-          if (lane == 0) {
-            mbar_wait(&S.empty[s], ph ^ 1);
-            mbar_arrive_tx(&S.full[s], nv);
-          }
-          __syncwarp();
-          if (lane == int(u) && nv) {
-            fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
-            bulk_load(bufs + size_t(s) * STAGE, src + lo, nv, &S.full[s]);
-          }
+        }
+        __syncwarp();
+        if (lane == 0) S.producer_blocked = 0;
+        __syncwarp();
+        if (lane == 0) {
+          mbar_wait(&S.empty[s], ph ^ 1);
+          mbar_arrive_tx(&S.full[s], nv * op.nin);
+        }
+        __syncwarp();
+        if (lane < op.nin && nv) {
+          fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
+          bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, &S.full[s]);
         }
       }
     } else if (warp == 2) {
       // signaler: runs its own loop below
     } else if (warp >= CW0) {
-      // ================= compute =================
-      const uint32_t tc = tid - CW0 * 32;
-      for (uint32_t t = 0; t < ntiles; ++t) {
-        const uint64_t lo = uint64_t(t) * T;
-        const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
-        Vec<DT> acc[kReduceVPT];
-        for (uint32_t u = 0; u < uses; ++u, ++it) {
-          const uint32_t s = it % NST, ph = (it / NST) & 1;
-          mbar_wait(&S.full[s], ph);
-          if (op.kind == 1) {
-            uint4* b = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
-#pragma unroll
-            for (int j = 0; j < kReduceVPT; ++j) {
-              const uint32_t v = tc + uint32_t(j) * (NCW * 32);
-              if (v < nv) {
-                if (u == 0) acc[j].init(b[v]);
-                else acc[j].add(b[v]);
-              }
-            }
-            if (u + 1 == uses) {  // result into this stage for the storer
-#pragma unroll
-              for (int j = 0; j < kReduceVPT; ++j) {
-                const uint32_t v = tc + uint32_t(j) * (NCW * 32);
-                if (v < nv) b[v] = acc[j].out();
-              }
-              fence_proxy_async_smem();
-            }
+      // ================= compute (REDUCE only; others just pass) =================
+      for (uint32_t t = 0; t < ntiles; ++t, ++it) {
+        const uint32_t s = it % NST, ph = (it / NST) & 1;
+        mbar_wait(&S.full[s], ph);
+        if (op.kind == 1) {
+          const uint64_t lo = uint64_t(t) * T;
+          const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
+          uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
+          for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
+            Vec<DT> acc;
+            acc.init(b0[v]);
+            for (int k = 1; k < op.nin; ++k) acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T)[v]);
+            b0[v] = acc.out();
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&S.ready[s]);
+          fence_proxy_async_smem();
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.ready[s]);
       }
     } else {
       // ================= storer (warp 1, lane 0) =================
@@ -574,8 +552,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             S.entry_mask |= 1u << d.rank;
           }
         }
-        for (uint32_t t = 0; t < ntiles; ++t, ++seq)
-        for (uint32_t u = 0; u < uses; ++u, ++it) {
+        for (uint32_t t = 0; t < ntiles; ++t, ++it, ++seq) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
           const uint64_t lo = uint64_t(t) * T;
           const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
@@ -593,12 +570,6 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
               drain();
               mbar_wait(&S.ready[s], ph);
             }
-          }
-          if (u + 1 < uses) {  // an input of a reduce tile: consumed, nothing to store
-            bulk_wait_read<0>();
-            while (f_rel != f_tail) mbar_arrive(&S.empty[f_stage[(f_rel++) % FIFO]]);
-            mbar_arrive(&S.empty[s]);
-            continue;
           }
           if (n > nv) {  // < 16 B chunk tail: element-wise, global -> global
             const char* in[kMaxOpIn];
@@ -637,7 +608,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           }
         }
       } else {
-        it += ntiles * uses;
+        it += ntiles;
         seq += ntiles;
       }
     }

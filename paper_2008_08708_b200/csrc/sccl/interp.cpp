@@ -210,9 +210,9 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
         }
         continue;
       }
-      // same tiling rule as the kernel: copy tiles of `tile`, reduce output
-      // tiles of min(tile, 16 KiB); counters count bytes so the two sides may differ
-      const int64_t T = op.kind == OP_COPY ? tile : std::min<int64_t>(tile, 16384);
+      // same tiling rule as the kernel: copy tiles of `tile`, reduce tiles
+      // of tile/nin; counters count bytes so the two sides may differ
+      const int64_t T = op.kind == OP_COPY ? tile : std::max<int64_t>(16, (tile / op.nin) & ~int64_t(15));
       const int64_t ntiles = (q.len + T - 1) / T;
       const uint64_t b0 = (e - 1) * uint64_t(q.len);
       for (int64_t t = 0; t < ntiles; ++t) {

@@ -122,12 +122,16 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   // groups so independent chunks travel in parallel instead of queueing
   // behind each other in one CTA (latency).
   const int G = p.pg.G;
-  // stage (= copy tile) size and pipeline depth: 3 x 32 KiB at 2 CTAs per
-  // SM (reduce tiles are min(stage, 16 KiB) of output, one stage per input);
-  // small chunks: the smallest power of two that holds one
+  int max_fanin = 1;
+  for (auto& rp : p.pg.ranks)
+    for (auto& op : rp.ops)
+      if (op.kind == OP_REDUCE) max_fanin = std::max(max_fanin, int(op.ins.size()));
+  // stage (= copy tile) size and pipeline depth, within kStageBudget bytes:
+  // bulk streaming 6 x 32 KiB; wide reductions 3 x 64 KiB (reduce tiles are
+  // stage / fan-in); small chunks: the smallest power of two that holds one
   int tile = req.tile;
   if (tile <= 0) {
-    tile = 32768;
+    tile = max_fanin >= 4 ? kMaxTile : 32768;
     if (maxlen < tile) {
       tile = 1024;
       while (tile < maxlen) tile *= 2;
@@ -137,8 +141,9 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     throw invalid_argument_error("tile_bytes must be a multiple of 16 in [256, 65536]");
   // stage budget: 192 KiB = 1 CTA/SM with a deep ring; SCCL_STAGE_BUDGET
   // (bytes) trades depth for CTAs per SM (96 KiB -> 2 CTAs/SM)
-  // 96 KiB of stages -> 2 CTAs per SM (tools/tune.py sweep)
-  int budget = kStageBudget / 2;
+  // streaming copies / 2-input reductions: 3 x 32 KiB at 2 CTAs per SM;
+  // wide reductions: 3 x 64 KiB at 1 CTA per SM (tools/tune.py sweep)
+  int budget = max_fanin >= 4 ? kStageBudget : kStageBudget / 2;
   if (const char* env = std::getenv("SCCL_STAGE_BUDGET")) budget = std::max(2 * 256, std::min(kStageBudget, std::atoi(env)));
   if (req.stage_budget > 0) budget = std::min(kStageBudget, req.stage_budget);
   const int nstage = std::max(2, std::min(6, budget / tile));
