@@ -1,5 +1,5 @@
-"""Multi-process path on ONE GPU: two processes, one rank each, both on
-cuda:0.  Exercises exactly what an 8xB200 run uses -- CUDA-IPC export /
+"""Multi-process path on ONE GPU: two (or four) processes, one rank each,
+all on cuda:0.  Exercises exactly what an 8xB200 run uses -- CUDA-IPC export /
 bind of the plan regions through torch.distributed (gloo), sys-scope
 counters, the per-(peer, channel) entry handshake, the registered receive
 buffer and its copy-out -- except that the peer is the same device (the
@@ -23,20 +23,28 @@ sys.path[:0] = [{root!r}, {oracle!r}]
 import numpy as np, torch, torch.distributed as dist
 import oracle as O
 from paper_2008_08708_b200 import sccl, schedules as S
-rank = int(sys.argv[1])
-dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=2)
+rank, W = int(sys.argv[1]), int(sys.argv[2])
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=W)
 torch.cuda.set_device(0)
-cases = [
-    (S.to_json(S.one_shot_allgather(2)), 1 << 16, O.U8, "simple"),
-    (S.to_json(S.one_shot_allgather(2)), 4096, O.U8, "ll"),
-    (S.allreduce_from(S.one_shot_allgather(2)), 1 << 18, O.BF16, "simple"),
-    (S.allreduce_from(S.one_shot_allgather(2)), 2048, O.F32, "ll"),
-]
+if W == 2:
+    cases = [
+        (S.to_json(S.one_shot_allgather(2)), 1 << 16, O.U8, "simple"),
+        (S.to_json(S.one_shot_allgather(2)), 4096, O.U8, "ll"),
+        (S.allreduce_from(S.one_shot_allgather(2)), 1 << 18, O.BF16, "simple"),
+        (S.allreduce_from(S.one_shot_allgather(2)), 2048, O.F32, "ll"),
+    ]
+else:  # multi-hop relays and combining trees through IPC-mapped peers
+    cases = [
+        (S.to_json(S.ring_allgather(4)), 1 << 16, O.U8, "simple"),
+        (S.allreduce_from(S.recursive_doubling_ring4()), 1 << 16, O.F32, "simple"),
+        (S.to_json(S.direct_alltoall(4)), 4096, O.U8, "ll"),
+        (S.allreduce_from(S.ring_allgather(4)), 8192, O.BF16, "ll"),
+    ]
 for js, nb, dt, proto in cases:
     d = json.loads(js)
-    ins = O.seeded_inputs(d["collective"], 2, nb, dt, 17)
+    ins = O.seeded_inputs(d["collective"], W, nb, dt, 17)
     ref = O.execute(d, ins, nb, dt)
-    plan = sccl.Plan(js, rank, 2, nb, dt, device=0, protocol=proto, timeout_ms=60000)
+    plan = sccl.Plan(js, rank, W, nb, dt, device=0, protocol=proto, timeout_ms=120000)
     plan.bind_with()
     send = torch.from_numpy(ins[rank]).cuda()
     for it in range(3):  # back-to-back launches: entry handshake + epochs
@@ -52,15 +60,16 @@ dist.destroy_process_group()
 """
 
 
-def test_two_processes_one_gpu(tmp_path):
+@pytest.mark.parametrize("world", [2, 4])
+def test_processes_one_gpu(tmp_path, world):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     script = tmp_path / "w.py"
     script.write_text(WORKER.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"), port=port))
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
-    procs = [subprocess.Popen([sys.executable, str(script), str(r)], stdout=subprocess.PIPE,
-                              stderr=subprocess.PIPE, text=True, env=env) for r in range(2)]
+    procs = [subprocess.Popen([sys.executable, str(script), str(r), str(world)], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True, env=env) for r in range(world)]
     try:
         outs = [p.communicate(timeout=600) for p in procs]
     finally:
@@ -70,4 +79,4 @@ def test_two_processes_one_gpu(tmp_path):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
     text = "".join(o for o, _ in outs)
-    assert text.count("OK") == 8, text
+    assert text.count("OK") == 4 * world, text
