@@ -37,18 +37,17 @@
 namespace sccl {
 namespace {
 
-constexpr int NCW = 8;               // compute warps
-constexpr int NT = kThreads;         // producer, storer, signaler + NCW compute warps
-static_assert(NT == (3 + NCW) * 32, "thread layout");
-constexpr int CW0 = 3;               // first compute warp
+constexpr int NSW = kStorerWarps;   // storer warps 1..NSW: stage s belongs to storer warp 1 + s % NSW
+constexpr int SIGW = 1 + NSW;        // signaler warp
+constexpr int CW0 = SIGW + 1;        // first compute warp
+constexpr int NCW = kThreads / 32 - CW0;  // compute warps
+constexpr int NT = kThreads;
+static_assert(NCW >= 4 && NT == (CW0 + NCW) * 32, "thread layout");
 constexpr int NPART = NT - 32;       // threads of the unaligned path (all but the signaler)
-constexpr int SIGQ = 64;             // storer -> signaler queue entries
-constexpr int NSTAGE = kMaxStages;   // barrier sets; stages in use = KParams::nstage
-constexpr int FIFO = 8;              // storer's in-flight tile records (> max sig_lag)
-constexpr uint64_t kStorerPatienceNs = 3000;  // storer spins this long before draining
-constexpr size_t SMEM_HDR = 2048;    // mbarriers, signal queue, control words, ahead of the stages
+constexpr int SIGQ = 64;             // tile completion ring (storers -> signaler), indexed by tile number
+constexpr int NSTAGE = kMaxStages;   // barrier sets; stages in use = KParams::nstage (a multiple of NSW)
+constexpr size_t SMEM_HDR = 2048;    // mbarriers, completion ring, control words, ahead of the stages
 __host__ __device__ constexpr size_t smem_bytes(int tile, int nstage) { return SMEM_HDR + size_t(nstage) * tile; }
-
 struct DPart {
   int64_t off, len;
 };
@@ -330,14 +329,31 @@ struct SigEntry {
 };
 struct Smem {
   uint64_t full[NSTAGE], ready[NSTAGE], empty[NSTAGE];
-  SigEntry q[SIGQ];                 // completed tiles whose counters must be released
-  uint32_t q_head, q_tail, q_done;  // storer pushes, signaler pops (release/acquire, cta)
-  volatile uint32_t completed_seq;  // storer: tiles < completed_seq fully written
-  volatile uint32_t producer_blocked;  // producer spins on a peer's counter
-  uint32_t entry_mask;
+  SigEntry q[SIGQ];      // tile `it` -> q[it % SIGQ]: its op, byte end, last-tile bit
+  uint32_t done[SIGQ];   // it + 1 once tile `it`'s stores are complete (storer release, signaler acquire)
+  uint32_t published;    // tiles < published are complete and their counters released (signaler)
+  uint32_t total, total_set;  // tile count of the program (producer, at its end)
+  uint32_t entry_mask;   // peers whose entry handshake this CTA has seen
 };
 static_assert(sizeof(Smem) <= SMEM_HDR, "smem header");
 
+// Simple (bulk) protocol.  Roles per CTA:
+//   warp 0          producer: waits the receipt counters of a tile, then
+//                   cp.async.bulk global->smem of every input;
+//   warps 1..NSW    storers: stage s belongs to storer warp 1 + s % NSW.
+//                   Lane o issues the bulk store to output o, every lane
+//                   commits and retires its own bulk group, so a storer
+//                   warp has one tile in flight and posts it to the
+//                   completion ring the moment its writes have landed
+//                   (no lag: a forwarded tile is visible to the next hop
+//                   one store latency after it was issued);
+//   warp SIGW       signaler: walks the completion ring in tile order and
+//                   releases the byte counters of the longest complete
+//                   prefix (one fence per batch, then relaxed stores);
+//   warps CW0..     compute: REDUCE tiles, f32 accumulate in smem.
+// No role blocks on a peer while holding a completed but unreleased tile,
+// so the program order argument of DESIGN.md section 4 gives deadlock
+// freedom without draining heuristics.
 template <int DT, bool SYS>
 __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -347,8 +363,6 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   const uint32_t NST = uint32_t(p.nstage);
   __shared__ const char* s_inp[kMaxOpIn];
   __shared__ char* s_outp[kMaxOpOut];
-  __shared__ uint64_t* s_sig[kMaxOpOut];
-  __shared__ uint8_t s_every[kMaxOpOut];
   __shared__ uint64_t s_e;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -363,13 +377,12 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       mbar_init(&S.ready[s], NCW);
       mbar_init(&S.empty[s], 1);
     }
-    S.completed_seq = 0;
-    S.q_head = S.q_tail = S.q_done = 0;
-    S.producer_blocked = 0;
+    S.published = S.total = S.total_set = 0;
     S.entry_mask = 1u << rank;
     s_e = p.epochs[blockIdx.x] + 1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = tid; i < SIGQ; i += NT) S.done[i] = 0;
   __syncthreads();
   const uint64_t e = s_e;
   if (p.multiprocess)  // "rank `rank`, channel ch entered launch e"
@@ -380,270 +393,214 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       }
 
   const uint32_t ob = p.prog[rank * p.kc + cg], oe = p.prog[rank * p.kc + cg + 1];
-  uint32_t it = 0;   // stage-use counter (same sequence in every role)
-  uint32_t seq = 0;  // tile sequence number (for local read-after-write)
+  uint32_t it = 0;  // tile number (same sequence in every role)
+  const uint32_t my_stage_class = uint32_t(warp - 1);  // storer warps
 
-  // storer FIFO of committed tiles awaiting read-release / completion
-  uint32_t f_stage[FIFO], f_op[FIFO], f_seq[FIFO];
-  uint64_t f_end[FIFO];
-  uint8_t f_last[FIFO];
-  uint32_t f_head = 0, f_tail = 0, f_rel = 0;  // [f_head, f_tail) pending completion; [f_rel, f_tail) pending release
-
-  // storer, lane 0: tile k of the FIFO is complete (its bulk group retired).
-  // Counter releases are handed to the signaler warp so the storer never
-  // sits in the release fence while it could be issuing stores.
-  auto signal_entry = [&](uint32_t k) {
-    const uint32_t x = k % FIFO;
-    fence_proxy_async_global();  // async-proxy writes -> generic observers
-    const DevOp op = p.ops[f_op[x]];
-    bool need = false;
-    for (int o = 0; o < op.nout && !need; ++o) {
-      const DevOut d = p.outs[op.out_begin + o];
-      need = d.flag >= 0 && (d.every_tile || f_last[x]);
+  // entry handshake before the first store into peer d (multi-process only)
+  auto await_entry = [&](int d, int opi) {
+    if (!(atomicOr(&S.entry_mask, 0u) & (1u << d))) {
+      wait_ge<SYS>(myflags + p.entry_base + d * p.nch + ch, e, p, rank, ch, opi, -2);
+      atomicOr(&S.entry_mask, 1u << d);
     }
-    if (need) {
-      const uint32_t h = S.q_head;
-      while (h - ld_acquire_cta(&S.q_tail) >= SIGQ) __nanosleep(20);
-      S.q[h % SIGQ] = SigEntry{f_op[x], f_last[x], f_end[x]};
-      st_release_cta(&S.q_head, h + 1);
-    }
-    S.completed_seq = f_seq[x] + 1;
-  };
-  auto drain = [&]() {  // storer: retire everything in flight
-    bulk_wait<0>();
-    while (f_rel != f_tail) mbar_arrive(&S.empty[f_stage[(f_rel++) % FIFO]]);
-    while (f_head != f_tail) signal_entry(f_head++);
   };
 
-  for (uint32_t oi = ob; oi < oe; ++oi) {
-    const DevOp op = p.ops[oi];
-    if (op.kind == 2) {  // end-of-program waits: every receipt has landed
-      if (warp == 0)
-        for (int i = lane; i < op.nin; i += 32) {
-          const DevIn in = p.ins[op.in_begin + i];
-          if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
-          const DPart q = dsplit16(int64_t(in.len), p.kb, cb);
-          if (q.len) wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, e * uint64_t(q.len), p, rank, ch,
-                                  int(oi - ob), in.flag);
-        }
-      continue;
-    }
-    if (int(op.chunk % uint32_t(p.kc)) != cg) continue;  // another channel's chunk group
-    const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
-    if (q.len == 0) continue;  // empty sub-range: nothing sent, nothing awaited
-    const uint64_t fbase = (e - 1) * uint64_t(q.len);
+  if (warp != SIGW) {
+    for (uint32_t oi = ob; oi < oe; ++oi) {
+      const DevOp op = p.ops[oi];
+      if (op.kind == 2) {  // end-of-program waits: every receipt has landed
+        if (warp == 0)
+          for (int i = lane; i < op.nin; i += 32) {
+            const DevIn in = p.ins[op.in_begin + i];
+            if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
+            const DPart q = dsplit16(int64_t(in.len), p.kb, cb);
+            if (q.len) wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, e * uint64_t(q.len), p, rank, ch,
+                                    int(oi - ob), in.flag);
+          }
+        continue;
+      }
+      if (int(op.chunk % uint32_t(p.kc)) != cg) continue;  // another channel's chunk group
+      const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
+      if (q.len == 0) continue;  // empty sub-range: nothing sent, nothing awaited
+      const uint64_t fbase = (e - 1) * uint64_t(q.len);
 
-    if (!op.vec) {
-      // ---- unaligned op: whole CTA (but the signaler), element-wise, synchronous ----
-      if (warp == 2) continue;
-      const int ptid = warp < 2 ? tid : tid - 32;
-      if (warp == 1 && lane == 0) drain();
-      named_sync(1);
-      if (tid < op.nin) {
-        const DevIn in = p.ins[op.in_begin + tid];
-        s_inp[tid] = p.base[in.rank][in.space] + in.off;
-        if (in.flag >= 0)
-          wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, fbase + uint64_t(q.len), p, rank, ch, int(oi - ob),
-                       in.flag);
-      }
-      if (tid < op.nout) {
-        const DevOut d = p.outs[op.out_begin + tid];
-        s_outp[tid] = p.base[d.rank][d.space] + d.off;
-        if (p.multiprocess && d.rank != rank && !(atomicOr(&S.entry_mask, 0u) & (1u << d.rank))) {
-          wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
-          atomicOr(&S.entry_mask, 1u << d.rank);
+      if (!op.vec) {
+        // ---- unaligned op: whole CTA (but the signaler), element-wise, synchronous.
+        // Every earlier tile's stores are complete: each storer warp retires
+        // its tile before it moves on.
+        const int ptid = tid < 32 * SIGW ? tid : tid - 32;
+        named_sync(1);
+        if (tid < op.nin) {
+          const DevIn in = p.ins[op.in_begin + tid];
+          s_inp[tid] = p.base[in.rank][in.space] + in.off;
+          if (in.flag >= 0)
+            wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, fbase + uint64_t(q.len), p, rank, ch,
+                         int(oi - ob), in.flag);
         }
-      }
-      named_sync(1);
-      if (op.kind == 0) elem_op<0>(s_inp, 1, s_outp, op.nout, q.off, q.len, ptid, NPART);
-      else elem_op<DT>(s_inp, op.nin, s_outp, op.nout, q.off, q.len, ptid, NPART);
-      named_sync(1);
-      if (warp == 1 && lane == 0) {
-        fence_rel<SYS>();
-        for (int o = 0; o < op.nout; ++o) {
-          const DevOut d = p.outs[op.out_begin + o];
-          if (d.flag >= 0)
-            st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
-                            fbase + uint64_t(q.len));
+        if (tid < op.nout) {
+          const DevOut d = p.outs[op.out_begin + tid];
+          s_outp[tid] = p.base[d.rank][d.space] + d.off;
+          if (p.multiprocess && d.rank != rank) await_entry(d.rank, int(oi - ob));
         }
-        S.completed_seq = seq + 1;
-      }
-      named_sync(1);
-      ++seq;
-      continue;
-    }
-
-    // ---- pipelined op ----
-    const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
-    const uint32_t ntiles = uint32_t((q.len + T - 1) / T);
-
-    if (warp == 0) {
-      // ================= producer =================
-      uint64_t ready = 0;  // lane k tracks input k's counter (k < 32)
-      const char* src = nullptr;
-      int32_t flag = -1;
-      if (lane < op.nin) {
-        const DevIn in = p.ins[op.in_begin + lane];
-        src = p.base[in.rank][in.space] + in.off + q.off;
-        flag = in.flag;
-      }
-      if (op.raw && lane == 0)  // input written by an earlier op of this CTA: the storer drains first
-        while (S.completed_seq < seq) __nanosleep(32);
-      __syncwarp();
-      for (uint32_t t = 0; t < ntiles; ++t, ++it) {
-        const uint32_t s = it % NST, ph = (it / NST) & 1;
-        const uint64_t lo = uint64_t(t) * T;
-        const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
-        const uint32_t nv = n & ~15u;
-        if (flag >= 0) {
-          const uint64_t need = fbase + lo + n;
-          const uint64_t* f = myflags + uint64_t(flag) * p.nch + ch;
-          if (ready < need) ready = ld_acquire<SYS>(f);
-          if (ready < need) {  // a peer is behind: let the storer publish what it holds
-            S.producer_blocked = 1;
-            ready = wait_ge<SYS>(f, need, p, rank, ch, int(oi - ob), flag);
+        named_sync(1);
+        if (op.kind == 0) elem_op<0>(s_inp, 1, s_outp, op.nout, q.off, q.len, ptid, NPART);
+        else elem_op<DT>(s_inp, op.nin, s_outp, op.nout, q.off, q.len, ptid, NPART);
+        named_sync(1);
+        if (tid == 32) {
+          fence_rel<SYS>();
+          for (int o = 0; o < op.nout; ++o) {
+            const DevOut d = p.outs[op.out_begin + o];
+            if (d.flag >= 0)
+              st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
+                              fbase + uint64_t(q.len));
           }
         }
-        __syncwarp();
-        if (lane == 0) S.producer_blocked = 0;
-        __syncwarp();
-        if (lane == 0) {
-          mbar_wait(&S.empty[s], ph ^ 1);
-          mbar_arrive_tx(&S.full[s], nv * op.nin);
-        }
-        __syncwarp();
-        if (lane < op.nin && nv) {
-          fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
-          bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, &S.full[s]);
-        }
+        named_sync(1);
+        continue;
       }
-    } else if (warp == 2) {
-      // signaler: runs its own loop below
-    } else if (warp >= CW0) {
-      // ================= compute (REDUCE only; others just pass) =================
-      for (uint32_t t = 0; t < ntiles; ++t, ++it) {
-        const uint32_t s = it % NST, ph = (it / NST) & 1;
-        mbar_wait(&S.full[s], ph);
-        if (op.kind == 1) {
-          const uint64_t lo = uint64_t(t) * T;
-          const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
-          uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
-          for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
-            Vec<DT> acc;
-            acc.init(b0[v]);
-            for (int k = 1; k < op.nin; ++k) acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T)[v]);
-            b0[v] = acc.out();
-          }
-          fence_proxy_async_smem();
+
+      // ---- pipelined op ----
+      const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
+      const uint32_t ntiles = uint32_t((q.len + T - 1) / T);
+
+      if (warp == 0) {
+        // ================= producer =================
+        uint64_t ready = 0;  // lane k tracks input k's counter (k < 32)
+        const char* src = nullptr;
+        int32_t flag = -1;
+        if (lane < op.nin) {
+          const DevIn in = p.ins[op.in_begin + lane];
+          src = p.base[in.rank][in.space] + in.off + q.off;
+          flag = in.flag;
         }
+        if (op.raw && lane == 0)  // input written by an earlier tile of this CTA
+          while (ld_acquire_cta(&S.published) < it) __nanosleep(32);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.ready[s]);
-      }
-    } else {
-      // ================= storer (warp 1, lane 0) =================
-      if (lane == 0) {
-        if (op.raw) drain();  // the producer waits for every earlier tile to be written
-        for (int o = 0; o < op.nout; ++o) {
-          const DevOut d = p.outs[op.out_begin + o];
-          s_outp[o] = p.base[d.rank][d.space] + d.off + q.off;
-          if (p.multiprocess && d.rank != rank && !(S.entry_mask & (1u << d.rank))) {
-            drain();  // never block while holding completed-but-unsignalled tiles
-            wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
-            S.entry_mask |= 1u << d.rank;
-          }
-        }
-        for (uint32_t t = 0; t < ntiles; ++t, ++it, ++seq) {
+        for (uint32_t t = 0; t < ntiles; ++t, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
           const uint64_t lo = uint64_t(t) * T;
           const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
           const uint32_t nv = n & ~15u;
-          if (!mbar_try(&S.ready[s], ph)) {
-            // Not ready.  A short wait is the producer catching up; a long
-            // one may be a peer dependency that itself waits for our
-            // pending tiles -- retire and signal everything before blocking.
-            const uint64_t t0 = globaltimer();
-            bool ok = false;
-            while (!(ok = mbar_try(&S.ready[s], ph)) && !S.producer_blocked &&
-                   globaltimer() - t0 < kStorerPatienceNs) {
-            }
-            if (!ok) {
-              drain();
-              mbar_wait(&S.ready[s], ph);
-            }
+          if (flag >= 0) {
+            const uint64_t need = fbase + lo + n;
+            if (ready < need)
+              ready = wait_ge<SYS>(myflags + uint64_t(flag) * p.nch + ch, need, p, rank, ch, int(oi - ob), flag);
           }
-          if (n > nv) {  // < 16 B chunk tail: element-wise, global -> global
+          __syncwarp();
+          if (lane == 0) {
+            mbar_wait(&S.empty[s], ph ^ 1);
+            mbar_arrive_tx(&S.full[s], nv * op.nin);
+          }
+          __syncwarp();
+          if (lane < op.nin && nv) {
+            fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
+            bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, &S.full[s]);
+          }
+        }
+      } else if (warp >= CW0) {
+        // ================= compute (REDUCE only; others just pass) =================
+        for (uint32_t t = 0; t < ntiles; ++t, ++it) {
+          const uint32_t s = it % NST, ph = (it / NST) & 1;
+          mbar_wait(&S.full[s], ph);
+          if (op.kind == 1) {
+            const uint64_t lo = uint64_t(t) * T;
+            const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
+            uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
+            for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
+              Vec<DT> acc;
+              acc.init(b0[v]);
+              for (int k = 1; k < op.nin; ++k)
+                acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T)[v]);
+              b0[v] = acc.out();
+            }
+            fence_proxy_async_smem();
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.ready[s]);
+        }
+      } else {
+        // ================= storer warp (stages s with s % NSW == warp - 1) =================
+        char* outp = nullptr;
+        if (lane < op.nout) {
+          const DevOut d = p.outs[op.out_begin + lane];
+          outp = p.base[d.rank][d.space] + d.off + q.off;
+          if (p.multiprocess && d.rank != rank) await_entry(d.rank, int(oi - ob));
+        }
+        __syncwarp();
+        for (uint32_t t = 0; t < ntiles; ++t, ++it) {
+          const uint32_t s = it % NST;
+          if (s % NSW != my_stage_class) continue;
+          const uint32_t ph = (it / NST) & 1;
+          const uint64_t lo = uint64_t(t) * T;
+          const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
+          const uint32_t nv = n & ~15u;
+          mbar_wait(&S.ready[s], ph);
+          if (n > nv && lane == 0) {  // < 16 B chunk tail: element-wise, global -> global
             const char* in[kMaxOpIn];
+            char* out[kMaxOpOut];
             for (int k = 0; k < op.nin; ++k) {
               const DevIn x = p.ins[op.in_begin + k];
               in[k] = p.base[x.rank][x.space] + x.off + q.off;
             }
-            if (op.kind == 0) elem_op<0>(in, 1, s_outp, op.nout, int64_t(lo + nv), n - nv, 0, 1);
-            else elem_op<DT>(in, op.nin, s_outp, op.nout, int64_t(lo + nv), n - nv, 0, 1);
-          }
-          if (nv)
-            for (int o = 0; o < op.nout; ++o) bulk_store(s_outp[o] + lo, bufs + size_t(s) * STAGE, nv);
-          bulk_commit();
-          const uint32_t x = f_tail % FIFO;
-          f_stage[x] = s;
-          f_op[x] = oi;
-          f_seq[x] = seq;
-          f_end[x] = lo + n;
-          f_last[x] = t + 1 == ntiles;
-          ++f_tail;
-          // smem of all but the newest group has been read: release stages
-          bulk_wait_read<1>();
-          while (f_tail - f_rel > 1) mbar_arrive(&S.empty[f_stage[(f_rel++) % FIFO]]);
-          // all but the newest sig_lag groups are complete: release counters
-          if (f_tail - f_head > uint32_t(p.sig_lag)) {
-            switch (p.sig_lag) {
-              case 0: bulk_wait<0>(); break;
-              case 1: bulk_wait<1>(); break;
-              case 2: bulk_wait<2>(); break;
-              case 3: bulk_wait<3>(); break;
-              case 4: bulk_wait<4>(); break;
-              case 5: bulk_wait<5>(); break;
-              default: bulk_wait<6>(); break;
+            for (int o = 0; o < op.nout; ++o) {
+              const DevOut d = p.outs[op.out_begin + o];
+              out[o] = p.base[d.rank][d.space] + d.off + q.off;
             }
-            while (f_tail - f_head > uint32_t(p.sig_lag)) signal_entry(f_head++);
+            if (op.kind == 0) elem_op<0>(in, 1, out, op.nout, int64_t(lo + nv), n - nv, 0, 1);
+            else elem_op<DT>(in, op.nin, out, op.nout, int64_t(lo + nv), n - nv, 0, 1);
+          }
+          if (outp && nv) bulk_store(outp + lo, bufs + size_t(s) * STAGE, nv);
+          bulk_commit();
+          bulk_wait_read<0>();  // smem read: the stage goes back to the producer
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.empty[s]);
+          bulk_wait<0>();               // writes landed
+          fence_proxy_async_global();   // async-proxy writes -> generic observers
+          __syncwarp();
+          if (lane == 0) {
+            while (it - ld_acquire_cta(&S.published) >= SIGQ) __nanosleep(20);
+            S.q[it % SIGQ] = SigEntry{oi, t + 1 == ntiles, lo + n};
+            st_release_cta(&S.done[it % SIGQ], it + 1);
           }
         }
-      } else {
-        it += ntiles;
-        seq += ntiles;
       }
     }
-    if (warp != 1) seq += ntiles;
-  }
-  if (warp == 1 && lane == 0) {
-    drain();
-    st_release_cta(&S.q_done, 1);
-  }
-  if (warp == 2 && lane == 0) {
+    if (warp == 0 && lane == 0) {
+      S.total = it;
+      st_release_cta(&S.total_set, 1);
+    }
+  } else if (lane == 0) {
     // ================= signaler =================
-    // release the counters of completed tiles: one fence per batch, then
-    // relaxed stores of the (monotone) byte counts
-    uint32_t tail = 0;
+    // release the counters of the longest complete prefix of tiles: one
+    // fence per batch, then relaxed stores of the (monotone) byte counts
+    uint32_t next = 0;
     for (;;) {
-      uint32_t h = ld_acquire_cta(&S.q_head);
-      if (h == tail) {
-        if (ld_acquire_cta(&S.q_done) && ld_acquire_cta(&S.q_head) == tail) break;
+      uint32_t end = next;
+      while (end - next < SIGQ && ld_acquire_cta(&S.done[end % SIGQ]) == end + 1) ++end;
+      if (end == next) {
+        if (ld_acquire_cta(&S.total_set) && next == S.total) break;
         __nanosleep(20);
         continue;
       }
-      fence_rel<SYS>();
-      for (; tail != h; ++tail) {
-        const SigEntry en = S.q[tail % SIGQ];
+      bool fenced = false;
+      for (uint32_t k = next; k != end; ++k) {
+        const SigEntry en = S.q[k % SIGQ];
         const DevOp op = p.ops[en.op];
         const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
         const uint64_t v = (e - 1) * uint64_t(q.len) + en.end;
         for (int o = 0; o < op.nout; ++o) {
           const DevOut d = p.outs[op.out_begin + o];
-          if (d.flag >= 0 && (d.every_tile || en.last))
+          if (d.flag >= 0 && (d.every_tile || en.last)) {
+            if (!fenced) {
+              fence_rel<SYS>();
+              fenced = true;
+            }
             st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
                             v);
+          }
         }
       }
-      st_release_cta(&S.q_tail, tail);
+      next = end;
+      st_release_cta(&S.published, next);
     }
   }
   __syncthreads();

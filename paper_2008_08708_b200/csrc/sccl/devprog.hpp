@@ -14,7 +14,8 @@ constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
 constexpr int kMaxTile = 65536; // one TMA pipeline stage (bytes)
 constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
 constexpr int kStageBudget = 196608;  // bytes of stages per CTA (nstage * tile)
-constexpr int kThreads = 352;   // producer, storer and signaler warps + 8 compute warps
+constexpr int kThreads = 352;   // producer, kStorerWarps storers, signaler + 6 compute warps
+constexpr int kStorerWarps = 3; // simple protocol: stage s is stored by warp 1 + s % 3 (nstage % 3 == 0)
 constexpr int kLLThreads = 256; // LL kernel
 constexpr int64_t kLLMaxChunk = 65536;         // auto protocol: LL up to this chunk size (copies)
 constexpr int64_t kLLMaxChunkReduce = 163840;  // ... and for schedules that reduce
@@ -61,8 +62,7 @@ struct KParams {
   int P, nch, rank0, nranks_launch;
   int kc, kb;            // nch = kc * kb: chunk groups x byte parts per chunk
   int tile;              // copy tile = pipeline stage bytes (<= kMaxTile); reduce tiles tile/nin
-  int nstage;            // pipeline stages (<= kMaxStages)
-  int sig_lag;           // bulk groups the storer keeps in flight before retiring (0..6)
+  int nstage;            // pipeline stages (<= kMaxStages, a multiple of kStorerWarps)
   int entry_base;        // index of the entry-handshake flags in FLAGS
   int multiprocess;      // 1: peers are other processes (entry handshake)
   int ll;                // 1: low-latency protocol (receipts are LL slots)

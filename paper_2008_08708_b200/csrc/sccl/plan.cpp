@@ -146,7 +146,9 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   int budget = max_fanin >= 4 ? kStageBudget : kStageBudget / 2;
   if (const char* env = std::getenv("SCCL_STAGE_BUDGET")) budget = std::max(2 * 256, std::min(kStageBudget, std::atoi(env)));
   if (req.stage_budget > 0) budget = std::min(kStageBudget, req.stage_budget);
-  const int nstage = std::max(2, std::min(6, budget / tile));
+  // stages come in multiples of the storer-warp count (each storer warp owns
+  // the stages s with s % kStorerWarps == its index): 3 or 6
+  const int nstage = budget / tile >= 2 * kStorerWarps ? 2 * kStorerWarps : kStorerWarps;
   int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, ll ? 0 : tile, nstage)
             : ll ? 2048 / kLLThreads
                  : std::max(1, std::min(2, int((227 << 10) / (nstage * tile + 2048))));
@@ -170,9 +172,6 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   p.nch = kc * kb;
   p.tile = tile;
   p.nstage = nstage;
-  // small tiles: retire every bulk group at once (latency); large: keep 6
-  // groups in flight (bandwidth; FIFO depth 8 in the kernel)
-  p.sig_lag = tile >= 16384 ? 6 : 0;
   p.resident_cap = loopback ? resident : 0;
 
   // device encoding
@@ -314,7 +313,6 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.kb = p.kb;
   k.tile = p.tile;
   k.nstage = p.nstage;
-  k.sig_lag = p.sig_lag;
   k.ll = p.ll ? 1 : 0;
   k.entry_base = p.entry_base;
 }
@@ -605,7 +603,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"sig_lag\":" << p->sig_lag << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

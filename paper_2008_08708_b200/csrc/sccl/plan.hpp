@@ -17,7 +17,7 @@ struct sccl_plan {
   int rank = 0, nranks = 0;
   bool loopback = false, host_only = false;
   int device = -1, dtype = 0, redop = 0;
-  int nch = 1, kc = 1, kb = 1, tile = 32768, nstage = 6, sig_lag = 3;
+  int nch = 1, kc = 1, kb = 1, tile = 32768, nstage = 6;
   int resident_cap = 0;  // loopback: CTAs that fit on the device at once
   bool ll = false;       // low-latency protocol
   long long timeout_ns = 0;

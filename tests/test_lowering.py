@@ -129,6 +129,6 @@ def test_auto_channel_policy():
     """Small chunks spread over chunk groups (latency); large chunks cut into
     byte parts (bandwidth)."""
     small = sccl.LoopbackPlan(CASES["ham8"], 1024, sccl.U8, device=-1).info()
-    assert small["chunk_groups"] > 1 and small["byte_parts"] == 1 and small["sig_lag"] == 0
+    assert small["chunk_groups"] > 1 and small["byte_parts"] == 1 and small["storer_warps"] == 3
     large = sccl.LoopbackPlan(CASES["ham8"], 64 << 20, sccl.U8, device=-1).info()
-    assert large["byte_parts"] > 1 and large["tile_bytes"] == 32768 and large["sig_lag"] == 6
+    assert large["byte_parts"] > 1 and large["tile_bytes"] == 32768 and large["nstage"] % 3 == 0

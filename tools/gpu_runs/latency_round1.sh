@@ -1,0 +1,2 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+python tools/tune.py '{"scheds":["ring","ag777","ag111","null1"],"sizes":[16384,65536,262144,1048576,4194304],"knobs":[{"protocol":"ll"},{"protocol":"simple"}]}' > gpurun_out/tune_lat.jsonl 2>&1
