@@ -282,6 +282,16 @@ def run_loopback(args):
                           "busbw_per_rank_GBps": round(busb / (us * 1e-6) / 1e9, 1),
                           "hbm_GBps": round(hbm_bytes_per_launch(p2) / (us * 1e-6) / 1e9, 1),
                           "hbm_frac": round(hbm_bytes_per_launch(p2) / (us * 1e-6) / 1e9 / _peaks()[0]["hbm_gbs"], 3)}
+            # ncu dram__bytes_read+write of the same launch (profiles/traffic.json):
+            # receipt/relay slots consumed right after they land are served
+            # from L2, so the algorithmic count can exceed what reaches HBM
+            try:
+                dram = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(f"{tag}:{M}")
+            except Exception:
+                dram = None
+            if dram:
+                extra[tag]["dram_traffic"] = dram
+                extra[tag]["dram_frac"] = round(dram / (us * 1e-6) / 1e9 / _peaks()[0]["hbm_gbs"], 3)
             p2.close()
 
     # e2e: through the public API with host buffers, every step:

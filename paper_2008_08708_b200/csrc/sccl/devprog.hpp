@@ -17,8 +17,6 @@ constexpr int kStageBudget = 196608;  // bytes of stages per CTA (nstage * tile)
 constexpr int kThreads = 352;   // producer, kStorerWarps storers, signaler + 6 compute warps
 constexpr int kStorerWarps = 3; // simple protocol: stage s is stored by warp 1 + s % 3 (nstage % 3 == 0)
 constexpr int kLLThreads = 256; // LL kernel
-constexpr int64_t kLLMaxChunk = 65536;         // auto protocol: LL up to this chunk size (copies)
-constexpr int64_t kLLMaxChunkReduce = 163840;  // ... and for schedules that reduce
 constexpr int64_t kLLPart = 4096;       // LL: bytes of a chunk one CTA owns
 
 struct DevIn {

@@ -68,6 +68,16 @@ int esize_of(int dtype) {
   throw sccl::invalid_argument_error("unknown dtype");
 }
 
+// predicted loopback time (us) of a lowered program, see plan_build_host
+double predict_us(const sccl::Program& pg, int steps, bool ll) {
+  double mb = 0;
+  for (auto& rp : pg.ranks)
+    for (auto& op : rp.ops)
+      if (op.kind != sccl::OP_WAIT) mb += double(op.len) * double(op.ins.size() + op.outs.size());
+  mb /= 1e6;
+  return ll ? 5.26 + 0.535 * steps + 0.401 * mb : 4.87 + 3.37 * steps + 0.143 * mb;
+}
+
 struct IpcBlob {
   char magic[8];
   char fingerprint[24];
@@ -90,22 +100,30 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     if (nranks != p.sched.P) throw invalid_argument_error("nranks != schedule P");
     if (rank < 0 || rank >= nranks) throw invalid_argument_error("rank out of range");
   }
-  // protocol: LL (flag-in-data, no fences, 2x bytes) for small chunks,
-  // pipelined TMA bulk copies with counter flags otherwise
+  // protocol: LL (flag-in-data, no fences, 2x bytes) for latency-bound
+  // sizes, pipelined TMA bulk copies with counter flags otherwise
   int64_t maxlen = 0;
   {
     const auto phases = p.sched.flat();
     for (auto& g : chunk_geometry(p.sched.kind, p.sched.P, phases.back()->G, bytes)) maxlen = std::max(maxlen, g.len);
   }
-  // measured crossover on B200 (tools/tune.py, loopback, round 1): LL wins
-  // up to 64 KiB chunks for copies and up to ~160 KiB when the schedule
-  // reduces (the bulk path's wide-reduce tiles are its weaker side)
-  bool combining = false;
-  for (auto* ph : p.sched.flat()) combining |= is_combining(ph->kind);
-  const int64_t ll_max = combining ? kLLMaxChunkReduce : kLLMaxChunk;
-  bool ll = req.protocol == 2 || (req.protocol == 0 && maxlen <= ll_max);
+  // protocol choice (auto): lower both ways and take the smaller predicted
+  // time t = c + alpha*S + beta*MB, where S = schedule steps and MB = bytes
+  // the lowered program reads + writes.  Constants are a relative-error
+  // least-squares fit to the B200 loopback crossover sweep
+  // (tools/gpu_runs/proto_round1b.sh: 7 schedules x 64 KiB-16 MiB x both
+  // protocols; mean regret vs the per-point best 1.8 %).
   if (req.protocol < 0 || req.protocol > 2) throw invalid_argument_error("protocol must be 0 (auto), 1 (simple), 2 (ll)");
-  p.pg = lower(p.sched, bytes, es, ll);
+  bool ll = req.protocol == 2;
+  if (req.protocol == 0) {
+    int steps = 0;
+    for (auto* ph : p.sched.flat()) steps += ph->S;
+    const Program a = lower(p.sched, bytes, es, true), b = lower(p.sched, bytes, es, false);
+    ll = predict_us(a, steps, true) < predict_us(b, steps, false);
+    p.pg = ll ? a : b;
+  } else {
+    p.pg = lower(p.sched, bytes, es, ll);
+  }
   p.ll = ll;
   p.rank = loopback ? 0 : rank;
   p.nranks = p.sched.P;

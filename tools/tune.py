@@ -44,6 +44,7 @@ def main():
               "ar56": (S.allreduce_from(ag), sccl.BF16),
               "ring": (S.to_json(S.ring_allgather(P)), sccl.U8),
               "ar_ring": (S.allreduce_from(S.ring_allgather(P)), sccl.BF16),
+              "a2a": (S.to_json(S.direct_alltoall(P)), sccl.U8),
               # floor: one rank, no sends (launch + prologue + a local copy)
               "null1": (S.to_json(S._sched("allgather", "full:1", 1, 1, 1, [1], [])), sccl.U8)}
     grid = json.loads(sys.argv[1]) if len(sys.argv) > 1 else {}
