@@ -294,6 +294,28 @@ def run_loopback(args):
                 extra[tag]["dram_frac"] = round(dram / (us * 1e-6) / 1e9 / _peaks()[0]["hbm_gbs"], 3)
             p2.close()
 
+    # comparison point on the same device: the same lowered program run as
+    # per-op cudaMemcpyAsync device-to-device copies in step order on one
+    # stream (the paper's per-step copy lowering) -- what a
+    # library-copy executor of the schedule achieves without the kernel
+    copy_engine = None
+    if not args.no_sweep and not info["protocol"] == "ll":
+        for r in recv:
+            r.zero_()
+        plan.launch_copy_engine(send, recv, stream)
+        stream.synchronize()
+        assert all(torch.equal(r, want) for r in recv), "bench: copy-engine result wrong"
+        ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ca.record(stream)
+        for _ in range(3):
+            plan.launch_copy_engine(send, recv, stream)
+        cb.record(stream)
+        stream.synchronize()
+        ce_ms = ca.elapsed_time(cb) / 3
+        copy_engine = {"ms": round(ce_ms, 3), "value": round(bus / (ce_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                       "kernel_speedup": round(ce_ms / ms, 2),
+                       "note": "same lowered program, one cudaMemcpyAsync D2D per op output, step order, one stream"}
+
     # e2e: through the public API with host buffers, every step:
     #   H2D of all P ranks' inputs (pinned host -> device),
     #   the collective,
@@ -379,6 +401,7 @@ def run_loopback(args):
         "gpu_launches": launches,
         "latency_sweep": sweep,
         "other_collectives": extra,
+        "copy_engine_baseline": copy_engine,
     }
     print(json.dumps(line), flush=True)
 

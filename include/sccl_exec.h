@@ -43,7 +43,7 @@ typedef struct {
   int device;         /* CUDA device ordinal; -1 = host-only plan (lowering, handle logic; no launch) */
   int nchannels;      /* byte parts per chunk (CTAs per rank per chunk group); 0 = auto              */
   int chunk_groups;   /* chunk groups (independent chunks run on different CTAs); 0 = auto          */
-  int tile_bytes;     /* pipeline stage / copy tile bytes, multiple of 16 in [256, 32768]; 0 = auto  */
+  int tile_bytes;     /* pipeline stage / copy tile bytes, multiple of 16 in [256, 65536]; 0 = auto  */
   int protocol;       /* 0 = auto, 1 = simple (TMA bulk + counters), 2 = LL (flag in data)          */
   int64_t timeout_ms; /* peer-wait watchdog; 0 = default (10 s), <0 = disabled                        */
 } sccl_plan_opts;
@@ -64,6 +64,16 @@ int sccl_schedule_canonicalize(const char* schedule_json, char* out, size_t* len
 int sccl_schedule_invert(const char* schedule_json, char* out, size_t* len);
 /* Allreduce = (RS, AG) composition */
 int sccl_schedule_compose_allreduce(const char* rs_json, const char* ag_json, char* out, size_t* len);
+
+/* Per-size algorithm and protocol choice (the alpha-beta
+ * cost model; "automatically switch between multiple
+ * implementations"): lowers every candidate schedule (same collective and
+ * P, e.g. a Pareto frontier) under both protocols for bytes_per_rank and
+ * returns the candidate index and protocol (1 simple, 2 LL) with the
+ * smallest predicted time under the fitted B200 model (
+ * the same model protocol=auto uses).  predicted_us may be NULL. */
+int sccl_schedule_select(const char* const* schedule_jsons, int n, size_t bytes_per_rank, int dtype, int* index,
+                         int* protocol, double* predicted_us);
 
 /* ---- plans ------------------------------------------------------------------ */
 

@@ -392,6 +392,40 @@ int sccl_schedule_compose_allreduce(const char* rs, const char* ag, char* out, s
   });
 }
 
+int sccl_schedule_select(const char* const* jsons, int n, size_t bytes, int dtype, int* index, int* protocol,
+                         double* predicted_us) {
+  return guarded([&] {
+    if (!jsons || n <= 0 || !index || !protocol) throw invalid_argument_error("NULL argument or no candidates");
+    const int es = esize_of(dtype);
+    double best = 0;
+    int bi = -1, bp = 0, P = -1;
+    Kind kind{};
+    for (int i = 0; i < n; ++i) {
+      if (!jsons[i]) throw invalid_argument_error("schedule_json is NULL");
+      const Schedule s = parse_schedule(jsons[i]);
+      if (i == 0) {
+        P = s.P;
+        kind = s.kind;
+      } else if (s.P != P || s.kind != kind) {
+        throw invalid_argument_error("candidates must share the collective and P");
+      }
+      int steps = 0;
+      for (auto* ph : s.flat()) steps += ph->S;
+      for (int ll = 0; ll < 2; ++ll) {  // lower() verifies and throws on invalid input
+        const double t = predict_us(lower(s, int64_t(bytes), es, ll != 0), steps, ll != 0);
+        if (bi < 0 || t < best) {
+          best = t;
+          bi = i;
+          bp = ll ? 2 : 1;
+        }
+      }
+    }
+    *index = bi;
+    *protocol = bp;
+    if (predicted_us) *predicted_us = best;
+  });
+}
+
 static int create_common(const char* json, int rank, int nranks, size_t bytes, int dtype, int redop,
                          const sccl_plan_opts* opts, sccl_plan** out, bool loopback) {
   return guarded([&] {

@@ -59,6 +59,9 @@ def lib():
         for name in ("sccl_schedule_verify", "sccl_schedule_canonicalize", "sccl_schedule_invert"):
             getattr(L, name).argtypes = [ctypes.c_char_p, c_p, ctypes.POINTER(c_sz)]
         L.sccl_schedule_compose_allreduce.argtypes = [ctypes.c_char_p, ctypes.c_char_p, c_p, ctypes.POINTER(c_sz)]
+        L.sccl_schedule_select.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_int, c_sz, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_double)]
         L.sccl_plan_create.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, c_sz, ctypes.c_int,
                                        ctypes.c_int, ctypes.POINTER(_Opts), ctypes.POINTER(c_p)]
         L.sccl_plan_create_loopback.argtypes = [ctypes.c_char_p, c_sz, ctypes.c_int, ctypes.c_int,
@@ -136,6 +139,18 @@ def invert(schedule) -> str:
 def compose_allreduce(rs, ag) -> str:
     """Allreduce = (RS, AG) (SPEC.md:347-355)."""
     return _string_call(lib().sccl_schedule_compose_allreduce, _text(rs), _text(ag))
+
+
+def select(schedules: Sequence, bytes_per_rank: int, dtype: int = U8):
+    """Per-size algorithm + protocol choice among candidate schedules of one
+    collective (e.g. a Pareto frontier) by the fitted B200 cost model
+    (PAPER.md:1037).  Returns (index, protocol name,
+    predicted microseconds)."""
+    arr = (ctypes.c_char_p * len(schedules))(*[_text(x) for x in schedules])
+    idx, proto, us = ctypes.c_int(-1), ctypes.c_int(0), ctypes.c_double(0.0)
+    _raise(lib().sccl_schedule_select(arr, len(schedules), bytes_per_rank, dtype, ctypes.byref(idx),
+                                      ctypes.byref(proto), ctypes.byref(us)))
+    return idx.value, {1: "simple", 2: "ll"}[proto.value], us.value
 
 
 def version() -> str:
