@@ -196,6 +196,61 @@ def test_allreduce_large_exact_sum(dt):
         assert torch.equal(r, want)
 
 
+def test_baseline_full_sizes():
+    """BASELINE configs 2-4 at their largest sizes, through size-independent
+    properties: AG (7,7,7) at 1 GiB per rank (every output == the
+    concatenation of the inputs), AR (8,2,2) bf16 at 1 GiB with
+    integer-valued inputs (exact sum in any order), A2A (8,1,1) at 256 MiB
+    (output block s of rank d == input block d of rank s)."""
+    P = 8
+    g = torch.Generator(device=DEV)
+    g.manual_seed(3)
+    # allgather, 1 GiB per rank: 8 GiB of inputs, 64 GiB of outputs
+    m = 1 << 30
+    plan = sccl.LoopbackPlan(SCHED["ag_777"], m, O.U8, device=0)
+    send = [torch.randint(0, 256, (m,), dtype=torch.uint8, device=DEV, generator=g) for _ in range(P)]
+    recv = [torch.empty(P * m, dtype=torch.uint8, device=DEV) for _ in range(P)]
+    plan.launch(send, recv)
+    torch.cuda.synchronize()
+    plan.check()
+    for r in recv:
+        for s in range(P):
+            assert torch.equal(r[s * m:(s + 1) * m], send[s])
+    plan.close()
+    del send, recv
+    torch.cuda.empty_cache()
+    # allreduce (8,2,2), bf16, 1 GiB per rank
+    M = 1 << 30
+    plan = sccl.LoopbackPlan(SCHED["ar_822"], M, O.BF16, device=0)
+    xs = [torch.randint(-16, 17, (M // 2,), device=DEV, generator=g).to(torch.bfloat16) for _ in range(P)]
+    recv = [torch.empty(M, dtype=torch.uint8, device=DEV) for _ in range(P)]
+    plan.launch([x.view(torch.uint8) for x in xs], recv)
+    torch.cuda.synchronize()
+    plan.check()
+    want = xs[0].float()
+    for x in xs[1:]:
+        want += x.float()
+    want = want.to(torch.bfloat16).view(torch.uint8)
+    for r in recv:
+        assert torch.equal(r, want)
+    plan.close()
+    del xs, recv, want
+    torch.cuda.empty_cache()
+    # alltoall (8,1,1), 256 MiB per rank
+    M = 256 << 20
+    B = M // P
+    plan = sccl.LoopbackPlan(SCHED["a2a_b5"], M, O.U8, device=0)
+    send = [torch.randint(0, 256, (M,), dtype=torch.uint8, device=DEV, generator=g) for _ in range(P)]
+    recv = [torch.empty(M, dtype=torch.uint8, device=DEV) for _ in range(P)]
+    plan.launch(send, recv)
+    torch.cuda.synchronize()
+    plan.check()
+    for d in range(P):
+        for s in range(P):
+            assert torch.equal(recv[d][s * B:(s + 1) * B], send[s][d * B:(d + 1) * B])
+    plan.close()
+
+
 def test_allreduce_bf16_bitexact_16MiB():
     js = SCHED["ar_56_14_14"]
     run_gpu(js, 16 << 20, O.BF16, seed=9)
