@@ -413,24 +413,42 @@ def run_multi(args):
     from paper_2008_08708_b200 import sccl
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # SCCL_BENCH_SHARE_GPU=1: every rank on cuda:0 (validates this multi-process
+    # path on a 1-GPU box: IPC peers, sys-scope flags, the JSON line).  The
+    # ranks time-slice one GPU, so its numbers are not performance; NCCL
+    # refuses duplicate GPUs, so the process group is gloo and the NCCL
+    # comparison is skipped.
+    shared = os.environ.get("SCCL_BENCH_SHARE_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     P = world
     js, sname = schedule_for(P, args.schedule)
     m = args.bytes
     plan = sccl.Plan(js, rank, P, m, sccl.U8, device=local, nchannels=args.nchannels, tile_bytes=args.tile)
     plan.bind_with()
     dev = torch.device("cuda", local)
-    send = torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    send = torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev, generator=g)
     recv = torch.empty(P * m, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         plan.launch(send, recv, stream)
     torch.cuda.synchronize()
-    ref = torch.empty(P * m, dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(ref, send)
+    if shared:
+        parts = [torch.empty(m, dtype=torch.uint8) for _ in range(P)]
+        dist.all_gather(parts, send.cpu())
+        ref = torch.cat(parts).to(dev)
+    else:
+        ref = torch.empty(P * m, dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(ref, send)
     torch.cuda.synchronize()
-    assert torch.equal(ref, recv), f"rank {rank}: allgather differs from NCCL"
+    assert torch.equal(ref, recv), f"rank {rank}: allgather differs from the gathered inputs"
     regptr, _ = plan.recv_buffer()
 
     def timed(fn, steps):
@@ -442,15 +460,15 @@ def run_multi(args):
             fn()
         b.record()
         torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(b) / steps], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([a.elapsed_time(b) / steps], device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
         return float(t)
 
     n0 = plan.launch_count
     with ClockSampler(local) as clk:
         ms = timed(lambda: plan.launch(send, regptr, stream), args.steps)
     launches = plan.launch_count - n0
-    ms_nccl = timed(lambda: dist.all_gather_into_tensor(ref, send), args.steps)
+    ms_nccl = None if shared else timed(lambda: dist.all_gather_into_tensor(ref, send), args.steps)
     plan.check()
     bus = P * (P - 1) * m
     value = bus / (ms * 1e-3) / 1e9
@@ -472,9 +490,11 @@ def run_multi(args):
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
             "config": {"workload": f"{sname}; one rank per GPU, CUDA IPC peers over NVLink", "ranks": P,
                        "bytes_per_rank": m, "parallelism": f"ranks{P}", "nchannels": plan.info()["nchannels"],
-                       "l2": "no flush: buffers >> L2"},
+                       "l2": "no flush: buffers >> L2",
+                       "shared_gpu": shared},
             "busbw_per_rank_GBps": round(per_gpu, 2),
-            "nccl": {"ms": round(ms_nccl, 4), "busbw_per_rank_GBps": round((P - 1) * m / (ms_nccl * 1e-3) / 1e9, 2)},
+            "nccl": None if shared else {"ms": round(ms_nccl, 4),
+                                         "busbw_per_rank_GBps": round((P - 1) * m / (ms_nccl * 1e-3) / 1e9, 2)},
             "roofline": {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": 900.0, "unit": "GB/s",
                          "frac": round(per_gpu / 900.0, 4), "traffic": None,
                          "peak_source": "nominal NVLink 5 per direction per GPU"},
