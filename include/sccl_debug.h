@@ -18,6 +18,13 @@ int sccl_debug_interpret_loopback(sccl_plan* plan, const void* const* sendbufs, 
                                   double timeout_s);
 const char* sccl_debug_last_error(void);
 
+/* Event trace of the simple-protocol kernel: every CTA appends up to
+ * records_per_cta records {globaltimer ns, event | op << 8 | tile << 32} to
+ * device_buf + blockIdx * records_per_cta * 2 (u64 words; the caller zeroes
+ * it).  device_buf = NULL turns tracing off.  Latency analysis only
+ * (tools/probes/trace_hops.py). */
+int sccl_debug_set_trace(sccl_plan* plan, void* device_buf, int records_per_cta);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,7 +46,8 @@ static_assert(NCW >= 4 && NT == (CW0 + NCW) * 32, "thread layout");
 constexpr int NPART = NT - 32;       // threads of the unaligned path (all but the signaler)
 constexpr int SIGQ = 64;             // tile completion ring (storers -> signaler), indexed by tile number
 constexpr int NSTAGE = kMaxStages;   // barrier sets; stages in use = KParams::nstage (a multiple of NSW)
-constexpr size_t SMEM_HDR = 2048;    // mbarriers, completion ring, control words, ahead of the stages
+constexpr int SIGWIN = 8;            // ops the signaler keeps prepared ahead of their completion
+constexpr size_t SMEM_HDR = 4096;    // mbarriers, completion ring, signaler op window, ahead of the stages
 __host__ __device__ constexpr size_t smem_bytes(int tile, int nstage) { return SMEM_HDR + size_t(nstage) * tile; }
 struct DPart {
   int64_t off, len;
@@ -135,7 +136,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void named_sync(int id) {  // every warp except the signaler
+__device__ __forceinline__ void named_sync(int id) {  // every warp but the signaler
   __syncwarp();
   asm volatile("barrier.sync %0, %1;" ::"r"(id), "n"(NPART) : "memory");
 }
@@ -323,17 +324,30 @@ __device__ void elem_op(const char* const* in, int nin, char* const* out, int no
   }
 }
 
-struct SigEntry {
-  uint32_t op, last;
-  uint64_t end;
+// debug trace (p.trace != nullptr): one record per event, per-CTA region
+__device__ __forceinline__ void trace_ev(const KParams& p, uint32_t* cnt, int ev, uint32_t op, uint32_t tile) {
+  if (!p.trace) return;
+  const uint32_t i = atomicAdd(cnt, 1u);
+  if (i >= uint32_t(p.trace_cap)) return;
+  uint64_t* r = p.trace + (size_t(blockIdx.x) * p.trace_cap + i) * 2;
+  r[0] = globaltimer();
+  r[1] = uint64_t(ev) | (uint64_t(op) << 8) | (uint64_t(tile) << 32);
+}
+
+// one op prepared by the signaler: output o's counter address (or null),
+// the op's per-channel byte range and tiling
+struct SigOp {
+  uint64_t* sig[kMaxOpOut];
+  uint64_t fbase, qlen;
+  uint32_t T, ntiles, every, nout, oi;
 };
 struct Smem {
   uint64_t full[NSTAGE], ready[NSTAGE], empty[NSTAGE];
-  SigEntry q[SIGQ];      // tile `it` -> q[it % SIGQ]: its op, byte end, last-tile bit
-  uint32_t done[SIGQ];   // it + 1 once tile `it`'s stores are complete (storer release, signaler acquire)
-  uint32_t published;    // tiles < published are complete and their counters released (signaler)
-  uint32_t total, total_set;  // tile count of the program (producer, at its end)
+  SigOp win[SIGWIN];     // signaler's op window (ring)
+  uint32_t done[SIGQ];   // it + 1 once tile `it`'s writes have landed (storer release, signaler acquire)
+  uint32_t published;    // tiles < published are complete and their counters released (in tile order)
   uint32_t entry_mask;   // peers whose entry handshake this CTA has seen
+  uint32_t trace_n;      // debug trace records written by this CTA
 };
 static_assert(sizeof(Smem) <= SMEM_HDR, "smem header");
 
@@ -344,13 +358,17 @@ static_assert(sizeof(Smem) <= SMEM_HDR, "smem header");
 //                   Lane o issues the bulk store to output o, every lane
 //                   commits and retires its own bulk group, so a storer
 //                   warp has one tile in flight and posts it to the
-//                   completion ring the moment its writes have landed
-//                   (no lag: a forwarded tile is visible to the next hop
-//                   one store latency after it was issued);
-//   warp SIGW       signaler: walks the completion ring in tile order and
-//                   releases the byte counters of the longest complete
-//                   prefix (one fence per batch, then relaxed stores);
+//                   completion ring the moment its writes have landed;
+//   warp SIGW       signaler: walks the program in the same tile order,
+//                   with every op's counter addresses loaded (lane o:
+//                   output o) before its tiles complete; per batch of
+//                   completed tiles of one op, one fence and one relaxed
+//                   store of the newest byte count (counters are byte
+//                   prefixes, so tiles publish in order);
 //   warps CW0..     compute: REDUCE tiles, f32 accumulate in smem.
+// p.selfpub = 1 (latency-bound plans): the storer warp that completed a
+// tile releases its counters itself once every earlier tile has (no
+// hand-off), at the cost of a fence on the store path.
 // No role blocks on a peer while holding a completed but unreleased tile,
 // so the program order argument of DESIGN.md section 4 gives deadlock
 // freedom without draining heuristics.
@@ -377,13 +395,14 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       mbar_init(&S.ready[s], NCW);
       mbar_init(&S.empty[s], 1);
     }
-    S.published = S.total = S.total_set = 0;
+    S.published = S.trace_n = 0;
     S.entry_mask = 1u << rank;
     s_e = p.epochs[blockIdx.x] + 1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < SIGQ; i += NT) S.done[i] = 0;
   __syncthreads();
+  if (tid == 0) trace_ev(p, &S.trace_n, TR_START, 0, 0);
   const uint64_t e = s_e;
   if (p.multiprocess)  // "rank `rank`, channel ch entered launch e"
     for (int t = tid; t < p.P; t += NT)
@@ -486,6 +505,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
               ready = wait_ge<SYS>(myflags + uint64_t(flag) * p.nch + ch, need, p, rank, ch, int(oi - ob), flag);
           }
           __syncwarp();
+          if (lane == 0) trace_ev(p, &S.trace_n, TR_FLAG, oi, t);
           if (lane == 0) {
             mbar_wait(&S.empty[s], ph ^ 1);
             mbar_arrive_tx(&S.full[s], nv * op.nin);
@@ -501,6 +521,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         for (uint32_t t = 0; t < ntiles; ++t, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
           mbar_wait(&S.full[s], ph);
+          if (warp == CW0 && lane == 0) trace_ev(p, &S.trace_n, TR_FULL, oi, t);
           if (op.kind == 1) {
             const uint64_t lo = uint64_t(t) * T;
             const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
@@ -520,9 +541,15 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       } else {
         // ================= storer warp (stages s with s % NSW == warp - 1) =================
         char* outp = nullptr;
+        uint64_t* sig = nullptr;  // output `lane`'s counter at its destination, if it has one
+        bool every = false;
         if (lane < op.nout) {
           const DevOut d = p.outs[op.out_begin + lane];
           outp = p.base[d.rank][d.space] + d.off + q.off;
+          if (d.flag >= 0) {
+            sig = reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch;
+            every = d.every_tile;
+          }
           if (p.multiprocess && d.rank != rank) await_entry(d.rank, int(oi - ob));
         }
         __syncwarp();
@@ -534,6 +561,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
           const uint32_t nv = n & ~15u;
           mbar_wait(&S.ready[s], ph);
+          if (lane == 0) trace_ev(p, &S.trace_n, TR_READY, oi, t);
           if (n > nv && lane == 0) {  // < 16 B chunk tail: element-wise, global -> global
             const char* in[kMaxOpIn];
             char* out[kMaxOpOut];
@@ -555,56 +583,109 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           if (lane == 0) mbar_arrive(&S.empty[s]);
           bulk_wait<0>();               // writes landed
           fence_proxy_async_global();   // async-proxy writes -> generic observers
-          __syncwarp();
-          if (lane == 0) {
-            while (it - ld_acquire_cta(&S.published) >= SIGQ) __nanosleep(20);
-            S.q[it % SIGQ] = SigEntry{oi, t + 1 == ntiles, lo + n};
+          __syncwarp();                 // (and lane 0's tail writes -> every lane)
+          if (p.selfpub) {
+            if (lane == 0) {
+              trace_ev(p, &S.trace_n, TR_DONE, oi, t);
+              while (ld_acquire_cta(&S.published) != it) {  // earlier tiles publish first
+              }
+            }
+            __syncwarp();
+            if (sig && (every || t + 1 == ntiles)) {
+              fence_rel<SYS>();
+              st_relaxed<SYS>(sig, fbase + lo + n);
+            }
+            __syncwarp();
+            if (lane == 0) {
+              trace_ev(p, &S.trace_n, TR_PUB, oi, uint32_t(lo + n));
+              st_release_cta(&S.published, it + 1);
+            }
+          } else if (lane == 0) {
+            trace_ev(p, &S.trace_n, TR_DONE, oi, t);
+            while (it - ld_acquire_cta(&S.published) >= SIGQ) {  // ring back-pressure
+            }
             st_release_cta(&S.done[it % SIGQ], it + 1);
           }
         }
       }
     }
-    if (warp == 0 && lane == 0) {
-      S.total = it;
-      st_release_cta(&S.total_set, 1);
-    }
-  } else if (lane == 0) {
+  } else if (!p.selfpub) {
     // ================= signaler =================
-    // release the counters of the longest complete prefix of tiles: one
-    // fence per batch, then relaxed stores of the (monotone) byte counts
-    uint32_t next = 0;
+    // Walks the same op / tile sequence as the other roles.  Up to SIGWIN
+    // ops ahead of completion are prepared in shared memory (lane o loads
+    // output o's counter address), so nothing on the signal path waits for a
+    // global load.  Each batch of consecutive completed tiles -- across op
+    // boundaries -- gets one release fence, then one relaxed store of the
+    // newest byte count per counter.
+    uint32_t next_oi = ob, wh = 0, wt = 0, t0 = 0, wtiles = 0;  // window [wh, wt), its unpublished tiles
     for (;;) {
-      uint32_t end = next;
-      while (end - next < SIGQ && ld_acquire_cta(&S.done[end % SIGQ]) == end + 1) ++end;
-      if (end == next) {
-        if (ld_acquire_cta(&S.total_set) && next == S.total) break;
-        __nanosleep(20);
-        continue;
-      }
-      bool fenced = false;
-      for (uint32_t k = next; k != end; ++k) {
-        const SigEntry en = S.q[k % SIGQ];
-        const DevOp op = p.ops[en.op];
+      while (wt - wh < uint32_t(SIGWIN) && next_oi < oe) {  // prepare ops ahead
+        const uint32_t oi = next_oi++;
+        const DevOp op = p.ops[oi];
+        if (op.kind == 2 || int(op.chunk % uint32_t(p.kc)) != cg || !op.vec) continue;
         const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
-        const uint64_t v = (e - 1) * uint64_t(q.len) + en.end;
-        for (int o = 0; o < op.nout; ++o) {
-          const DevOut d = p.outs[op.out_begin + o];
-          if (d.flag >= 0 && (d.every_tile || en.last)) {
-            if (!fenced) {
-              fence_rel<SYS>();
-              fenced = true;
-            }
-            st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
-                            v);
-          }
+        if (q.len == 0) continue;
+        SigOp& w = S.win[wt % SIGWIN];
+        bool every = false;
+        if (lane < op.nout) {
+          const DevOut d = p.outs[op.out_begin + lane];
+          w.sig[lane] = d.flag >= 0 ? reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) +
+                                          uint64_t(d.flag) * p.nch + ch
+                                    : nullptr;
+          every = d.every_tile;
+        }
+        const uint32_t em = __ballot_sync(0xffffffffu, every);
+        const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
+        const uint32_t nt = uint32_t((q.len + T - 1) / T);
+        if (lane == 0) {
+          w.fbase = (e - 1) * uint64_t(q.len);
+          w.qlen = uint64_t(q.len);
+          w.T = T;
+          w.ntiles = nt;
+          w.every = em;
+          w.nout = op.nout;
+          w.oi = oi;
+        }
+        wtiles += nt;
+        ++wt;
+      }
+      __syncwarp();
+      if (wh == wt) break;  // every tile published
+      uint32_t k = 0;       // tiles it, it+1, ... that have landed
+      if (lane == 0)
+        while (k < wtiles && k < uint32_t(SIGQ) && ld_acquire_cta(&S.done[(it + k) % SIGQ]) == it + k + 1) ++k;
+      k = __shfl_sync(0xffffffffu, k, 0);
+      if (k == 0) continue;
+      fence_rel<SYS>();
+      for (uint32_t left = k; left;) {
+        const SigOp& w = S.win[wh % SIGWIN];
+        const uint32_t take = min(left, w.ntiles - t0);
+        const uint32_t tl = t0 + take - 1;  // newest published tile of this op
+        const bool last = tl + 1 == w.ntiles;
+        const uint64_t end = min(uint64_t(tl + 1) * w.T, w.qlen);
+        if (lane < int(w.nout)) {
+          uint64_t* f = w.sig[lane];
+          if (f && (((w.every >> lane) & 1u) || last)) st_relaxed<SYS>(f, w.fbase + end);
+        }
+        if (lane == 0) trace_ev(p, &S.trace_n, TR_PUB, w.oi, uint32_t(end));
+        t0 += take;
+        left -= take;
+        if (last) {
+          ++wh;
+          t0 = 0;
         }
       }
-      next = end;
-      st_release_cta(&S.published, next);
+      __syncwarp();
+      wtiles -= k;
+      it += k;
+      if (lane == 0) st_release_cta(&S.published, it);
     }
   }
   __syncthreads();
-  if (tid == 0) p.epochs[blockIdx.x] = e;
+  if (tid == 0) {
+    trace_ev(p, &S.trace_n, TR_END, 0, 0);
+    p.epochs[blockIdx.x] = e;
+  }
 }
 
 

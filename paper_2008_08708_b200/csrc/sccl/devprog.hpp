@@ -14,7 +14,7 @@ constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
 constexpr int kMaxTile = 65536; // one TMA pipeline stage (bytes)
 constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
 constexpr int kStageBudget = 196608;  // bytes of stages per CTA (nstage * tile)
-constexpr int kThreads = 352;   // producer, kStorerWarps storers, signaler + 6 compute warps
+constexpr int kThreads = 352;   // producer, kStorerWarps storer warps, signaler + 6 compute warps
 constexpr int kStorerWarps = 3; // simple protocol: stage s is stored by warp 1 + s % 3 (nstage % 3 == 0)
 constexpr int kLLThreads = 256; // LL kernel
 constexpr int64_t kLLPart = 4096;       // LL: bytes of a chunk one CTA owns
@@ -64,6 +64,13 @@ struct KParams {
   int entry_base;        // index of the entry-handshake flags in FLAGS
   int multiprocess;      // 1: peers are other processes (entry handshake)
   int ll;                // 1: low-latency protocol (receipts are LL slots)
+  uint64_t* trace;       // debug: per-CTA event records (nullptr = off), sccl_debug_set_trace
+  int trace_cap;         // records per CTA
+  int selfpub;           // 1: storer warps release their own counters (latency-bound plans)
 };
+
+// debug trace events of the simple-protocol kernel (record = {globaltimer ns,
+// event | op << 8 | tile << 32}); see tools/probes/trace_hops.py
+enum TraceEvent : int { TR_START = 0, TR_FLAG = 1, TR_FULL = 2, TR_READY = 3, TR_DONE = 4, TR_PUB = 5, TR_END = 6 };
 
 }  // namespace sccl

@@ -243,3 +243,13 @@ extern "C" int sccl_debug_interpret_loopback(sccl_plan* p, const void* const* se
   }
   return SCCL_OK;
 }
+
+extern "C" int sccl_debug_set_trace(sccl_plan* p, void* buf, int records_per_cta) {
+  if (!p || (buf && records_per_cta <= 0)) {
+    g_ierr = "bad trace arguments";
+    return SCCL_INVALID_ARGUMENT;
+  }
+  p->d_trace = static_cast<uint64_t*>(buf);
+  p->trace_cap = buf ? records_per_cta : 0;
+  return SCCL_OK;
+}

@@ -190,6 +190,27 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   p.nch = kc * kb;
   p.tile = tile;
   p.nstage = nstage;
+  // Counter release: latency-bound plans (at most 16 tiles per CTA) let
+  // each storer warp release its own tile's counters (no hand-off, ~0.3 us
+  // less per hop); longer ones keep the fence off the store path in the
+  // signaler warp, batched across ops.  Crossover from the B200 A/B sweep
+  // (tools/gpu_runs/winsig_round1h.sh: 7 schedules x 64 KiB-128 MiB).
+  {
+    int64_t max_tiles = 0;
+    for (auto& rp : p.pg.ranks)
+      for (int g = 0; g < kc; ++g) {
+        int64_t n = 0;
+        for (auto& op : rp.ops) {
+          if (op.kind == OP_WAIT || std::max(0, op.chunk) % kc != g) continue;
+          const int64_t part = split16(op.len, kb, kb - 1).len;  // the last part is the longest
+          const int64_t T = op.kind == OP_COPY ? tile : std::max<int64_t>(16, (tile / int64_t(op.ins.size())) & ~int64_t(15));
+          n += (part + T - 1) / T;
+        }
+        max_tiles = std::max(max_tiles, n);
+      }
+    p.selfpub = max_tiles <= 16;
+  }
+  if (const char* env = std::getenv("SCCL_SELFPUB")) p.selfpub = std::atoi(env) != 0;
   p.resident_cap = loopback ? resident : 0;
 
   // device encoding
@@ -333,6 +354,9 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.nstage = p.nstage;
   k.ll = p.ll ? 1 : 0;
   k.entry_base = p.entry_base;
+  k.trace = p.d_trace;
+  k.trace_cap = p.trace_cap;
+  k.selfpub = p.selfpub ? 1 : 0;
 }
 
 }  // namespace
@@ -655,7 +679,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

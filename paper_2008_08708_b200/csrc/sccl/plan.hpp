@@ -20,6 +20,7 @@ struct sccl_plan {
   int nch = 1, kc = 1, kb = 1, tile = 32768, nstage = 6;
   int resident_cap = 0;  // loopback: CTAs that fit on the device at once
   bool ll = false;       // low-latency protocol
+  bool selfpub = false;  // simple protocol: storer warps release their own counters (latency-bound plans)
   long long timeout_ns = 0;
 
   // host copy of the device program (also used by the CPU interpreter)
@@ -45,6 +46,8 @@ struct sccl_plan {
   int* h_err = nullptr;  // host-mapped watchdog record
   int* d_err = nullptr;
   int64_t launches = 0;
+  uint64_t* d_trace = nullptr;  // debug trace buffer (caller-owned), sccl_debug_set_trace
+  int trace_cap = 0;
 };
 
 namespace sccl {

@@ -80,6 +80,7 @@ def lib():
         L.sccl_debug_interpret_loopback.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p),
                                                     ctypes.c_double]
         L.sccl_debug_last_error.restype = ctypes.c_char_p
+        L.sccl_debug_set_trace.argtypes = [c_p, c_p, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -193,6 +194,11 @@ class _PlanBase:
 
     def check(self):
         _raise(lib().sccl_plan_check(self._h))
+
+    def set_trace(self, buf=None, records_per_cta: int = 0):
+        """Debug: event trace of the simple-protocol kernel into a zeroed
+        device buffer of grid * records_per_cta * 2 u64 words (None = off)."""
+        _raise(lib().sccl_debug_set_trace(self._h, _ptr(buf) if buf is not None else None, records_per_cta))
 
     @property
     def launch_count(self) -> int:
