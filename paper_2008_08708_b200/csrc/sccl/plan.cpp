@@ -75,7 +75,7 @@ double predict_us(const sccl::Program& pg, int steps, bool ll) {
     for (auto& op : rp.ops)
       if (op.kind != sccl::OP_WAIT) mb += double(op.len) * double(op.ins.size() + op.outs.size());
   mb /= 1e6;
-  return ll ? 5.26 + 0.535 * steps + 0.401 * mb : 4.87 + 3.37 * steps + 0.143 * mb;
+  return ll ? 4.80 + 0.544 * steps + 0.410 * mb : 4.26 + 2.61 * steps + 0.143 * mb;
 }
 
 struct IpcBlob {
@@ -111,8 +111,8 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   // time t = c + alpha*S + beta*MB, where S = schedule steps and MB = bytes
   // the lowered program reads + writes.  Constants are a relative-error
   // least-squares fit to the B200 loopback crossover sweep
-  // (tools/gpu_runs/proto_round1b.sh: 7 schedules x 64 KiB-16 MiB x both
-  // protocols; mean regret vs the per-point best 1.8 %).
+  // (tools/gpu_runs/proto_round1i.sh: 7 schedules x 16 KiB-16 MiB x both
+  // protocols; mean regret vs the per-point best 1.9 %).
   if (req.protocol < 0 || req.protocol > 2) throw invalid_argument_error("protocol must be 0 (auto), 1 (simple), 2 (ll)");
   bool ll = req.protocol == 2;
   if (req.protocol == 0) {
