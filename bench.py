@@ -182,6 +182,7 @@ def run_loopback(args):
     send = [torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev) for _ in range(P)]
     recv = [torch.empty(P * m, dtype=torch.uint8, device=dev) for _ in range(P)]
     stream = torch.cuda.Stream()
+    torch.cuda.synchronize()  # inputs were generated on the default stream
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             plan.launch(send, recv, stream)
@@ -302,6 +303,7 @@ def run_loopback(args):
     if not args.no_sweep and not info["protocol"] == "ll":
         for r in recv:
             r.zero_()
+        torch.cuda.synchronize()  # the zeroing ran on the default stream
         plan.launch_copy_engine(send, recv, stream)
         stream.synchronize()
         assert all(torch.equal(r, want) for r in recv), "bench: copy-engine result wrong"

@@ -17,6 +17,7 @@ from paper_2008_08708_b200 import schedules as S  # noqa: E402
 
 def time_plan(plan, send, recv, iters):
     st = torch.cuda.Stream()
+    torch.cuda.synchronize()  # inputs may come from the default stream
     for _ in range(3):
         plan.launch(send, recv, st)
     st.synchronize()
