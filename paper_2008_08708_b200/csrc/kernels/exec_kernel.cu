@@ -820,11 +820,15 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
   __shared__ const char* s_inp[kMaxOpIn];
   __shared__ char* s_outp[kMaxOpOut];
   __shared__ uint8_t s_inll[kMaxOpIn], s_outll[kMaxOpOut];
+  __shared__ uint32_t s_trace_n;
   if (tid == 0) {
+    s_trace_n = 0;
+    trace_ev(p, &s_trace_n, TR_START, 0, 0);
     s_e = p.epochs[blockIdx.x] + 1;
     s_entry_mask = 1u << rank;
   }
   __syncthreads();
+  if (tid == 0) trace_ev(p, &s_trace_n, TR_FLAG, 0, 0);  // epoch known
   const uint64_t e = s_e;
   const uint32_t ef = uint32_t(e);
   uint64_t* const myflags = reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]);
@@ -868,6 +872,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
       }
     }
     __syncthreads();
+    if (tid == 0) trace_ev(p, &s_trace_n, TR_FULL, oi, 0);  // descriptors read
     const int64_t npair = (q.len + 7) / 8;
     for (int64_t k = tid; k < npair; k += LL_NT) {
       const int n = int(min(int64_t(8), q.len - 8 * k));
@@ -888,9 +893,13 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
       }
     }
     __syncthreads();
+    if (tid == 0) trace_ev(p, &s_trace_n, TR_DONE, oi, 0);  // op's data moved
   }
   __syncthreads();
-  if (tid == 0) p.epochs[blockIdx.x] = e;
+  if (tid == 0) {
+    trace_ev(p, &s_trace_n, TR_END, 0, 0);
+    p.epochs[blockIdx.x] = e;
+  }
 }
 
 template <int DT>
