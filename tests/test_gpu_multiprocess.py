@@ -32,6 +32,8 @@ if W == 2:
         (S.to_json(S.one_shot_allgather(2)), 4096, O.U8, "ll"),
         (S.allreduce_from(S.one_shot_allgather(2)), 1 << 18, O.BF16, "simple"),
         (S.allreduce_from(S.one_shot_allgather(2)), 2048, O.F32, "ll"),
+        # > 16 tiles per CTA: counters released by the windowed signaler warp
+        (S.to_json(S.one_shot_allgather(2)), 32 << 20, O.U8, "simple"),
     ]
 else:  # multi-hop relays and combining trees through IPC-mapped peers
     cases = [
@@ -39,6 +41,7 @@ else:  # multi-hop relays and combining trees through IPC-mapped peers
         (S.allreduce_from(S.recursive_doubling_ring4()), 1 << 16, O.F32, "simple"),
         (S.to_json(S.direct_alltoall(4)), 4096, O.U8, "ll"),
         (S.allreduce_from(S.ring_allgather(4)), 8192, O.BF16, "ll"),
+        (S.to_json(S.ring_allgather(4)), 8 << 20, O.U8, "simple"),  # windowed signaler, sys scope
     ]
 for js, nb, dt, proto in cases:
     d = json.loads(js)
@@ -79,4 +82,4 @@ def test_processes_one_gpu(tmp_path, world):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
     text = "".join(o for o, _ in outs)
-    assert text.count("OK") == 4 * world, text
+    assert text.count("OK") == 5 * world, text

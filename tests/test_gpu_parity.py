@@ -196,6 +196,18 @@ def test_allreduce_large_exact_sum(dt):
         assert torch.equal(r, want)
 
 
+@pytest.mark.parametrize("selfpub", ["0", "1"])
+@pytest.mark.parametrize("name,nbytes", [("ag_777", 4 << 20), ("ar_56_14_14", 4 << 20), ("ag_b7_ring8", 1 << 20),
+                                         ("a2a_b5", 8 << 20), ("ar_822", 1 << 20)])
+def test_counter_release_modes(monkeypatch, selfpub, name, nbytes):
+    """Both counter-release modes of the bulk protocol (storer warps publish
+    their own tiles / the windowed signaler warp), forced, bit-exact."""
+    monkeypatch.setenv("SCCL_SELFPUB", selfpub)
+    js = SCHED[name]
+    dt = O.BF16 if name.startswith("ar") else O.U8
+    run_gpu(js, nbytes, dt, protocol="simple", repeats=2)
+
+
 def test_baseline_full_sizes():
     """BASELINE configs 2-4 at their largest sizes, through size-independent
     properties: AG (7,7,7) at 1 GiB per rank (every output == the
