@@ -208,6 +208,21 @@ def test_counter_release_modes(monkeypatch, selfpub, name, nbytes):
     run_gpu(js, nbytes, dt, protocol="simple", repeats=2)
 
 
+@pytest.mark.parametrize("P", [2, 3, 5, 6, 16])
+@pytest.mark.parametrize("protocol", ["ll", "simple"])
+def test_rank_counts(P, protocol):
+    """Odd, non-power-of-two and the maximum (16, the kernel's pointer
+    table) rank counts: one-shot and ring allgathers, the ring allreduce,
+    the direct alltoall, at an unaligned size."""
+    nb = 8 * 1000 + 48
+    cases = [(S.to_json(S.one_shot_allgather(P)), O.U8), (S.to_json(S.ring_allgather(P)), O.U8),
+             (S.allreduce_from(S.ring_allgather(P)), O.BF16), (S.to_json(S.direct_alltoall(P)), O.U8)]
+    if P <= 8 and P not in (4, 6):  # K_4* and K_6* have no Hamiltonian decomposition
+        cases.append((S.to_json(S.hamiltonian_allgather(P)), O.U8))
+    for js, dt in cases:
+        run_gpu(js, nb if json.loads(js)["collective"] != "alltoall" else P * 1024, dt, protocol=protocol)
+
+
 def test_baseline_full_sizes():
     """BASELINE configs 2-4 at their largest sizes, through size-independent
     properties: AG (7,7,7) at 1 GiB per rank (every output == the
