@@ -68,14 +68,25 @@ int esize_of(int dtype) {
   throw sccl::invalid_argument_error("unknown dtype");
 }
 
-// predicted loopback time (us) of a lowered program, see plan_build_host
-double predict_us(const sccl::Program& pg, int steps, bool ll) {
+// predicted time (us) of a lowered program, see plan_build_host.  sys:
+// system-scope signalling (multi-process mode), whose release fences make
+// every bulk-protocol step ~1.7 us dearer (fit with SCCL_LOOPBACK_SYS=1).
+double predict_us(const sccl::Program& pg, int steps, bool ll, bool sys = false) {
   double mb = 0;
   for (auto& rp : pg.ranks)
     for (auto& op : rp.ops)
       if (op.kind != sccl::OP_WAIT) mb += double(op.len) * double(op.ins.size() + op.outs.size());
   mb /= 1e6;
-  return ll ? 4.80 + 0.544 * steps + 0.410 * mb : 4.26 + 2.61 * steps + 0.143 * mb;
+  if (ll) return sys ? 5.10 + 0.562 * steps + 0.408 * mb : 4.80 + 0.544 * steps + 0.410 * mb;
+  return sys ? 4.31 + 4.28 * steps + 0.156 * mb : 4.26 + 2.61 * steps + 0.143 * mb;
+}
+
+bool loopback_sys() {  // SCCL_LOOPBACK_SYS=1: loopback launches use system scope (measurement only)
+  static const bool v = [] {
+    const char* e = std::getenv("SCCL_LOOPBACK_SYS");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
 }
 
 struct IpcBlob {
@@ -119,7 +130,8 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     int steps = 0;
     for (auto* ph : p.sched.flat()) steps += ph->S;
     const Program a = lower(p.sched, bytes, es, true), b = lower(p.sched, bytes, es, false);
-    ll = predict_us(a, steps, true) < predict_us(b, steps, false);
+    const bool sys = !loopback || loopback_sys();
+    ll = predict_us(a, steps, true, sys) < predict_us(b, steps, false, sys);
     p.pg = ll ? a : b;
   } else {
     p.pg = lower(p.sched, bytes, es, ll);
@@ -620,7 +632,9 @@ int sccl_launch_loopback(sccl_plan* p, const void* const* sendbufs, void* const*
     k.nranks_launch = p->nranks;
     k.multiprocess = 0;
     cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
-    cuda_check(launch_exec(k, p->dtype, false, static_cast<cudaStream_t>(stream)), "launch");
+    // SCCL_LOOPBACK_SYS=1 (measurement only): system-scope fences and flags,
+    // as in multi-process mode, to price that mode's signalling on one GPU
+    cuda_check(launch_exec(k, p->dtype, loopback_sys(), static_cast<cudaStream_t>(stream)), "launch");
     p->launches++;
   });
 }
