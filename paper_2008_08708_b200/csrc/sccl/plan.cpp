@@ -220,7 +220,10 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
         }
         max_tiles = std::max(max_tiles, n);
       }
-    p.selfpub = max_tiles <= 16;
+    // system scope (multi-process) makes the fence on the store path ~3x
+    // dearer, so only very short plans self-publish there (measured with
+    // SCCL_LOOPBACK_SYS=1, tools/gpu_runs/sys_pub_round1n.sh)
+    p.selfpub = max_tiles <= ((!loopback || loopback_sys()) ? 4 : 16);
   }
   if (const char* env = std::getenv("SCCL_SELFPUB")) p.selfpub = std::atoi(env) != 0;
   p.resident_cap = loopback ? resident : 0;
