@@ -168,6 +168,22 @@ __device__ __noinline__ void watchdog_fire(const KParams& p, int rank, int ch, i
   __trap();
 }
 
+// mbarrier phase wait bounded by the watchdog: a pipeline hand-off that
+// never completes (a bug, not a peer) traps instead of hanging the GPU.
+__device__ __noinline__ void mbar_wait_slow(uint64_t* b, uint32_t parity, const KParams& p, int rank, int ch,
+                                            int op) {
+  const uint64_t t0 = globaltimer();
+  for (uint32_t spins = 1;; ++spins) {
+    if (mbar_try(b, parity)) return;
+    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
+      watchdog_fire(p, rank, ch, op, -4, parity, 0);
+  }
+}
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* b, uint32_t parity, const KParams& p, int rank, int ch,
+                                             int op) {
+  if (!mbar_try(b, parity)) mbar_wait_slow(b, parity, p, rank, ch, op);
+}
+
 // Spin until *f >= target; returns the value seen.  Bounded by timeout_ns.
 template <bool SYS>
 __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p, int rank, int ch, int op,
@@ -342,7 +358,11 @@ struct SigOp {
   uint32_t T, ntiles, every, nout, oi;
 };
 struct Smem {
-  uint64_t full[NSTAGE], ready[NSTAGE], empty[NSTAGE];
+  // per stage: full = a COPY tile landed (storer waits), fullr = a REDUCE
+  // tile's inputs landed (compute warps wait), ready = reduced tile in smem
+  // (storer waits), empty = stage read out (producer waits).  Each barrier
+  // counts only the uses that touch it, so no role can alias a phase.
+  uint64_t full[NSTAGE], fullr[NSTAGE], ready[NSTAGE], empty[NSTAGE];
   SigOp win[SIGWIN];     // signaler's op window (ring)
   uint32_t done[SIGQ];   // it + 1 once tile `it`'s writes have landed (storer release, signaler acquire)
   uint32_t published;    // tiles < published are complete and their counters released (in tile order)
@@ -392,6 +412,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   if (tid == 0) {
     for (int s = 0; s < p.nstage; ++s) {
       mbar_init(&S.full[s], 1);
+      mbar_init(&S.fullr[s], 1);
       mbar_init(&S.ready[s], NCW);
       mbar_init(&S.empty[s], 1);
     }
@@ -414,6 +435,10 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   const uint32_t ob = p.prog[rank * p.kc + cg], oe = p.prog[rank * p.kc + cg + 1];
   uint32_t it = 0;  // tile number (same sequence in every role)
   const uint32_t my_stage_class = uint32_t(warp - 1);  // storer warps
+  // bit s = parity of stage s's next phase of a barrier that only some uses
+  // touch: storers track `full` (copy uses) and `ready` (reduce uses),
+  // compute warps `fullr` (reduce uses)
+  uint32_t cpar = 0, rpar = 0;
 
   // entry handshake before the first store into peer d (multi-process only)
   auto await_entry = [&](int d, int opi) {
@@ -506,23 +531,25 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           }
           __syncwarp();
           if (lane == 0) trace_ev(p, &S.trace_n, TR_FLAG, oi, t);
+          uint64_t* const fb = op.kind == 1 ? &S.fullr[s] : &S.full[s];
           if (lane == 0) {
-            mbar_wait(&S.empty[s], ph ^ 1);
-            mbar_arrive_tx(&S.full[s], nv * op.nin);
+            mbar_wait_wd(&S.empty[s], ph ^ 1, p, rank, ch, int(oi - ob));
+            mbar_arrive_tx(fb, nv * op.nin);
           }
           __syncwarp();
           if (lane < op.nin && nv) {
             fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
-            bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, &S.full[s]);
+            bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, fb);
           }
         }
       } else if (warp >= CW0) {
-        // ================= compute (REDUCE only; others just pass) =================
+        // ================= compute (REDUCE tiles; copy tiles go straight to the storer) =================
         for (uint32_t t = 0; t < ntiles; ++t, ++it) {
-          const uint32_t s = it % NST, ph = (it / NST) & 1;
-          mbar_wait(&S.full[s], ph);
-          if (warp == CW0 && lane == 0) trace_ev(p, &S.trace_n, TR_FULL, oi, t);
+          const uint32_t s = it % NST;
           if (op.kind == 1) {
+            mbar_wait_wd(&S.fullr[s], (rpar >> s) & 1u, p, rank, ch, int(oi - ob));
+            rpar ^= 1u << s;
+            if (warp == CW0 && lane == 0) trace_ev(p, &S.trace_n, TR_FULL, oi, t);
             const uint64_t lo = uint64_t(t) * T;
             const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
             uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
@@ -534,9 +561,9 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
               b0[v] = acc.out();
             }
             fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.ready[s]);
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&S.ready[s]);
         }
       } else {
         // ================= storer warp (stages s with s % NSW == warp - 1) =================
@@ -556,11 +583,17 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         for (uint32_t t = 0; t < ntiles; ++t, ++it) {
           const uint32_t s = it % NST;
           if (s % NSW != my_stage_class) continue;
-          const uint32_t ph = (it / NST) & 1;
           const uint64_t lo = uint64_t(t) * T;
           const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
           const uint32_t nv = n & ~15u;
-          mbar_wait(&S.ready[s], ph);
+          if (op.kind == 1) {  // reduce: the compute warps' result
+            mbar_wait_wd(&S.ready[s], (rpar >> s) & 1u, p, rank, ch, int(oi - ob));
+            rpar ^= 1u << s;
+          } else {  // copy: the loaded tile itself
+            mbar_wait_wd(&S.full[s], (cpar >> s) & 1u, p, rank, ch, int(oi - ob));
+            cpar ^= 1u << s;
+            if (lane == 0) trace_ev(p, &S.trace_n, TR_FULL, oi, t);
+          }
           if (lane == 0) trace_ev(p, &S.trace_n, TR_READY, oi, t);
           if (n > nv && lane == 0) {  // < 16 B chunk tail: element-wise, global -> global
             const char* in[kMaxOpIn];

@@ -19,3 +19,12 @@ def _built():
     import subprocess
     subprocess.check_call(["make", "-s", "-j8", "all"], cwd=ROOT, stdout=subprocess.DEVNULL)
     yield
+
+
+def pytest_collection_modifyitems(config, items):
+    """Bound every GPU test (pytest-timeout): a kernel that never finishes
+    fails its test instead of stalling the suite.  The kernel's own watchdog
+    (10 s default) normally traps first."""
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(300))
