@@ -110,10 +110,13 @@ __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
   else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// release fence before a flag store.  fence.release (PTX 8.6) is MEMBAR
+// without the L1 invalidation (CCTL.IVALL) that fence.acq_rel adds: every
+// use here is a release pattern, the acquire side uses ld.acquire.
 template <bool SYS>
 __device__ __forceinline__ void fence_rel() {
-  if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
-  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (SYS) asm volatile("fence.release.sys;" ::: "memory");
+  else asm volatile("fence.release.gpu;" ::: "memory");
 }
 template <bool SYS>
 __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {

@@ -1,0 +1,7 @@
+# release-only fences on the signal path (no L1 invalidation): parity, hop trace, sizes, sys scope, bench
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 300 python tools/probes/trace_hops.py 16384:1 262144:8 1048576:32 > gpurun_out/trace_fencerel.jsonl 2>&1
+SCCL_LOOPBACK_SYS=1 timeout 300 python tools/probes/trace_hops.py 16384:1 262144:8 > gpurun_out/trace_fencerel_sys.jsonl 2>&1
+timeout 600 python tools/tune.py '{"scheds":["ag777","ring","ar56","ar_ring","ar822","ag111","a2a"],"sizes":[65536,262144,1048576,4194304,16777216,134217728],"knobs":[{"protocol":"simple"}]}' > gpurun_out/tune_fencerel.jsonl 2>&1
+timeout 400 python bench.py --no-sweep --cpu-seconds 1 > gpurun_out/bench.log 2>&1
