@@ -13,6 +13,10 @@
  * Threading: plans are immutable after creation and
  * bind; at most one launch of a plan may be in flight per stream order;
  * distinct plans may run concurrently.  sccl_last_error is thread-local.
+ * Co-residency: a launch's CTAs wait on each other (loopback: across ranks
+ * on the one device), so concurrent launches on one device must fit
+ * together (sccl_plan_info reports "grid"); a loopback plan sized by
+ * default to the whole device should not overlap another launch.
  */
 #ifndef SCCL_EXEC_H
 #define SCCL_EXEC_H

@@ -223,6 +223,35 @@ def test_rank_counts(P, protocol):
         run_gpu(js, nb if json.loads(js)["collective"] != "alltoall" else P * 1024, dt, protocol=protocol)
 
 
+def test_concurrent_distinct_plans():
+    """Three loopback plans (both protocols) with disjoint flags/scratch on
+    three streams at once (grids that fit together), each bit-exact."""
+    cases = [(SCHED["ag_b7_ring8"], 4096, O.U8, 5, "ll"), (SCHED["ar_822"], 1 << 16, O.BF16, 6, "ll"),
+             (SCHED["ag_777"], 1 << 20, O.U8, 7, "simple")]
+    plans = [sccl.LoopbackPlan(js, nb, dt, device=0, nchannels=2, chunk_groups=1, protocol=pr)
+             for js, nb, dt, _, pr in cases]
+    assert sum(pl.info()["grid"] for pl in plans) <= 148
+    outs = []
+    for plan, (js, nb, dt, seed, _) in zip(plans, cases):
+        d = json.loads(js)
+        ins = O.seeded_inputs(d["collective"], d["P"], nb, dt, seed)
+        ref = O.execute(d, ins, nb, dt)
+        send = [torch.from_numpy(x).to(DEV) for x in ins]
+        recv = [torch.zeros(r.size, dtype=torch.uint8, device=DEV) for r in ref]
+        outs.append((plan, send, recv, ref))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in outs]
+    for _ in range(5):
+        for (plan, send, recv, _), st in zip(outs, streams):
+            plan.launch(send, recv, st)
+    torch.cuda.synchronize()
+    for plan, send, recv, ref in outs:
+        plan.check()
+        for a, b in zip(recv, ref):
+            assert np.array_equal(a.cpu().numpy(), b)
+        plan.close()
+
+
 def test_baseline_full_sizes():
     """BASELINE configs 2-4 at their largest sizes, through size-independent
     properties: AG (7,7,7) at 1 GiB per rank (every output == the
