@@ -357,7 +357,7 @@ __device__ __forceinline__ void trace_ev(const KParams& p, uint32_t* cnt, int ev
 // the op's per-channel byte range and tiling
 struct SigOp {
   uint64_t* sig[kMaxOpOut];
-  uint64_t fbase, qlen;
+  uint64_t fbase, qlen, wlo, whi;  // the op's counter base and part length; this item's byte window
   uint32_t T, ntiles, every, nout, oi;
 };
 struct Smem {
@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   __shared__ const char* s_inp[kMaxOpIn];
   __shared__ char* s_outp[kMaxOpOut];
   __shared__ uint64_t s_e;
+  __shared__ uint32_t s_nwin;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int lr = blockIdx.x / p.nch, ch = blockIdx.x % p.nch;
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
     S.published = S.trace_n = 0;
     S.entry_mask = 1u << rank;
     s_e = p.epochs[blockIdx.x] + 1;
+    s_nwin = p.nwin ? p.nwin[blockIdx.x] : 1u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < SIGQ; i += NT) S.done[i] = 0;
@@ -451,11 +453,28 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
     }
   };
 
+  // Window-major order (p.window > 0): the CTA walks byte window w of every
+  // op before window w+1 of any, so a receipt is forwarded or reduced a few
+  // tiles after it landed, while it is still in L2, instead of one whole op
+  // later.  Every role walks the same (window, op, tile) sequence.
+  const uint32_t W = p.window;
+  const uint32_t nwin = s_nwin;
+  auto item = [&](const DevOp& op, uint32_t w, DPart& q, uint64_t& wlo, uint64_t& whi) -> bool {
+    if (op.kind == 2 || int(op.chunk % uint32_t(p.kc)) != cg) return false;
+    q = dsplit16(int64_t(op.len), p.kb, cb);
+    if (q.len == 0) return false;  // empty sub-range: nothing sent, nothing awaited
+    wlo = W ? uint64_t(w) * W : 0;
+    if (wlo >= uint64_t(q.len)) return false;
+    whi = W ? min(uint64_t(q.len), wlo + W) : uint64_t(q.len);
+    return true;
+  };
+
   if (warp != SIGW) {
+    for (uint32_t w = 0; w < nwin; ++w)
     for (uint32_t oi = ob; oi < oe; ++oi) {
       const DevOp op = p.ops[oi];
-      if (op.kind == 2) {  // end-of-program waits: every receipt has landed
-        if (warp == 0)
+      if (op.kind == 2) {  // end-of-program waits (after the last window): every receipt has landed
+        if (warp == 0 && w + 1 == nwin)
           for (int i = lane; i < op.nin; i += 32) {
             const DevIn in = p.ins[op.in_begin + i];
             if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
@@ -465,15 +484,15 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           }
         continue;
       }
-      if (int(op.chunk % uint32_t(p.kc)) != cg) continue;  // another channel's chunk group
-      const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
-      if (q.len == 0) continue;  // empty sub-range: nothing sent, nothing awaited
+      DPart q;
+      uint64_t wlo, whi;
+      if (!item(op, w, q, wlo, whi)) continue;
       const uint64_t fbase = (e - 1) * uint64_t(q.len);
 
       if (!op.vec) {
-        // ---- unaligned op: whole CTA (but the signaler), element-wise, synchronous.
-        // Every earlier tile's stores are complete: each storer warp retires
-        // its tile before it moves on.
+        // ---- unaligned op (op-major plans only): whole CTA (but the signaler),
+        // element-wise, synchronous.  Every earlier tile's stores are
+        // complete: each storer warp retires its tile before it moves on.
         const int ptid = tid < 32 * SIGW ? tid : tid - 32;
         named_sync(1);
         if (tid < op.nin) {
@@ -505,9 +524,9 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         continue;
       }
 
-      // ---- pipelined op ----
+      // ---- pipelined op: tiles of this window ----
       const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
-      const uint32_t ntiles = uint32_t((q.len + T - 1) / T);
+      const uint32_t ntiles = uint32_t((whi - wlo + T - 1) / T);
 
       if (warp == 0) {
         // ================= producer =================
@@ -524,8 +543,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         __syncwarp();
         for (uint32_t t = 0; t < ntiles; ++t, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
-          const uint64_t lo = uint64_t(t) * T;
-          const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
+          const uint64_t lo = wlo + uint64_t(t) * T;
+          const uint32_t n = uint32_t(min(uint64_t(T), whi - lo));
           const uint32_t nv = n & ~15u;
           if (flag >= 0) {
             const uint64_t need = fbase + lo + n;
@@ -553,8 +572,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             mbar_wait_wd(&S.fullr[s], (rpar >> s) & 1u, p, rank, ch, int(oi - ob));
             rpar ^= 1u << s;
             if (warp == CW0 && lane == 0) trace_ev(p, &S.trace_n, TR_FULL, oi, t);
-            const uint64_t lo = uint64_t(t) * T;
-            const uint32_t nv = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo)) >> 4;
+            const uint64_t lo = wlo + uint64_t(t) * T;
+            const uint32_t nv = uint32_t(min(uint64_t(T), whi - lo)) >> 4;
             uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
             for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
               Vec<DT> acc;
@@ -586,8 +605,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         for (uint32_t t = 0; t < ntiles; ++t, ++it) {
           const uint32_t s = it % NST;
           if (s % NSW != my_stage_class) continue;
-          const uint64_t lo = uint64_t(t) * T;
-          const uint32_t n = uint32_t(min(uint64_t(T), uint64_t(q.len) - lo));
+          const uint64_t lo = wlo + uint64_t(t) * T;
+          const uint32_t n = uint32_t(min(uint64_t(T), whi - lo));
           const uint32_t nv = n & ~15u;
           if (op.kind == 1) {  // reduce: the compute warps' result
             mbar_wait_wd(&S.ready[s], (rpar >> s) & 1u, p, rank, ch, int(oi - ob));
@@ -627,7 +646,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
               }
             }
             __syncwarp();
-            if (sig && (every || t + 1 == ntiles)) {
+            if (sig && (every || lo + n == uint64_t(q.len))) {
               fence_rel<SYS>();
               st_relaxed<SYS>(sig, fbase + lo + n);
             }
@@ -647,40 +666,47 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
     }
   } else if (!p.selfpub) {
     // ================= signaler =================
-    // Walks the same op / tile sequence as the other roles.  Up to SIGWIN
-    // ops ahead of completion are prepared in shared memory (lane o loads
-    // output o's counter address), so nothing on the signal path waits for a
-    // global load.  Each batch of consecutive completed tiles -- across op
-    // boundaries -- gets one release fence, then one relaxed store of the
-    // newest byte count per counter.
-    uint32_t next_oi = ob, wh = 0, wt = 0, t0 = 0, wtiles = 0;  // window [wh, wt), its unpublished tiles
+    // Walks the same (window, op, tile) sequence as the other roles.  Up to
+    // SIGWIN items ahead of completion are prepared in shared memory (lane o
+    // loads output o's counter address), so nothing on the signal path waits
+    // for a global load.  Each batch of consecutive completed tiles -- across
+    // item boundaries -- gets one release fence, then one relaxed store of
+    // the newest byte count per counter.
+    uint32_t nw = ob < oe ? 0 : nwin, next_oi = ob, wh = 0, wt = 0, t0 = 0, wtiles = 0;  // items [wh, wt)
     for (;;) {
-      while (wt - wh < uint32_t(SIGWIN) && next_oi < oe) {  // prepare ops ahead
-        const uint32_t oi = next_oi++;
+      while (wt - wh < uint32_t(SIGWIN) && nw < nwin) {  // prepare items ahead
+        const uint32_t oi = next_oi, w = nw;
+        if (++next_oi == oe) {
+          next_oi = ob;
+          ++nw;
+        }
+        if (oi >= oe) continue;
         const DevOp op = p.ops[oi];
-        if (op.kind == 2 || int(op.chunk % uint32_t(p.kc)) != cg || !op.vec) continue;
-        const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
-        if (q.len == 0) continue;
-        SigOp& w = S.win[wt % SIGWIN];
+        DPart q;
+        uint64_t wlo, whi;
+        if (!op.vec || !item(op, w, q, wlo, whi)) continue;
+        SigOp& x = S.win[wt % SIGWIN];
         bool every = false;
         if (lane < op.nout) {
           const DevOut d = p.outs[op.out_begin + lane];
-          w.sig[lane] = d.flag >= 0 ? reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) +
+          x.sig[lane] = d.flag >= 0 ? reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) +
                                           uint64_t(d.flag) * p.nch + ch
                                     : nullptr;
           every = d.every_tile;
         }
         const uint32_t em = __ballot_sync(0xffffffffu, every);
         const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
-        const uint32_t nt = uint32_t((q.len + T - 1) / T);
+        const uint32_t nt = uint32_t((whi - wlo + T - 1) / T);
         if (lane == 0) {
-          w.fbase = (e - 1) * uint64_t(q.len);
-          w.qlen = uint64_t(q.len);
-          w.T = T;
-          w.ntiles = nt;
-          w.every = em;
-          w.nout = op.nout;
-          w.oi = oi;
+          x.fbase = (e - 1) * uint64_t(q.len);
+          x.qlen = uint64_t(q.len);
+          x.wlo = wlo;
+          x.whi = whi;
+          x.T = T;
+          x.ntiles = nt;
+          x.every = em;
+          x.nout = op.nout;
+          x.oi = oi;
         }
         wtiles += nt;
         ++wt;
@@ -694,19 +720,20 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       if (k == 0) continue;
       fence_rel<SYS>();
       for (uint32_t left = k; left;) {
-        const SigOp& w = S.win[wh % SIGWIN];
-        const uint32_t take = min(left, w.ntiles - t0);
-        const uint32_t tl = t0 + take - 1;  // newest published tile of this op
-        const bool last = tl + 1 == w.ntiles;
-        const uint64_t end = min(uint64_t(tl + 1) * w.T, w.qlen);
-        if (lane < int(w.nout)) {
-          uint64_t* f = w.sig[lane];
-          if (f && (((w.every >> lane) & 1u) || last)) st_relaxed<SYS>(f, w.fbase + end);
+        const SigOp& x = S.win[wh % SIGWIN];
+        const uint32_t take = min(left, x.ntiles - t0);
+        const uint32_t tl = t0 + take - 1;  // newest published tile of this item
+        const bool item_done = tl + 1 == x.ntiles;
+        const uint64_t end = min(x.wlo + uint64_t(tl + 1) * x.T, x.whi);
+        const bool last = end == x.qlen;  // the op's final byte
+        if (lane < int(x.nout)) {
+          uint64_t* f = x.sig[lane];
+          if (f && (((x.every >> lane) & 1u) || last)) st_relaxed<SYS>(f, x.fbase + end);
         }
-        if (lane == 0) trace_ev(p, &S.trace_n, TR_PUB, w.oi, uint32_t(end));
+        if (lane == 0) trace_ev(p, &S.trace_n, TR_PUB, x.oi, uint32_t(end));
         t0 += take;
         left -= take;
-        if (last) {
+        if (item_done) {
           ++wh;
           t0 = 0;
         }

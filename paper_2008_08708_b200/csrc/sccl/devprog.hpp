@@ -67,6 +67,8 @@ struct KParams {
   uint64_t* trace;       // debug: per-CTA event records (nullptr = off), sccl_debug_set_trace
   int trace_cap;         // records per CTA
   int selfpub;           // 1: storer warps release their own counters (latency-bound plans)
+  uint32_t window;       // simple protocol: bytes of an op a CTA moves before the next op (0 = whole op)
+  const uint32_t* nwin;  // [launched CTAs] windows of each CTA's program
 };
 
 // debug trace events of the simple-protocol kernel (record = {globaltimer ns,

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
@@ -291,6 +292,49 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     }
   p.prog[size_t(P) * p.kc] = uint32_t(p.ops.size());
 
+  // Window-major execution (simple protocol, every op 16-byte aligned, some
+  // op reads a receipt -- a relay or a reduction): a CTA moves one byte
+  // window of each op, in program order, before the next window, so relayed
+  // and reduced receipts are read back while they are still in L2.  The
+  // window is one tile when a CTA has several ops per step (the other ops of
+  // the step cover the hop latency), up to 4 tiles when it has one (a ring);
+  // measured on B200 (tools/gpu_runs/window_round1r.sh).  Schedules that
+  // never re-read a receipt (one-shot, direct alltoall) stay op-major: the
+  // per-window descriptor reloads would only cost.  SCCL_WINDOW=<bytes>
+  // overrides (0 = op-major).
+  {
+    bool all_vec = true, rereads = false;
+    size_t nops0 = 0;
+    for (size_t i = 0; i < p.ops.size(); ++i) {
+      const DevOp& d = p.ops[i];
+      if (d.kind == OP_WAIT) continue;
+      all_vec &= d.vec != 0;
+      for (uint32_t k = 0; k < d.nin; ++k) rereads |= p.ins[d.in_begin + k].flag >= 0;
+      if (i < p.prog[size_t(p.kc)]) ++nops0;  // rank 0's ops, all chunk groups
+    }
+    int steps = 0;
+    for (auto* ph : p.sched.flat()) steps += ph->S;
+    const double ops_per_step = double(nops0) / double(std::max(1, p.kc * steps));
+    const int m = std::max(1, std::min(4, int(std::ceil(4.0 / std::max(ops_per_step, 1e-9)))));
+    p.window = (!p.ll && all_vec && rereads) ? uint32_t(p.tile) * uint32_t(m) : 0u;
+    if (const char* env = std::getenv("SCCL_WINDOW")) {
+      const long w = std::atol(env);
+      p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
+    }
+    const int nl = loopback ? P : 1;
+    p.nwin.assign(size_t(nl) * p.nch, 1u);
+    for (int lr = 0; lr < nl; ++lr) {
+      const int r = loopback ? lr : p.rank;
+      for (int ch = 0; ch < p.nch; ++ch) {
+        const int cg = ch % p.kc, cb = ch / p.kc;
+        int64_t maxq = 0;
+        for (uint32_t o = p.prog[size_t(r) * p.kc + cg]; o < p.prog[size_t(r) * p.kc + cg + 1]; ++o)
+          if (p.ops[o].kind != OP_WAIT) maxq = std::max(maxq, split16(int64_t(p.ops[o].len), p.kb, cb).len);
+        if (p.window) p.nwin[size_t(lr) * p.nch + ch] = uint32_t(std::max<int64_t>(1, (maxq + p.window - 1) / p.window));
+      }
+    }
+  }
+
   // memory layout of one rank's region
   auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
   p.entry_base = p.pg.max_slots * p.nch;
@@ -319,6 +363,7 @@ void plan_device_setup(sccl_plan& p) {
   upload(p.ins, &p.d_ins);
   upload(p.outs, &p.d_outs);
   upload(p.prog, &p.d_prog);
+  upload(p.nwin, &p.d_nwin);
   int nlaunch = p.loopback ? p.nranks : 1;
   size_t ne = size_t(nlaunch) * p.nch;
   cuda_check(cudaMalloc(&p.d_epochs, ne * sizeof(uint64_t)), "cudaMalloc(epochs)");
@@ -358,6 +403,8 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.ins = p.d_ins;
   k.outs = p.d_outs;
   k.prog = p.d_prog;
+  k.window = p.window;
+  k.nwin = p.d_nwin;
   k.epochs = p.d_epochs;
   k.errinfo = p.d_err;
   k.timeout_ns = p.timeout_ns;
@@ -696,7 +743,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";
@@ -716,6 +763,7 @@ int sccl_plan_destroy(sccl_plan* p) {
     cudaFree(p->d_ins);
     cudaFree(p->d_outs);
     cudaFree(p->d_prog);
+    cudaFree(p->d_nwin);
     cudaFree(p->d_epochs);
     cudaFree(p->d_region);
     if (p->h_err) cudaFreeHost(p->h_err);

@@ -28,12 +28,15 @@ struct sccl_plan {
   std::vector<sccl::DevIn> ins;
   std::vector<sccl::DevOut> outs;
   std::vector<uint32_t> prog;  // [P*kc+1]: op range per (rank, chunk group)
+  uint32_t window = 0;         // simple protocol: window-major byte window (0 = op-major)
+  std::vector<uint32_t> nwin;  // [launched CTAs] windows of each CTA's program
 
   // device program
   sccl::DevOp* d_ops = nullptr;
   sccl::DevIn* d_ins = nullptr;
   sccl::DevOut* d_outs = nullptr;
   uint32_t* d_prog = nullptr;
+  uint32_t* d_nwin = nullptr;
   uint64_t* d_epochs = nullptr;
 
   // plan memory: per rank region = [flags | scratch | recv (multi-process)]
