@@ -14,7 +14,9 @@ GPU times: K launches captured in one CUDA graph, CUDA events around the
 replay (host launch cost excluded), after 3 warm-up launches; no L2 flush
 (sizes < 126 MB are L2-resident between launches, as in nccl-tests).
 busbw per rank follows nccl-tests: AG (P-1)m, AR 2(P-1)/P M, A2A (P-1)/P M.
-hbm_frac = algorithmic HBM bytes of the lowered program / t / measured peak.
+hbm_frac = algorithmic HBM bytes of the lowered program / t / measured peak
+(can pass 1: window-major execution re-reads relayed receipts from L2);
+frac_of_min = (inputs read once + outputs written once) / t / peak.
 
 usage: python tools/size_sweep.py [cfg1,cfg2,cfg3,cfg4] [--max-log2 N]
 """
@@ -80,8 +82,10 @@ def gpu_sweep(cfg, coll, scheds, dtypes, sizes):
                 us = time_plan(plan, [x[:sz] for x in send], [x[:plan.recv_bytes] for x in recv], iters_for(sz))
                 info = plan.info()
                 hb = hbm_bytes(plan)
+                mn = P * sz + P * P * sz if coll == "allgather" else 2 * P * sz  # inputs once + outputs once
                 row.update({"us": round(us, 2), "busbw_per_rank_GBps": round(busbytes(coll, sz) / us / 1e3, 2),
                             "hbm_GBps": round(hb / us / 1e3, 1), "hbm_frac": round(hb / us / 1e3 / pk, 3),
+                            "frac_of_min": round(mn / us / 1e3 / pk, 3),
                             "protocol": info["protocol"], "grid": info["grid"], "tile": info["tile_bytes"],
                             "nstage": info["nstage"]})
                 print(json.dumps(row), flush=True)
