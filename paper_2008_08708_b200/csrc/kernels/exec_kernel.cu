@@ -91,6 +91,32 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint
                "r"(bytes)
                : "memory");
 }
+// L2 eviction policies for bulk copies: receipts that a later op of the
+// receiver reads (forwards, reduce inputs) are kept; data read or written
+// for the last time is evicted first, so it does not push those out.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_load_hint(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store_hint(void* dst, const void* src_smem, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src_smem)), "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -444,6 +470,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   // touch: storers track `full` (copy uses) and `ready` (reduce uses),
   // compute warps `fullr` (reduce uses)
   uint32_t cpar = 0, rpar = 0;
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
   // entry handshake before the first store into peer d (multi-process only)
   auto await_entry = [&](int d, int opi) {
@@ -561,7 +588,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           __syncwarp();
           if (lane < op.nin && nv) {
             fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
-            bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, fb);
+            if (p.l2hint) bulk_load_hint(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, fb, pol_first);
+            else bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, fb);
           }
         }
       } else if (warp >= CW0) {
@@ -631,7 +659,10 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             if (op.kind == 0) elem_op<0>(in, 1, out, op.nout, int64_t(lo + nv), n - nv, 0, 1);
             else elem_op<DT>(in, op.nin, out, op.nout, int64_t(lo + nv), n - nv, 0, 1);
           }
-          if (outp && nv) bulk_store(outp + lo, bufs + size_t(s) * STAGE, nv);
+          if (outp && nv) {
+            if (p.l2hint) bulk_store_hint(outp + lo, bufs + size_t(s) * STAGE, nv, every ? pol_last : pol_first);
+            else bulk_store(outp + lo, bufs + size_t(s) * STAGE, nv);
+          }
           bulk_commit();
           bulk_wait_read<0>();  // smem read: the stage goes back to the producer
           __syncwarp();

@@ -69,6 +69,7 @@ struct KParams {
   int selfpub;           // 1: storer warps release their own counters (latency-bound plans)
   uint32_t window;       // simple protocol: bytes of an op a CTA moves before the next op (0 = whole op)
   const uint32_t* nwin;  // [launched CTAs] windows of each CTA's program
+  int l2hint;            // 1: L2 eviction hints on bulk copies (launch traffic >> L2)
 };
 
 // debug trace events of the simple-protocol kernel (record = {globaltimer ns,

@@ -321,6 +321,17 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
       const long w = std::atol(env);
       p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
     }
+    // L2 eviction hints (keep receipts a later op re-reads, evict single-use
+    // data first) only pay when a launch streams well past the 126 MB L2;
+    // below that everything stays resident and the hints only evict what
+    // the next launch or the caller would reuse.
+    double launch_bytes = 0;
+    for (auto& rp : p.pg.ranks)
+      for (auto& op : rp.ops)
+        if (op.kind != OP_WAIT) launch_bytes += double(op.len) * double(op.ins.size() + op.outs.size());
+    if (!loopback) launch_bytes *= 1.0 / P;  // this rank's share
+    p.l2hint = !p.ll && launch_bytes > 512e6;
+    if (const char* env = std::getenv("SCCL_L2HINT")) p.l2hint = std::atoi(env) != 0;
     const int nl = loopback ? P : 1;
     p.nwin.assign(size_t(nl) * p.nch, 1u);
     for (int lr = 0; lr < nl; ++lr) {
@@ -404,6 +415,7 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.outs = p.d_outs;
   k.prog = p.d_prog;
   k.window = p.window;
+  k.l2hint = p.l2hint ? 1 : 0;
   k.nwin = p.d_nwin;
   k.epochs = p.d_epochs;
   k.errinfo = p.d_err;
@@ -743,7 +755,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";
