@@ -292,17 +292,29 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     }
   p.prog[size_t(P) * p.kc] = uint32_t(p.ops.size());
 
-  // Window-major execution (simple protocol, every op 16-byte aligned, some
-  // op reads a receipt -- a relay or a reduction): a CTA moves one byte
-  // window of each op, in program order, before the next window, so relayed
-  // and reduced receipts are read back while they are still in L2.  The
-  // window is one tile when a CTA has several ops per step (the other ops of
-  // the step cover the hop latency), up to 4 tiles when it has one (a ring);
-  // measured on B200 (tools/gpu_runs/window_round1r.sh).  Schedules that
-  // never re-read a receipt (one-shot, direct alltoall) stay op-major: the
-  // per-window descriptor reloads would only cost.  SCCL_WINDOW=<bytes>
-  // overrides (0 = op-major).
+  // Window-major execution and L2 eviction hints, for launches that stream
+  // well past the 126 MB L2 (> 1 GB of program traffic; below that the data
+  // stays L2-resident anyway and both only add overhead -- measured, AR at
+  // 16 MiB/rank: 3-5 % slower with them).
+  //  * window-major (simple protocol, every op 16-byte aligned, some op
+  //    re-reads a receipt -- a relay or a reduction): a CTA moves one byte
+  //    window of each op, in program order, before the next window, so
+  //    relayed and reduced receipts are read back while they are still in
+  //    L2.  One tile when a CTA has several ops per step (the other ops of the
+  //    step cover the hop latency), up to 4 tiles when it has one (a ring);
+  //    measured on B200 (tools/gpu_runs/window_round1r.sh, window2_round1s.sh).
+  //    Schedules that never re-read a receipt (one-shot, direct alltoall)
+  //    stay op-major: the per-window descriptor reloads would only cost.
+  //  * hints: receipts a later op re-reads are stored evict-last, single-use
+  //    loads and stores evict-first (tools/gpu_runs/l2hint_round1t.sh).
+  // SCCL_WINDOW=<bytes> (0 = op-major) and SCCL_L2HINT=0/1 override.
   {
+    double launch_bytes = 0;
+    for (auto& rp : p.pg.ranks)
+      for (auto& op : rp.ops)
+        if (op.kind != OP_WAIT) launch_bytes += double(op.len) * double(op.ins.size() + op.outs.size());
+    if (!loopback) launch_bytes *= 1.0 / P;  // this rank's share
+    const bool streams = !p.ll && launch_bytes > 1e9;
     bool all_vec = true, rereads = false;
     size_t nops0 = 0;
     for (size_t i = 0; i < p.ops.size(); ++i) {
@@ -316,21 +328,12 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     for (auto* ph : p.sched.flat()) steps += ph->S;
     const double ops_per_step = double(nops0) / double(std::max(1, p.kc * steps));
     const int m = std::max(1, std::min(4, int(std::ceil(4.0 / std::max(ops_per_step, 1e-9)))));
-    p.window = (!p.ll && all_vec && rereads) ? uint32_t(p.tile) * uint32_t(m) : 0u;
+    p.window = (streams && all_vec && rereads) ? uint32_t(p.tile) * uint32_t(m) : 0u;
     if (const char* env = std::getenv("SCCL_WINDOW")) {
       const long w = std::atol(env);
       p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
     }
-    // L2 eviction hints (keep receipts a later op re-reads, evict single-use
-    // data first) only pay when a launch streams well past the 126 MB L2;
-    // below that everything stays resident and the hints only evict what
-    // the next launch or the caller would reuse.
-    double launch_bytes = 0;
-    for (auto& rp : p.pg.ranks)
-      for (auto& op : rp.ops)
-        if (op.kind != OP_WAIT) launch_bytes += double(op.len) * double(op.ins.size() + op.outs.size());
-    if (!loopback) launch_bytes *= 1.0 / P;  // this rank's share
-    p.l2hint = !p.ll && launch_bytes > 512e6;
+    p.l2hint = streams;
     if (const char* env = std::getenv("SCCL_L2HINT")) p.l2hint = std::atoi(env) != 0;
     const int nl = loopback ? P : 1;
     p.nwin.assign(size_t(nl) * p.nch, 1u);
