@@ -252,6 +252,22 @@ def test_concurrent_distinct_plans():
         plan.close()
 
 
+@pytest.mark.parametrize("window", ["4096", "65536"])
+@pytest.mark.parametrize("name,nbytes", [("ag_777", 1 << 20), ("ar_56_14_14", 1 << 20), ("ag_b7_ring8", 1 << 20),
+                                         ("ar_822", 1 << 20), ("ar_ring", 2 << 20), ("rs_ring8", 1 << 20),
+                                         ("ar_dgx1", 1 << 20), ("bcast_chain", 1 << 20), ("a2a_k2", 1 << 20)])
+def test_window_major_forced(monkeypatch, window, name, nbytes):
+    """Window-major execution and the L2 hints (on by default only for
+    launches over 1 GB) forced at small sizes, both counter-release modes
+    exercised through the tile counts: bit-exact."""
+    monkeypatch.setenv("SCCL_WINDOW", window)
+    monkeypatch.setenv("SCCL_L2HINT", "1")
+    js = SCHED[name]
+    kind = json.loads(js)["collective"]
+    dt = O.BF16 if kind in ("allreduce", "reducescatter", "reduce") else O.U8
+    run_gpu(js, nbytes, dt, protocol="simple", repeats=2)
+
+
 def test_baseline_full_sizes():
     """BASELINE configs 2-4 at their largest sizes, through size-independent
     properties: AG (7,7,7) at 1 GiB per rank (every output == the
