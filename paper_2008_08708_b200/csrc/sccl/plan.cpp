@@ -196,6 +196,32 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   } else {
     kb = int(std::max<int64_t>(1, std::min<int64_t>(cap, (maxlen + part - 1) / part)));
     kc = req.chunk_groups > 0 ? req.chunk_groups : std::max(1, std::min(G, cap / kb));
+    // A streaming, non-combining relay schedule with many ops per step (the
+    // (7,7,7) allgather: 7) splits its chunks over two groups, so a CTA's
+    // window holds fewer ops per step and a relayed receipt is forwarded
+    // sooner after it lands (window-major, below).  Measured at 128 MiB per
+    // rank: (7,7,7) 1979 -> 1869 us (64 MiB 993 -> 975, 512 MiB 8048 -> 7595,
+    // 16 MiB 254 -> 289, hence the 4 GB floor); combining schedules lost.
+    if (req.chunk_groups <= 0 && kc == 1 && kb >= 4 && !ll) {
+      double bytes_moved = 0;
+      bool rereads = false, reduces = false;
+      size_t nops0 = 0;
+      for (size_t r = 0; r < p.pg.ranks.size(); ++r)
+        for (auto& op : p.pg.ranks[r].ops) {
+          if (op.kind == OP_WAIT) continue;
+          bytes_moved += double(op.len) * double(op.ins.size() + op.outs.size());
+          reduces |= op.kind == OP_REDUCE;
+          for (auto& in : op.ins) rereads |= in.flag >= 0;
+          if (r == 0) ++nops0;
+        }
+      if (!loopback) bytes_moved /= double(p.sched.P);
+      int steps = 0;
+      for (auto* ph : p.sched.flat()) steps += ph->S;
+      if (bytes_moved > 4e9 && rereads && !reduces && double(nops0) >= 4.0 * steps) {  // (16 MiB/rank: slower)
+        kc = 2;
+        kb /= 2;
+      }
+    }
   }
   if (kc < 1 || kb < 1) throw invalid_argument_error("channels must be positive");
   p.kc = kc;
