@@ -10,15 +10,22 @@
 //    sub-range of every chunk; the CTA runs its rank's whole op list on that
 //    sub-range, so program order replaces intra-rank synchronisation and
 //    only cross-rank receipts carry flags;
-//  * warp-specialised TMA pipeline over a ring of NSTAGE shared-memory
-//    stages (mbarrier full / ready / empty per stage):
-//      warp 0  producer  waits the receipt counters a tile needs, then
-//                        cp.async.bulk global->smem for every input;
-//      warps 2+ compute  REDUCE ops: in-place f32-accumulate of the nin
-//                        input tiles in smem (fixed order, one rounding);
-//      warp 1  storer    cp.async.bulk smem->global to every destination
-//                        (local output and/or peer HBM), bulk groups
-//                        retired with a lag, then fence + counter release;
+//  * warp-specialised TMA pipeline over a ring of shared-memory stages
+//    (mbarriers full / fullr / ready / empty per stage):
+//      warp 0     producer  waits the receipt counters a tile needs, then
+//                           cp.async.bulk global->smem for every input;
+//      warps 1-3  storers   stage s belongs to warp 1 + s % 3; lane o
+//                           issues the cp.async.bulk smem->global store to
+//                           output o (local and/or peer HBM) and retires it;
+//      warp 4     signaler  releases byte counters in tile order, one fence
+//                           per batch (or the storers do it themselves for
+//                           latency-bound plans);
+//      warps 5+   compute   REDUCE tiles: in-place f32 accumulate of the nin
+//                           input tiles in smem (fixed order, one rounding);
+//                           copy tiles go from producer to storer directly;
+//  * window-major order for launches that stream past L2: every role walks
+//    byte window w of every op before window w+1, so relayed receipts are
+//    re-read from L2 (bulk copies carry L2 eviction hints);
 //  * flags count BYTES of a (receipt, channel) sub-range that have landed:
 //    (epoch-1)*len + bytes_done.  Producer and consumer may tile the same
 //    chunk differently (copy tiles are a whole stage, reduce tiles a stage
