@@ -1,0 +1,100 @@
+"""Host-side plan policies (no GPU): protocol choice, counter-release mode,
+window-major execution, L2 hints and chunk-group split, read from the plan
+summary of host-only plans (device=-1).  The thresholds are the measured
+ones documented in DESIGN.md section 4."""
+import pytest
+
+from paper_2008_08708_b200 import sccl
+from paper_2008_08708_b200 import schedules as S
+
+P = 8
+AG = S.hamiltonian_allgather(P)
+SCHED = {
+    "ag777": (S.to_json(AG), sccl.U8),
+    "ring": (S.to_json(S.ring_allgather(P)), sccl.U8),
+    "ag111": (S.to_json(S.one_shot_allgather(P)), sccl.U8),
+    "a2a": (S.to_json(S.direct_alltoall(P)), sccl.U8),
+    "ar822": (S.allreduce_from(S.one_shot_allgather(P)), sccl.BF16),
+    "ar56": (S.allreduce_from(AG), sccl.BF16),
+}
+
+
+def info(name, nbytes, **kw):
+    js, dt = SCHED[name]
+    plan = sccl.LoopbackPlan(js, nbytes, dt, device=-1, **kw)
+    try:
+        return plan.info()
+    finally:
+        plan.close()
+
+
+@pytest.mark.parametrize("name", list(SCHED))
+def test_small_is_ll_large_is_simple(name):
+    assert info(name, 1024)["protocol"] == "ll"
+    assert info(name, 64 << 20)["protocol"] == "simple"
+
+
+def test_window_major_only_for_streaming_relay_schedules():
+    # relays / reductions re-read receipts: window-major above 1 GB per launch
+    for name in ("ag777", "ring", "ar56", "ar822"):
+        assert info(name, 128 << 20, protocol="simple")["window"] > 0, name
+        assert info(name, 4 << 20, protocol="simple")["window"] == 0, name
+    # nothing is re-read: op-major at any size
+    for name in ("ag111", "a2a"):
+        assert info(name, 128 << 20, protocol="simple")["window"] == 0, name
+
+
+def test_window_size_follows_ops_per_step():
+    ring = info("ring", 128 << 20, protocol="simple")  # one op per step: 4 tiles
+    assert ring["window"] == 4 * ring["tile_bytes"]
+    ar56 = info("ar56", 128 << 20, protocol="simple")  # seven ops per step: 1 tile
+    assert ar56["window"] == ar56["tile_bytes"]
+
+
+def test_chunk_group_split_for_big_copy_relays():
+    big = info("ag777", 128 << 20, protocol="simple")
+    assert big["chunk_groups"] == 2 and big["window"] == 2 * big["tile_bytes"]
+    assert info("ag777", 16 << 20, protocol="simple")["chunk_groups"] == 1  # below 4 GB of traffic: no split
+    assert info("ar56", 128 << 20, protocol="simple")["chunk_groups"] == 1  # combining: no split
+
+
+def test_l2_hints_above_one_gigabyte():
+    assert info("ag777", 128 << 20, protocol="simple")["l2hint"] == 1
+    assert info("a2a", 128 << 20, protocol="simple")["l2hint"] == 1
+    assert info("ar822", 16 << 20, protocol="simple")["l2hint"] == 0
+    assert info("ag777", 1 << 20, protocol="simple")["l2hint"] == 0
+
+
+def test_counter_release_mode():
+    assert info("ring", 1 << 20, protocol="simple")["selfpub"] == 1   # <= 16 tiles per CTA
+    assert info("ag777", 128 << 20, protocol="simple")["selfpub"] == 0
+
+
+def test_env_overrides(monkeypatch):
+    monkeypatch.setenv("SCCL_WINDOW", "0")
+    monkeypatch.setenv("SCCL_L2HINT", "0")
+    monkeypatch.setenv("SCCL_SELFPUB", "1")
+    i = info("ag777", 128 << 20, protocol="simple")
+    assert i["window"] == 0 and i["l2hint"] == 0 and i["selfpub"] == 1
+    monkeypatch.setenv("SCCL_WINDOW", "4096")
+    assert info("ag111", 1 << 20, protocol="simple")["window"] == 4096
+
+
+def test_multiprocess_plans_use_the_sys_scope_model():
+    """One rank per GPU signals at system scope: the bulk step is dearer, so
+    the LL protocol is chosen up to larger sizes than in loopback."""
+    js, dt = SCHED["ring"]
+    sizes = [1 << k for k in range(12, 25)]
+
+    def last_ll(make):
+        best = 0
+        for sz in sizes:
+            plan = make(sz)
+            if plan.info()["protocol"] == "ll":
+                best = sz
+            plan.close()
+        return best
+
+    loop = last_ll(lambda sz: sccl.LoopbackPlan(js, sz, dt, device=-1))
+    multi = last_ll(lambda sz: sccl.Plan(js, 0, P, sz, dt, device=-1))
+    assert multi >= loop > 0
