@@ -54,7 +54,7 @@ constexpr int NPART = NT - 32;       // threads of the unaligned path (all but t
 constexpr int SIGQ = 64;             // tile completion ring (storers -> signaler), indexed by tile number
 constexpr int NSTAGE = kMaxStages;   // barrier sets; stages in use = KParams::nstage (a multiple of NSW)
 constexpr int SIGWIN = 8;            // ops the signaler keeps prepared ahead of their completion
-constexpr size_t SMEM_HDR = 4096;    // mbarriers, completion ring, signaler op window, ahead of the stages
+constexpr size_t SMEM_HDR = kSmemHdr;  // mbarriers, completion ring, signaler op window, discard records
 __host__ __device__ constexpr size_t smem_bytes(int tile, int nstage) { return SMEM_HDR + size_t(nstage) * tile; }
 struct DPart {
   int64_t off, len;
@@ -123,6 +123,15 @@ __device__ __forceinline__ void bulk_store_hint(void* dst, const void* src_smem,
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
                "r"(smem_u32(src_smem)), "r"(bytes), "l"(pol)
                : "memory");
+}
+// Drop the fully covered 128-byte L2 lines of [p, p + n) without writing
+// them back (discard.global.L2): for receipt slots in scratch that have been
+// consumed -- their bytes are dead until the next launch rewrites them.
+// (the 32 lanes of a warp split the lines)
+__device__ __forceinline__ void l2_discard_warp(const char* p, uint32_t n, int lane) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p), e = (a + n) & ~uintptr_t(127);
+  for (uintptr_t l = ((a + 127) & ~uintptr_t(127)) + uintptr_t(lane) * 128; l < e; l += 32 * 128)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
@@ -400,6 +409,11 @@ struct Smem {
   // counts only the uses that touch it, so no role can alias a phase.
   uint64_t full[NSTAGE], fullr[NSTAGE], ready[NSTAGE], empty[NSTAGE];
   SigOp win[SIGWIN];     // signaler's op window (ring)
+  // reduce tile in stage s: input k's global range if it is a scratch receipt
+  // read for the last time (producer lane k writes it with the load; the
+  // compute warps drop those L2 lines after reducing: dead data, no write-back)
+  const char* dsc[NSTAGE][32];
+  uint32_t dsn[NSTAGE];
   uint32_t done[SIGQ];   // it + 1 once tile `it`'s writes have landed (storer release, signaler acquire)
   uint32_t published;    // tiles < published are complete and their counters released (in tile order)
   uint32_t entry_mask;   // peers whose entry handshake this CTA has seen
@@ -454,6 +468,10 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       mbar_init(&S.empty[s], 1);
     }
     S.published = S.trace_n = 0;
+    for (int s = 0; s < NSTAGE; ++s) {
+      S.dsn[s] = 0;
+      for (int k = 0; k < 32; ++k) S.dsc[s][k] = nullptr;
+    }
     S.entry_mask = 1u << rank;
     s_e = p.epochs[blockIdx.x] + 1;
     s_nwin = p.nwin ? p.nwin[blockIdx.x] : 1u;
@@ -567,10 +585,12 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         uint64_t ready = 0;  // lane k tracks input k's counter (k < 32)
         const char* src = nullptr;
         int32_t flag = -1;
+        bool dead_after = false;  // a scratch receipt: consumed by this read
         if (lane < op.nin) {
           const DevIn in = p.ins[op.in_begin + lane];
           src = p.base[in.rank][in.space] + in.off + q.off;
           flag = in.flag;
+          dead_after = p.discard && in.dead_after;
         }
         if (op.raw && lane == 0)  // input written by an earlier tile of this CTA
           while (ld_acquire_cta(&S.published) < it) __nanosleep(32);
@@ -588,10 +608,13 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           __syncwarp();
           if (lane == 0) trace_ev(p, &S.trace_n, TR_FLAG, oi, t);
           uint64_t* const fb = op.kind == 1 ? &S.fullr[s] : &S.full[s];
-          if (lane == 0) {
-            mbar_wait_wd(&S.empty[s], ph ^ 1, p, rank, ch, int(oi - ob));
-            mbar_arrive_tx(fb, nv * op.nin);
+          if (lane == 0) mbar_wait_wd(&S.empty[s], ph ^ 1, p, rank, ch, int(oi - ob));
+          __syncwarp();
+          if (p.discard && op.kind == 1) {  // dead scratch receipts of this reduce tile
+            S.dsc[s][lane] = (dead_after && nv) ? src + lo : nullptr;
+            if (lane == 0) S.dsn[s] = nv;
           }
+          if (lane == 0) mbar_arrive_tx(fb, nv * op.nin);
           __syncwarp();
           if (lane < op.nin && nv) {
             fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
@@ -616,6 +639,11 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
               for (int k = 1; k < op.nin; ++k)
                 acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T)[v]);
               b0[v] = acc.out();
+            }
+            if (p.discard) {  // dead scratch receipts of this tile: drop their L2 lines (no write-back)
+              const uint32_t dn = S.dsn[s];
+              for (int k = warp - CW0; k < op.nin; k += NCW)
+                if (const char* d = S.dsc[s][k]) l2_discard_warp(d, dn, lane);
             }
             fence_proxy_async_smem();
             __syncwarp();

@@ -15,6 +15,7 @@ constexpr int kMaxTile = 65536; // one TMA pipeline stage (bytes)
 constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
 constexpr int kStageBudget = 196608;  // bytes of stages per CTA (nstage * tile)
 constexpr int kThreads = 352;   // producer, kStorerWarps storer warps, signaler + 6 compute warps
+constexpr int kSmemHdr = 8192;  // simple kernel: shared-memory header (barriers, rings, signaler window) ahead of the stages
 constexpr int kStorerWarps = 3; // simple protocol: stage s is stored by warp 1 + s % 3 (nstage % 3 == 0)
 constexpr int kLLThreads = 256; // LL kernel
 constexpr int64_t kLLPart = 4096;       // LL: bytes of a chunk one CTA owns
@@ -24,7 +25,9 @@ struct DevIn {
   uint64_t len;   // chunk length (used by WAIT ops; equal to op len otherwise)
   int32_t flag;   // receipt slot at the executing rank, -1 = none
   uint32_t chunk; // chunk id (WAIT ops filter by chunk group)
-  uint8_t rank, space, pad0, pad1;
+  uint8_t rank, space;
+  uint8_t dead_after;  // a scratch receipt this op is the only reader of (its bytes are dead once read)
+  uint8_t pad1;
   uint32_t pad2;
 };
 
@@ -70,6 +73,7 @@ struct KParams {
   uint32_t window;       // simple protocol: bytes of an op a CTA moves before the next op (0 = whole op)
   const uint32_t* nwin;  // [launched CTAs] windows of each CTA's program
   int l2hint;            // 1: L2 eviction hints on bulk copies (launch traffic >> L2)
+  int discard;           // 1: drop consumed scratch receipts of reduce tiles from L2 (no write-back)
 };
 
 // debug trace events of the simple-protocol kernel (record = {globaltimer ns,

@@ -182,7 +182,7 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   const int nstage = budget / tile >= 2 * kStorerWarps ? 2 * kStorerWarps : kStorerWarps;
   int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, ll ? 0 : tile, nstage)
             : ll ? 2048 / kLLThreads
-                 : std::max(1, std::min(2, int((227 << 10) / (nstage * tile + 2048))));
+                 : std::max(1, std::min(2, int((227 << 10) / (nstage * tile + kSmemHdr))));
   const int resident = std::max(1, req.sms * std::max(1, bps));
   const int cap = loopback ? std::max(1, resident / p.sched.P) : 32;
   // bytes of a chunk one CTA should own: one stage for the bulk protocol
@@ -264,6 +264,16 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   // (ops of different chunks never depend on each other within a rank);
   // end-of-program waits are split by chunk group the same way
   p.prog.assign(size_t(P) * p.kc + 1, 0);
+  // readers per (rank, receipt slot): a scratch receipt with one reader is
+  // dead once that reader has loaded it (the kernel may drop it from L2)
+  std::vector<std::vector<int>> readers(P);
+  for (int r = 0; r < P; ++r) {
+    readers[r].assign(size_t(std::max(1, p.pg.ranks[r].nslots)), 0);
+    for (const Op& op : p.pg.ranks[r].ops)
+      if (op.kind != OP_WAIT)
+        for (auto& in : op.ins)
+          if (in.flag >= 0 && in.flag < int(readers[r].size())) ++readers[r][size_t(in.flag)];
+  }
   auto encode = [&](int r, const Op& op, const std::vector<OpIn>& ins) {
     if (op.kind != OP_WAIT && (ins.size() > size_t(kMaxOpIn) || op.outs.size() > size_t(kMaxOpOut)))
       throw invalid_argument_error("op fan-in/fan-out exceeds executor limits (32)");
@@ -285,6 +295,8 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
       x.chunk = uint32_t(std::max(0, in.chunk));
       x.rank = uint8_t(in.loc.rank);
       x.space = uint8_t(in.loc.space);
+      x.dead_after = op.kind != OP_WAIT && in.flag >= 0 && in.loc.space == SP_SCRATCH &&
+                     in.flag < int(readers[r].size()) && readers[r][size_t(in.flag)] == 1;
       vec &= in.loc.off % 16 == 0;
       if (in.flag < 0 && in.loc.space != SP_SEND) d.raw = 1;
       p.ins.push_back(x);
@@ -361,6 +373,16 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
     }
     p.l2hint = streams;
     if (const char* env = std::getenv("SCCL_L2HINT")) p.l2hint = std::atoi(env) != 0;
+    // Wide reductions (fan-in >= 4, e.g. the one-shot allreduce) also drop
+    // their consumed scratch receipts from L2 (discard.global.L2: no
+    // write-back of dead bytes): (8,2,2) at 64/128 MiB 321 -> 296 /
+    // 614 -> 560 us.  Chains of 2-input reduces lost 10-20 % to the discard
+    // instructions, so they keep the write-back.  SCCL_DISCARD=0/1 overrides.
+    int fanin = 1;
+    for (auto& d : p.ops)
+      if (d.kind == OP_REDUCE) fanin = std::max(fanin, int(d.nin));
+    p.discard = p.l2hint && fanin >= 4;
+    if (const char* env = std::getenv("SCCL_DISCARD")) p.discard = std::atoi(env) != 0 && !p.ll;
     const int nl = loopback ? P : 1;
     p.nwin.assign(size_t(nl) * p.nch, 1u);
     for (int lr = 0; lr < nl; ++lr) {
@@ -445,6 +467,7 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.prog = p.d_prog;
   k.window = p.window;
   k.l2hint = p.l2hint ? 1 : 0;
+  k.discard = p.discard ? 1 : 0;
   k.nwin = p.d_nwin;
   k.epochs = p.d_epochs;
   k.errinfo = p.d_err;
@@ -784,7 +807,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

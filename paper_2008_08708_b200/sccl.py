@@ -13,7 +13,8 @@ import os
 from typing import List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsccl_exec.so")
+# SCCL_LIB: an alternative build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("SCCL_LIB") or os.path.join(_HERE, "lib", "libsccl_exec.so")
 
 OK, INVALID_ARGUMENT, CUDA_ERROR, PEER_TIMEOUT, INTERNAL = 0, 1, 4, 5, 6
 U8, I32, F32, BF16, F16 = 0, 1, 2, 3, 4

@@ -262,6 +262,7 @@ def test_window_major_forced(monkeypatch, window, name, nbytes):
     exercised through the tile counts: bit-exact."""
     monkeypatch.setenv("SCCL_WINDOW", window)
     monkeypatch.setenv("SCCL_L2HINT", "1")
+    monkeypatch.setenv("SCCL_DISCARD", "1")  # drop consumed scratch receipts from L2
     js = SCHED[name]
     kind = json.loads(js)["collective"]
     dt = O.BF16 if kind in ("allreduce", "reducescatter", "reduce") else O.U8

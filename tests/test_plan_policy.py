@@ -65,6 +65,13 @@ def test_l2_hints_above_one_gigabyte():
     assert info("ag777", 1 << 20, protocol="simple")["l2hint"] == 0
 
 
+def test_discard_only_for_wide_streaming_reductions():
+    assert info("ar822", 128 << 20, protocol="simple")["discard"] == 1   # fan-in 8
+    assert info("ar56", 128 << 20, protocol="simple")["discard"] == 0    # 2-input reduce chain
+    assert info("ar822", 16 << 20, protocol="simple")["discard"] == 0    # fits L2
+    assert info("ag777", 128 << 20, protocol="simple")["discard"] == 0   # no reduction
+
+
 def test_counter_release_mode():
     assert info("ring", 1 << 20, protocol="simple")["selfpub"] == 1   # <= 16 tiles per CTA
     assert info("ag777", 128 << 20, protocol="simple")["selfpub"] == 0
