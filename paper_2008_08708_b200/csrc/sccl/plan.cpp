@@ -160,9 +160,19 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   // stage (= copy tile) size and pipeline depth, within kStageBudget bytes:
   // bulk streaming 6 x 32 KiB; wide reductions 3 x 64 KiB (reduce tiles are
   // stage / fan-in); small chunks: the smallest power of two that holds one
+  // Wide reductions take 3 x 64 KiB stages at 1 CTA/SM (8 KiB per input at
+  // fan-in 8) while the data fits L2; launches streaming past it (> 1 GB)
+  // run window-major with receipt discards and do better at 2 CTAs/SM with
+  // 3 x 32 KiB (AR (8,2,2) 64 MiB: 298 -> 280 us, 256 MiB 1109 -> 1081 us).
+  double prog_bytes = 0;
+  for (auto& rp : p.pg.ranks)
+    for (auto& op : rp.ops)
+      if (op.kind != OP_WAIT) prog_bytes += double(op.len) * double(op.ins.size() + op.outs.size());
+  if (!loopback) prog_bytes /= double(p.sched.P);
+  const bool wide = max_fanin >= 4 && !(prog_bytes > 1e9 && !ll);
   int tile = req.tile;
   if (tile <= 0) {
-    tile = max_fanin >= 4 ? kMaxTile : 32768;
+    tile = wide ? kMaxTile : 32768;
     if (maxlen < tile) {
       tile = 1024;
       while (tile < maxlen) tile *= 2;
@@ -174,7 +184,7 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   // (bytes) trades depth for CTAs per SM (96 KiB -> 2 CTAs/SM)
   // streaming copies / 2-input reductions: 3 x 32 KiB at 2 CTAs per SM;
   // wide reductions: 3 x 64 KiB at 1 CTA per SM (tools/tune.py sweep)
-  int budget = max_fanin >= 4 ? kStageBudget : kStageBudget / 2;
+  int budget = wide ? kStageBudget : kStageBudget / 2;
   if (const char* env = std::getenv("SCCL_STAGE_BUDGET")) budget = std::max(2 * 256, std::min(kStageBudget, std::atoi(env)));
   if (req.stage_budget > 0) budget = std::min(kStageBudget, req.stage_budget);
   // stages come in multiples of the storer-warp count (each storer warp owns
