@@ -102,74 +102,72 @@ struct IpcBlob {
 
 namespace sccl {
 
-void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks, int64_t bytes, int dtype,
-                     int redop, int device, const ChannelRequest& req, int64_t timeout_ms, bool loopback) {
-  if (redop != SCCL_SUM) throw invalid_argument_error("only SCCL_SUM is supported");
-  const int es = esize_of(dtype);
-  p.sched = parse_schedule(json);
-  if (p.sched.P > kMaxRanks) throw invalid_argument_error("P exceeds the executor's 16-rank pointer table");
-  if (!loopback) {
-    if (nranks != p.sched.P) throw invalid_argument_error("nranks != schedule P");
-    if (rank < 0 || rank >= nranks) throw invalid_argument_error("rank out of range");
-  }
-  // protocol: LL (flag-in-data, no fences, 2x bytes) for latency-bound
-  // sizes, pipelined TMA bulk copies with counter flags otherwise
-  int64_t maxlen = 0;
-  {
-    const auto phases = p.sched.flat();
-    for (auto& g : chunk_geometry(p.sched.kind, p.sched.P, phases.back()->G, bytes)) maxlen = std::max(maxlen, g.len);
-  }
-  // protocol choice (auto): lower both ways and take the smaller predicted
-  // time t = c + alpha*S + beta*MB, where S = schedule steps and MB = bytes
-  // the lowered program reads + writes.  Constants are a relative-error
-  // least-squares fit to the B200 loopback crossover sweep
-  // (tools/gpu_runs/proto_round1i.sh: 7 schedules x 16 KiB-16 MiB x both
-  // protocols; mean regret vs the per-point best 1.9 %).
-  if (req.protocol < 0 || req.protocol > 2) throw invalid_argument_error("protocol must be 0 (auto), 1 (simple), 2 (ll)");
-  bool ll = req.protocol == 2;
-  if (req.protocol == 0) {
-    int steps = 0;
-    for (auto* ph : p.sched.flat()) steps += ph->S;
-    const Program a = lower(p.sched, bytes, es, true), b = lower(p.sched, bytes, es, false);
-    const bool sys = !loopback || loopback_sys();
-    ll = predict_us(a, steps, true, sys) < predict_us(b, steps, false, sys);
-    p.pg = ll ? a : b;
-  } else {
-    p.pg = lower(p.sched, bytes, es, ll);
-  }
-  p.ll = ll;
-  p.rank = loopback ? 0 : rank;
-  p.nranks = p.sched.P;
-  p.loopback = loopback;
-  p.dtype = dtype;
-  p.redop = redop;
-  p.device = device;
-  p.host_only = device < 0;
-  p.timeout_ns = timeout_ms < 0 ? 0 : (timeout_ms == 0 ? 10000LL : timeout_ms) * 1000000LL;
+namespace {
 
-  // ---- channels (CTAs per rank) and tile (= one TMA pipeline stage) ----
-  // channel j = (chunk group j % kc, byte part j / kc).  Large chunks are cut
-  // into byte parts so every SM streams; small chunks are spread over chunk
-  // groups so independent chunks travel in parallel instead of queueing
-  // behind each other in one CTA (latency).
-  const int G = p.pg.G;
-  int max_fanin = 1;
-  for (auto& rp : p.pg.ranks)
-    for (auto& op : rp.ops)
-      if (op.kind == OP_REDUCE) max_fanin = std::max(max_fanin, int(op.ins.size()));
-  // stage (= copy tile) size and pipeline depth, within kStageBudget bytes:
-  // bulk streaming 6 x 32 KiB; wide reductions 3 x 64 KiB (reduce tiles are
-  // stage / fan-in); small chunks: the smallest power of two that holds one
-  // Wide reductions take 3 x 64 KiB stages at 1 CTA/SM (8 KiB per input at
-  // fan-in 8) while the data fits L2; launches streaming past it (> 1 GB)
-  // run window-major with receipt discards and do better at 2 CTAs/SM with
-  // 3 x 32 KiB (AR (8,2,2) 64 MiB: 298 -> 280 us, 256 MiB 1109 -> 1081 us).
-  double prog_bytes = 0;
-  for (auto& rp : p.pg.ranks)
-    for (auto& op : rp.ops)
-      if (op.kind != OP_WAIT) prog_bytes += double(op.len) * double(op.ins.size() + op.outs.size());
-  if (!loopback) prog_bytes /= double(p.sched.P);
-  const bool wide = max_fanin >= 4 && !(prog_bytes > 1e9 && !ll);
+// Facts about a lowered program the plan policies below are decided from.
+struct ProgramStats {
+  int steps = 0;            // schedule steps, all phases
+  int max_fanin = 1;        // widest REDUCE
+  double bytes = 0;         // reads + writes of the lowered ops (this rank's share when multi-process)
+  bool rereads = false;     // some op reads a receipt (a relay or a reduction)
+  bool reduces = false;
+  size_t nops_rank0 = 0;    // rank 0's non-WAIT ops
+};
+
+ProgramStats program_stats(const Schedule& sched, const Program& pg, bool loopback) {
+  ProgramStats st;
+  for (auto* ph : sched.flat()) st.steps += ph->S;
+  for (size_t r = 0; r < pg.ranks.size(); ++r)
+    for (auto& op : pg.ranks[r].ops) {
+      if (op.kind == OP_WAIT) continue;
+      st.bytes += double(op.len) * double(op.ins.size() + op.outs.size());
+      if (op.kind == OP_REDUCE) {
+        st.reduces = true;
+        st.max_fanin = std::max(st.max_fanin, int(op.ins.size()));
+      }
+      for (auto& in : op.ins) st.rereads |= in.flag >= 0;
+      if (r == 0) ++st.nops_rank0;
+    }
+  if (!loopback) st.bytes /= double(sched.P);
+  return st;
+}
+
+// A launch streams when its program moves > 1 GB: past the 126 MB L2, the
+// window-major order, L2 hints, receipt discards and the stage choice for
+// streaming reductions pay; below it the data stays L2-resident.
+constexpr double kStreamBytes = 1e9;
+
+// Protocol (auto): lower both ways and take the smaller predicted time
+// t = c + alpha*S + beta*MB (S = schedule steps, MB = bytes the lowered
+// program reads + writes).  Constants: a relative-error least-squares fit
+// to the B200 loopback crossover sweep (tools/gpu_runs/proto_round1i.sh:
+// 7 schedules x 16 KiB-16 MiB x both protocols; mean regret vs the
+// per-point best 1.9 %); system scope uses its own fit.
+bool choose_ll(sccl_plan& p, int64_t bytes, int es, int protocol, bool loopback) {
+  if (protocol < 0 || protocol > 2) throw invalid_argument_error("protocol must be 0 (auto), 1 (simple), 2 (ll)");
+  if (protocol != 0) {
+    p.pg = lower(p.sched, bytes, es, protocol == 2);
+    return protocol == 2;
+  }
+  int steps = 0;
+  for (auto* ph : p.sched.flat()) steps += ph->S;
+  Program a = lower(p.sched, bytes, es, true), b = lower(p.sched, bytes, es, false);
+  const bool sys = !loopback || loopback_sys();
+  const bool ll = predict_us(a, steps, true, sys) < predict_us(b, steps, false, sys);
+  p.pg = ll ? std::move(a) : std::move(b);
+  return ll;
+}
+
+// Stage (= copy tile) size and pipeline depth.  Streaming copies and
+// 2-input reductions: 3 x 32 KiB at 2 CTAs/SM.  Wide reductions (fan-in
+// >= 4) that fit L2: 3 x 64 KiB at 1 CTA/SM (8 KiB per input at fan-in 8);
+// streaming ones run window-major with receipt discards and do better at
+// 2 CTAs/SM with 3 x 32 KiB (AR (8,2,2) 64 MiB 298 -> 280 us, 256 MiB
+// 1109 -> 1081 us).  Small chunks: the smallest power of two that holds
+// one.  Stages come in multiples of the storer-warp count (each storer warp
+// owns the stages s with s % kStorerWarps == its index): 3 or 6.
+void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const ChannelRequest& req) {
+  const bool wide = st.max_fanin >= 4 && !(st.bytes > kStreamBytes && !p.ll);
   int tile = req.tile;
   if (tile <= 0) {
     tile = wide ? kMaxTile : 32768;
@@ -180,102 +178,85 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   }
   if (tile % 16 || tile > kMaxTile || tile < 256)
     throw invalid_argument_error("tile_bytes must be a multiple of 16 in [256, 65536]");
-  // stage budget: 192 KiB = 1 CTA/SM with a deep ring; SCCL_STAGE_BUDGET
-  // (bytes) trades depth for CTAs per SM (96 KiB -> 2 CTAs/SM)
-  // streaming copies / 2-input reductions: 3 x 32 KiB at 2 CTAs per SM;
-  // wide reductions: 3 x 64 KiB at 1 CTA per SM (tools/tune.py sweep)
+  // SCCL_STAGE_BUDGET (bytes of stages per CTA) trades depth for CTAs per SM
   int budget = wide ? kStageBudget : kStageBudget / 2;
   if (const char* env = std::getenv("SCCL_STAGE_BUDGET")) budget = std::max(2 * 256, std::min(kStageBudget, std::atoi(env)));
   if (req.stage_budget > 0) budget = std::min(kStageBudget, req.stage_budget);
-  // stages come in multiples of the storer-warp count (each storer warp owns
-  // the stages s with s % kStorerWarps == its index): 3 or 6
-  const int nstage = budget / tile >= 2 * kStorerWarps ? 2 * kStorerWarps : kStorerWarps;
-  int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, ll ? 0 : tile, nstage)
-            : ll ? 2048 / kLLThreads
-                 : std::max(1, std::min(2, int((227 << 10) / (nstage * tile + kSmemHdr))));
+  p.tile = tile;
+  p.nstage = budget / tile >= 2 * kStorerWarps ? 2 * kStorerWarps : kStorerWarps;
+}
+
+// Channels: channel j = (chunk group j % kc, byte part j / kc).  Large
+// chunks are cut into byte parts so every SM streams (one stage per part:
+// fewer, longer parts lost more to idle SMs than they gained in
+// pipelining); small chunks are spread over chunk groups so independent
+// chunks travel in parallel instead of queueing in one CTA.  A streaming,
+// copy-only relay schedule with >= 4 ops per step (the (7,7,7) allgather:
+// 7) splits into two chunk groups, so a CTA's window holds fewer ops per
+// step and a relayed receipt is forwarded sooner after it lands: (7,7,7)
+// at 128 MiB/rank 1979 -> 1869 us (64 MiB 993 -> 975, 512 MiB 8048 -> 7595;
+// 16 MiB 254 -> 289, hence its 4 GB floor); combining schedules lost.
+void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const ChannelRequest& req, bool loopback) {
+  const int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, p.ll ? 0 : p.tile, p.nstage)
+                  : p.ll ? 2048 / kLLThreads
+                         : std::max(1, std::min(2, int((227 << 10) / (p.nstage * p.tile + kSmemHdr))));
   const int resident = std::max(1, req.sms * std::max(1, bps));
   const int cap = loopback ? std::max(1, resident / p.sched.P) : 32;
-  // bytes of a chunk one CTA should own: one stage for the bulk protocol
-  // (measured: fewer, longer byte parts lose more to idle SMs than they
-  // gain in pipelining), small for LL (latency)
-  const int64_t part = ll ? kLLPart : tile;
+  const int64_t part = p.ll ? kLLPart : p.tile;
   int kb, kc;
   if (req.nchannels > 0) {
     kb = req.nchannels;
     kc = req.chunk_groups > 0 ? req.chunk_groups : 1;
   } else {
     kb = int(std::max<int64_t>(1, std::min<int64_t>(cap, (maxlen + part - 1) / part)));
-    kc = req.chunk_groups > 0 ? req.chunk_groups : std::max(1, std::min(G, cap / kb));
-    // A streaming, non-combining relay schedule with many ops per step (the
-    // (7,7,7) allgather: 7) splits its chunks over two groups, so a CTA's
-    // window holds fewer ops per step and a relayed receipt is forwarded
-    // sooner after it lands (window-major, below).  Measured at 128 MiB per
-    // rank: (7,7,7) 1979 -> 1869 us (64 MiB 993 -> 975, 512 MiB 8048 -> 7595,
-    // 16 MiB 254 -> 289, hence the 4 GB floor); combining schedules lost.
-    if (req.chunk_groups <= 0 && kc == 1 && kb >= 4 && !ll) {
-      double bytes_moved = 0;
-      bool rereads = false, reduces = false;
-      size_t nops0 = 0;
-      for (size_t r = 0; r < p.pg.ranks.size(); ++r)
-        for (auto& op : p.pg.ranks[r].ops) {
-          if (op.kind == OP_WAIT) continue;
-          bytes_moved += double(op.len) * double(op.ins.size() + op.outs.size());
-          reduces |= op.kind == OP_REDUCE;
-          for (auto& in : op.ins) rereads |= in.flag >= 0;
-          if (r == 0) ++nops0;
-        }
-      if (!loopback) bytes_moved /= double(p.sched.P);
-      int steps = 0;
-      for (auto* ph : p.sched.flat()) steps += ph->S;
-      if (bytes_moved > 4e9 && rereads && !reduces && double(nops0) >= 4.0 * steps) {  // (16 MiB/rank: slower)
-        kc = 2;
-        kb /= 2;
-      }
+    kc = req.chunk_groups > 0 ? req.chunk_groups : std::max(1, std::min(p.pg.G, cap / kb));
+    if (req.chunk_groups <= 0 && kc == 1 && kb >= 4 && !p.ll && st.bytes > 4 * kStreamBytes && st.rereads &&
+        !st.reduces && double(st.nops_rank0) >= 4.0 * st.steps) {
+      kc = 2;
+      kb /= 2;
     }
   }
   if (kc < 1 || kb < 1) throw invalid_argument_error("channels must be positive");
   p.kc = kc;
   p.kb = kb;
   p.nch = kc * kb;
-  p.tile = tile;
-  p.nstage = nstage;
-  // Counter release: latency-bound plans (at most 16 tiles per CTA) let
-  // each storer warp release its own tile's counters (no hand-off, ~0.3 us
-  // less per hop); longer ones keep the fence off the store path in the
-  // signaler warp, batched across ops.  Crossover from the B200 A/B sweep
-  // (tools/gpu_runs/winsig_round1h.sh: 7 schedules x 64 KiB-128 MiB).
-  {
-    int64_t max_tiles = 0;
-    for (auto& rp : p.pg.ranks)
-      for (int g = 0; g < kc; ++g) {
-        int64_t n = 0;
-        for (auto& op : rp.ops) {
-          if (op.kind == OP_WAIT || std::max(0, op.chunk) % kc != g) continue;
-          const int64_t part = split16(op.len, kb, kb - 1).len;  // the last part is the longest
-          const int64_t T = op.kind == OP_COPY ? tile : std::max<int64_t>(16, (tile / int64_t(op.ins.size())) & ~int64_t(15));
-          n += (part + T - 1) / T;
-        }
-        max_tiles = std::max(max_tiles, n);
-      }
-    // system scope (multi-process) makes the fence on the store path ~3x
-    // dearer, so only very short plans self-publish there (measured with
-    // SCCL_LOOPBACK_SYS=1, tools/gpu_runs/sys_pub_round1n.sh)
-    p.selfpub = max_tiles <= ((!loopback || loopback_sys()) ? 4 : 16);
-  }
-  if (const char* env = std::getenv("SCCL_SELFPUB")) p.selfpub = std::atoi(env) != 0;
   p.resident_cap = loopback ? resident : 0;
+}
 
-  // device encoding
+// Counter release: latency-bound plans (<= 16 tiles per CTA) let each
+// storer warp release its own tile's counters (no hand-off, ~0.3 us less
+// per hop); longer ones keep the fence off the store path in the signaler
+// warp, batched across ops (tools/gpu_runs/winsig_round1h.sh).  System scope
+// makes the fence on the store path ~3x dearer, so only very short plans
+// self-publish there (<= 4 tiles; tools/gpu_runs/sys_pub_round1n.sh).
+void choose_release(sccl_plan& p, bool loopback) {
+  int64_t max_tiles = 0;
+  for (auto& rp : p.pg.ranks)
+    for (int g = 0; g < p.kc; ++g) {
+      int64_t n = 0;
+      for (auto& op : rp.ops) {
+        if (op.kind == OP_WAIT || std::max(0, op.chunk) % p.kc != g) continue;
+        const int64_t part = split16(op.len, p.kb, p.kb - 1).len;  // the last part is the longest
+        const int64_t T = op.kind == OP_COPY ? p.tile : std::max<int64_t>(16, (p.tile / int64_t(op.ins.size())) & ~int64_t(15));
+        n += (part + T - 1) / T;
+      }
+      max_tiles = std::max(max_tiles, n);
+    }
+  p.selfpub = max_tiles <= ((!loopback || loopback_sys()) ? 4 : 16);
+  if (const char* env = std::getenv("SCCL_SELFPUB")) p.selfpub = std::atoi(env) != 0;
+}
+
+// Device encoding: one op list per (rank, chunk group) -- a CTA walks only
+// its own ops (ops of different chunks never depend on each other within a
+// rank); end-of-program waits are split by chunk group the same way.  A
+// scratch receipt with one reader is marked dead_after (the kernel may drop
+// it from L2 once that reader has loaded it).
+void encode_program(sccl_plan& p) {
   const int P = p.sched.P;
   p.ops.clear();
   p.ins.clear();
   p.outs.clear();
-  // one op list per (rank, chunk group): a CTA walks only its own ops
-  // (ops of different chunks never depend on each other within a rank);
-  // end-of-program waits are split by chunk group the same way
   p.prog.assign(size_t(P) * p.kc + 1, 0);
-  // readers per (rank, receipt slot): a scratch receipt with one reader is
-  // dead once that reader has loaded it (the kernel may drop it from L2)
   std::vector<std::vector<int>> readers(P);
   for (int r = 0; r < P; ++r) {
     readers[r].assign(size_t(std::max(1, p.pg.ranks[r].nslots)), 0);
@@ -339,83 +320,101 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
       }
     }
   p.prog[size_t(P) * p.kc] = uint32_t(p.ops.size());
+}
 
-  // Window-major execution and L2 eviction hints, for launches that stream
-  // well past the 126 MB L2 (> 1 GB of program traffic; below that the data
-  // stays L2-resident anyway and both only add overhead -- measured, AR at
-  // 16 MiB/rank: 3-5 % slower with them).
-  //  * window-major (simple protocol, every op 16-byte aligned, some op
-  //    re-reads a receipt -- a relay or a reduction): a CTA moves one byte
-  //    window of each op, in program order, before the next window, so
-  //    relayed and reduced receipts are read back while they are still in
-  //    L2.  One tile when a CTA has several ops per step (the other ops of the
-  //    step cover the hop latency), up to 4 tiles when it has one (a ring);
-  //    measured on B200 (tools/gpu_runs/window_round1r.sh, window2_round1s.sh).
-  //    Schedules that never re-read a receipt (one-shot, direct alltoall)
-  //    stay op-major: the per-window descriptor reloads would only cost.
-  //  * hints: receipts a later op re-reads are stored evict-last, single-use
-  //    loads and stores evict-first (tools/gpu_runs/l2hint_round1t.sh).
-  // SCCL_WINDOW=<bytes> (0 = op-major) and SCCL_L2HINT=0/1 override.
-  {
-    double launch_bytes = 0;
-    for (auto& rp : p.pg.ranks)
-      for (auto& op : rp.ops)
-        if (op.kind != OP_WAIT) launch_bytes += double(op.len) * double(op.ins.size() + op.outs.size());
-    if (!loopback) launch_bytes *= 1.0 / P;  // this rank's share
-    const bool streams = !p.ll && launch_bytes > 1e9;
-    bool all_vec = true, rereads = false;
-    size_t nops0 = 0;
-    for (size_t i = 0; i < p.ops.size(); ++i) {
-      const DevOp& d = p.ops[i];
-      if (d.kind == OP_WAIT) continue;
-      all_vec &= d.vec != 0;
-      for (uint32_t k = 0; k < d.nin; ++k) rereads |= p.ins[d.in_begin + k].flag >= 0;
-      if (i < p.prog[size_t(p.kc)]) ++nops0;  // rank 0's ops, all chunk groups
-    }
-    int steps = 0;
-    for (auto* ph : p.sched.flat()) steps += ph->S;
-    const double ops_per_step = double(nops0) / double(std::max(1, p.kc * steps));
-    const int m = std::max(1, std::min(4, int(std::ceil(4.0 / std::max(ops_per_step, 1e-9)))));
-    p.window = (streams && all_vec && rereads) ? uint32_t(p.tile) * uint32_t(m) : 0u;
-    if (const char* env = std::getenv("SCCL_WINDOW")) {
-      const long w = std::atol(env);
-      p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
-    }
-    p.l2hint = streams;
-    if (const char* env = std::getenv("SCCL_L2HINT")) p.l2hint = std::atoi(env) != 0;
-    // Wide reductions (fan-in >= 4, e.g. the one-shot allreduce) also drop
-    // their consumed scratch receipts from L2 (discard.global.L2: no
-    // write-back of dead bytes): (8,2,2) at 64/128 MiB 321 -> 296 /
-    // 614 -> 560 us.  Chains of 2-input reduces lost 10-20 % to the discard
-    // instructions, so they keep the write-back.  SCCL_DISCARD=0/1 overrides.
-    int fanin = 1;
-    for (auto& d : p.ops)
-      if (d.kind == OP_REDUCE) fanin = std::max(fanin, int(d.nin));
-    p.discard = p.l2hint && fanin >= 4;
-    if (const char* env = std::getenv("SCCL_DISCARD")) p.discard = std::atoi(env) != 0 && !p.ll;
-    const int nl = loopback ? P : 1;
-    p.nwin.assign(size_t(nl) * p.nch, 1u);
-    for (int lr = 0; lr < nl; ++lr) {
-      const int r = loopback ? lr : p.rank;
-      for (int ch = 0; ch < p.nch; ++ch) {
-        const int cg = ch % p.kc, cb = ch / p.kc;
-        int64_t maxq = 0;
-        for (uint32_t o = p.prog[size_t(r) * p.kc + cg]; o < p.prog[size_t(r) * p.kc + cg + 1]; ++o)
-          if (p.ops[o].kind != OP_WAIT) maxq = std::max(maxq, split16(int64_t(p.ops[o].len), p.kb, cb).len);
-        if (p.window) p.nwin[size_t(lr) * p.nch + ch] = uint32_t(std::max<int64_t>(1, (maxq + p.window - 1) / p.window));
-      }
+// Streaming policies (launches over kStreamBytes):
+//  * window-major (simple protocol, every op 16-byte aligned, some op
+//    re-reads a receipt): a CTA moves one byte window of each op, in
+//    program order, before the next window, so relayed and reduced receipts
+//    are read back while still in L2.  One tile when a CTA has several ops
+//    per step (the other ops of the step cover the hop latency), up to 4
+//    tiles when it has one (a ring) (tools/gpu_runs/window_round1r.sh,
+//    window2_round1s.sh).  Schedules that never re-read a receipt (one-shot,
+//    direct alltoall) stay op-major: the per-window descriptor reloads
+//    would only cost.  Below kStreamBytes: AR at 16 MiB/rank was 3-5 %
+//    slower with windows and hints.
+//  * L2 hints: receipts a later op re-reads are stored evict-last,
+//    single-use loads and stores evict-first (tools/gpu_runs/l2hint_round1t.sh).
+//  * discards: wide reductions (fan-in >= 4) drop consumed scratch receipts
+//    from L2 (discard.global.L2: no write-back of dead bytes): (8,2,2) at
+//    64/128 MiB 321 -> 296 / 614 -> 560 us; chains of 2-input reduces lost
+//    10-20 % to the discard instructions and keep the write-back.
+// SCCL_WINDOW=<bytes> (0 = op-major), SCCL_L2HINT and SCCL_DISCARD override.
+void choose_streaming(sccl_plan& p, const ProgramStats& st, bool loopback) {
+  const bool streams = !p.ll && st.bytes > kStreamBytes;
+  bool all_vec = true;
+  for (auto& d : p.ops) all_vec &= d.kind == OP_WAIT || d.vec;
+  const double ops_per_step = double(st.nops_rank0) / double(std::max(1, p.kc * st.steps));
+  const int m = std::max(1, std::min(4, int(std::ceil(4.0 / std::max(ops_per_step, 1e-9)))));
+  p.window = (streams && all_vec && st.rereads) ? uint32_t(p.tile) * uint32_t(m) : 0u;
+  if (const char* env = std::getenv("SCCL_WINDOW")) {
+    const long w = std::atol(env);
+    p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
+  }
+  p.l2hint = streams;
+  if (const char* env = std::getenv("SCCL_L2HINT")) p.l2hint = std::atoi(env) != 0;
+  p.discard = p.l2hint && st.max_fanin >= 4;
+  if (const char* env = std::getenv("SCCL_DISCARD")) p.discard = std::atoi(env) != 0 && !p.ll;
+  // windows of each launched CTA's program
+  const int nl = loopback ? p.sched.P : 1;
+  p.nwin.assign(size_t(nl) * p.nch, 1u);
+  if (!p.window) return;
+  for (int lr = 0; lr < nl; ++lr) {
+    const int r = loopback ? lr : p.rank;
+    for (int ch = 0; ch < p.nch; ++ch) {
+      const int cg = ch % p.kc, cb = ch / p.kc;
+      int64_t maxq = 0;
+      for (uint32_t o = p.prog[size_t(r) * p.kc + cg]; o < p.prog[size_t(r) * p.kc + cg + 1]; ++o)
+        if (p.ops[o].kind != OP_WAIT) maxq = std::max(maxq, split16(int64_t(p.ops[o].len), p.kb, cb).len);
+      p.nwin[size_t(lr) * p.nch + ch] = uint32_t(std::max<int64_t>(1, (maxq + p.window - 1) / p.window));
     }
   }
+}
 
-  // memory layout of one rank's region
+// Memory layout of one rank's region: [flags | scratch | recv (multi-process)].
+void layout_memory(sccl_plan& p, bool loopback) {
   auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
   p.entry_base = p.pg.max_slots * p.nch;
-  p.flags_bytes = up(sizeof(uint64_t) * size_t(p.entry_base + P * p.nch), 4096);
+  p.flags_bytes = up(sizeof(uint64_t) * size_t(p.entry_base + p.sched.P * p.nch), 4096);
   p.scratch_off = p.flags_bytes;
-  size_t scratch = up(size_t(p.pg.scratch_bytes), 4096);
+  const size_t scratch = up(size_t(p.pg.scratch_bytes), 4096);
   p.recv_off = p.scratch_off + scratch;
   p.region_bytes = p.recv_off + (loopback ? 0 : up(size_t(p.pg.recv_bytes), 4096));
   p.region_bytes = up(p.region_bytes, 1 << 21);
+}
+
+}  // namespace
+
+void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks, int64_t bytes, int dtype,
+                     int redop, int device, const ChannelRequest& req, int64_t timeout_ms, bool loopback) {
+  if (redop != SCCL_SUM) throw invalid_argument_error("only SCCL_SUM is supported");
+  const int es = esize_of(dtype);
+  p.sched = parse_schedule(json);
+  if (p.sched.P > kMaxRanks) throw invalid_argument_error("P exceeds the executor's 16-rank pointer table");
+  if (!loopback) {
+    if (nranks != p.sched.P) throw invalid_argument_error("nranks != schedule P");
+    if (rank < 0 || rank >= nranks) throw invalid_argument_error("rank out of range");
+  }
+  int64_t maxlen = 0;  // the largest chunk
+  for (auto& g : chunk_geometry(p.sched.kind, p.sched.P, p.sched.flat().back()->G, bytes)) maxlen = std::max(maxlen, g.len);
+
+  p.ll = choose_ll(p, bytes, es, req.protocol, loopback);
+  p.rank = loopback ? 0 : rank;
+  p.nranks = p.sched.P;
+  p.loopback = loopback;
+  p.dtype = dtype;
+  p.redop = redop;
+  p.device = device;
+  p.host_only = device < 0;
+  p.timeout_ns = timeout_ms < 0 ? 0 : (timeout_ms == 0 ? 10000LL : timeout_ms) * 1000000LL;
+
+  const ProgramStats st = program_stats(p.sched, p.pg, loopback);
+  choose_stages(p, st, maxlen, req);
+  choose_channels(p, st, maxlen, req, loopback);
+  choose_release(p, loopback);
+  encode_program(p);
+  choose_streaming(p, st, loopback);
+  layout_memory(p, loopback);
 }
 
 }  // namespace sccl
