@@ -42,8 +42,17 @@ else:  # multi-hop relays and combining trees through IPC-mapped peers
         (S.to_json(S.direct_alltoall(4)), 4096, O.U8, "ll"),
         (S.allreduce_from(S.ring_allgather(4)), 8192, O.BF16, "ll"),
         (S.to_json(S.ring_allgather(4)), 8 << 20, O.U8, "simple"),  # windowed signaler, sys scope
+        # window-major + L2 hints + receipt discards forced (sys scope)
+        ("FORCE", S.allreduce_from(S.one_shot_allgather(4)), 4 << 20, O.BF16, "simple"),
     ]
-for js, nb, dt, proto in cases:
+for case in cases:
+    forced = case[0] == "FORCE"
+    js, nb, dt, proto = case[1:] if forced else case
+    for k, v in (("SCCL_WINDOW", "65536"), ("SCCL_L2HINT", "1"), ("SCCL_DISCARD", "1")):
+        if forced:
+            os.environ[k] = v
+        else:
+            os.environ.pop(k, None)
     d = json.loads(js)
     ins = O.seeded_inputs(d["collective"], W, nb, dt, 17)
     ref = O.execute(d, ins, nb, dt)
@@ -82,4 +91,4 @@ def test_processes_one_gpu(tmp_path, world):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
     text = "".join(o for o, _ in outs)
-    assert text.count("OK") == 5 * world, text
+    assert text.count("OK") == (5 if world == 2 else 6) * world, text
