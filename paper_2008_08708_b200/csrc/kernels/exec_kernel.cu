@@ -950,17 +950,28 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
   __shared__ char* s_outp[kMaxOpOut];
   __shared__ uint8_t s_inll[kMaxOpIn], s_outll[kMaxOpOut];
   __shared__ uint32_t s_trace_n;
+  __shared__ uint32_t s_ob, s_oe;
+  __shared__ DevOp s_op[2];  // this op and the next one (prefetched while this one moves data)
+  // Prologue round trips in parallel: the epoch (thread 0) and the program
+  // range plus its first op (thread PF) -- they used to be three dependent
+  // loads after the epoch.
+  constexpr int PF = LL_NT - 32;  // the prefetching thread (not one of the descriptor threads below)
   if (tid == 0) {
     s_trace_n = 0;
     trace_ev(p, &s_trace_n, TR_START, 0, 0);
     s_e = p.epochs[blockIdx.x] + 1;
     s_entry_mask = 1u << rank;
   }
+  if (tid == PF) {
+    const uint32_t b = p.prog[rank * p.kc + cg], en = p.prog[rank * p.kc + cg + 1];
+    s_ob = b;
+    s_oe = en;
+    if (b < en) s_op[0] = p.ops[b];
+  }
   __syncthreads();
   if (tid == 0) trace_ev(p, &s_trace_n, TR_FLAG, 0, 0);  // epoch known
   const uint64_t e = s_e;
   const uint32_t ef = uint32_t(e);
-  uint64_t* const myflags = reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]);
   if (p.multiprocess)
     for (int t = tid; t < p.P; t += LL_NT)
       if (t != rank) {
@@ -968,9 +979,11 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
         st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[t][SP_FLAGS_IDX]) + p.entry_base + rank * p.nch + ch, e);
       }
 
-  const uint32_t ob = p.prog[rank * p.kc + cg], oe = p.prog[rank * p.kc + cg + 1];
+  const uint32_t ob = s_ob, oe = s_oe;
   for (uint32_t oi = ob; oi < oe; ++oi) {
-    const DevOp op = p.ops[oi];
+    __syncthreads();  // s_op[cur] (prefetched last iteration) visible; s_op[next] no longer read
+    const DevOp op = s_op[(oi - ob) & 1];
+    if (tid == PF && oi + 1 < oe) s_op[(oi + 1 - ob) & 1] = p.ops[oi + 1];
     if (op.kind == 2) {  // receipts nobody forwards: consume them
       for (int i = 0; i < op.nin; ++i) {
         const DevIn in = p.ins[op.in_begin + i];
@@ -991,12 +1004,14 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
       s_inll[tid] = in.flag >= 0;
       s_inp[tid] = p.base[in.rank][in.space] + in.off + (in.flag >= 0 ? 2 * q.off : q.off);
     }
-    if (tid < op.nout) {
-      const DevOut d = p.outs[op.out_begin + tid];
-      s_outll[tid] = d.flag >= 0;
-      s_outp[tid] = p.base[d.rank][d.space] + d.off + (d.flag >= 0 ? 2 * q.off : q.off);
+    if (tid >= 32 && tid < 32 + op.nout) {  // outputs on warp 1: loaded in parallel with the inputs
+      const int o = tid - 32;
+      const DevOut d = p.outs[op.out_begin + o];
+      s_outll[o] = d.flag >= 0;
+      s_outp[o] = p.base[d.rank][d.space] + d.off + (d.flag >= 0 ? 2 * q.off : q.off);
       if (p.multiprocess && d.rank != rank && !(atomicOr(&s_entry_mask, 0u) & (1u << d.rank))) {
-        wait_ge<SYS>(myflags + p.entry_base + d.rank * p.nch + ch, e, p, rank, ch, int(oi - ob), -2);
+        wait_ge<SYS>(reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]) + p.entry_base + d.rank * p.nch + ch, e,
+                     p, rank, ch, int(oi - ob), -2);
         atomicOr(&s_entry_mask, 1u << d.rank);
       }
     }

@@ -38,7 +38,8 @@ for name, js in cases.items():
     plan.set_trace(None)
     rec = buf.view(grid, CAP, 2).cpu().tolist()
     t0 = min(r[0] for cta in rec for r in cta if r[0])
-    seg = {"entry": [], "epoch": [], "desc1": [], "data1": [], "ops": [], "exit": []}
+    seg = {"entry": [], "epoch": [], "desc1": [], "d_op": [], "d_in": [], "d_ptr": [], "d_bar": [], "data1": [],
+           "ops": [], "exit": []}
     for cta in rec:
         ev = [(t - t0, meta & 0xff) for t, meta in cta if t]
         if not ev:
@@ -47,6 +48,12 @@ for name, js in cases.items():
         st, ep, ds, dn, en = get(0), get(1), get(2), get(4), get(6)
         seg["entry"].append(st[0])
         seg["epoch"].append(ep[0] - st[0])
+        e7, e8, e9 = get(7), get(8), get(9)
+        if ds and e7 and e8 and e9:
+            seg["d_op"].append(e7[0] - ep[0])
+            seg["d_in"].append(e8[0] - e7[0])
+            seg["d_ptr"].append(e9[0] - e8[0])
+            seg["d_bar"].append(ds[0] - e9[0])
         if ds:
             seg["desc1"].append(ds[0] - ep[0])
             seg["data1"].append(dn[0] - ds[0])
