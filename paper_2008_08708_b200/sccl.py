@@ -303,3 +303,40 @@ class Plan(_PlanBase):
     def launch(self, sendbuf, recvbuf=None, stream=None):
         _raise(lib().sccl_launch(self._h, ctypes.c_void_p(_ptr(sendbuf)), ctypes.c_void_p(_ptr(recvbuf)),
                                  ctypes.c_void_p(_stream_ptr(stream))))
+
+
+class AutoLoopbackPlan:
+    """Per-size algorithm switching over a set of synthesized schedules of one
+    collective (e.g. a Pareto frontier; "automatically switch
+    between multiple implementations"): each new per-rank byte count picks
+    its schedule and protocol with `select` (the fitted B200 cost model) and
+    caches the plan; launches reuse it."""
+
+    def __init__(self, schedules: Sequence, dtype: int = U8, device: int = 0, max_plans: int = 16):
+        self.schedules = [_text(s).decode() for s in schedules]
+        self.dtype, self.device, self.max_plans = dtype, device, max_plans
+        self._plans = {}  # bytes_per_rank -> (schedule index, protocol, LoopbackPlan)
+
+    def plan_for(self, bytes_per_rank: int):
+        if bytes_per_rank not in self._plans:
+            if len(self._plans) >= self.max_plans:  # evict the oldest
+                oldest = next(iter(self._plans))
+                self._plans.pop(oldest)[2].close()
+            i, proto, _ = select(self.schedules, bytes_per_rank, self.dtype)
+            self._plans[bytes_per_rank] = (i, proto, LoopbackPlan(self.schedules[i], bytes_per_rank, self.dtype,
+                                                                  device=self.device, protocol=proto))
+        return self._plans[bytes_per_rank]
+
+    def launch(self, sendbufs: Sequence, recvbufs: Sequence, bytes_per_rank: int, stream=None):
+        i, proto, plan = self.plan_for(bytes_per_rank)
+        plan.launch(sendbufs, recvbufs, stream)
+        return i, proto
+
+    def check(self):
+        for _, _, plan in self._plans.values():
+            plan.check()
+
+    def close(self):
+        for _, _, plan in self._plans.values():
+            plan.close()
+        self._plans.clear()

@@ -269,6 +269,30 @@ def test_window_major_forced(monkeypatch, window, name, nbytes):
     run_gpu(js, nbytes, dt, protocol="simple", repeats=2)
 
 
+def test_auto_plan_switches_per_size():
+    """AutoLoopbackPlan over an allgather frontier: each size picks its
+    schedule and protocol, results equal the oracle of the chosen schedule."""
+    cands = [SCHED["ag_777"], SCHED["ag_b4_oneshot8"], SCHED["ag_b7_ring8"], SCHED["ag_b8_bidir8"]]
+    auto = sccl.AutoLoopbackPlan(cands, O.U8, device=0)
+    chosen = set()
+    for nb in (1024, 65536, 1 << 20, 16 << 20):
+        i, proto, plan = auto.plan_for(nb)
+        chosen.add((i, proto))
+        d = json.loads(cands[i])
+        ins = O.seeded_inputs(d["collective"], d["P"], nb, O.U8, nb)
+        ref = O.execute(d, ins, nb, O.U8)
+        send = [torch.from_numpy(x).to(DEV) for x in ins]
+        recv = [torch.zeros(r.size, dtype=torch.uint8, device=DEV) for r in ref]
+        torch.cuda.synchronize()
+        assert auto.launch(send, recv, nb) == (i, proto)
+        torch.cuda.synchronize()
+        auto.check()
+        for a, b in zip(recv, ref):
+            assert np.array_equal(a.cpu().numpy(), b)
+    assert len({p for _, p in chosen}) == 2  # LL for the small sizes, the bulk protocol for the large
+    auto.close()
+
+
 def test_baseline_full_sizes():
     """BASELINE configs 2-4 at their largest sizes, through size-independent
     properties: AG (7,7,7) at 1 GiB per rank (every output == the

@@ -70,3 +70,15 @@ def test_select_regret_vs_measured_b200_frontier():
             regrets.append(rows[cl[i][0]] / min(rows.values()) - 1)
     assert len(regrets) == 42
     assert sum(regrets) / len(regrets) <= 0.10, regrets
+
+
+def test_auto_plan_caches_per_size():
+    c = [S.to_json(S.hamiltonian_allgather(8)), S.to_json(S.one_shot_allgather(8))]
+    auto = sccl.AutoLoopbackPlan(c, sccl.U8, device=-1, max_plans=2)
+    a = auto.plan_for(1024)
+    assert auto.plan_for(1024) is a          # cached
+    assert a[1] == "ll"
+    auto.plan_for(1 << 20)
+    auto.plan_for(1 << 24)                   # evicts the oldest (1024)
+    assert 1024 not in auto._plans and len(auto._plans) == 2
+    auto.close()
