@@ -444,7 +444,8 @@ def run_multi(args):
     P = world
     js, sname = schedule_for(P, args.schedule)
     m = args.bytes
-    plan = sccl.Plan(js, rank, P, m, sccl.U8, device=local, nchannels=args.nchannels, tile_bytes=args.tile)
+    plan = sccl.Plan(js, rank, P, m, sccl.U8, device=local, nchannels=args.nchannels, tile_bytes=args.tile,
+                     mem_handles=args.mem)
     plan.bind_with()
     dev = torch.device("cuda", local)
     g = torch.Generator(device=dev)
@@ -506,7 +507,7 @@ def run_multi(args):
             "config": {"workload": f"{sname}; one rank per GPU, CUDA IPC peers over NVLink", "ranks": P,
                        "bytes_per_rank": m, "parallelism": f"ranks{P}", "nchannels": plan.info()["nchannels"],
                        "l2": "no flush: buffers >> L2",
-                       "shared_gpu": shared},
+                       "shared_gpu": shared, "mem_handles": args.mem},
             "busbw_per_rank_GBps": round(per_gpu, 2),
             "nccl": None if shared else {"ms": round(ms_nccl, 4),
                                          "busbw_per_rank_GBps": round((P - 1) * m / (ms_nccl * 1e-3) / 1e9, 2)},
@@ -530,6 +531,8 @@ def main():
     ap.add_argument("--bytes", type=int, default=128 << 20, help="per-rank allgather input")
     ap.add_argument("--schedule", default="auto", choices=["auto", "777", "oneshot", "ring"])
     ap.add_argument("--nchannels", type=int, default=0)
+    ap.add_argument("--mem", default="ipc", choices=["ipc", "vmm"],
+                    help="N>1: share plan regions through CUDA IPC handles or VMM (cuMem) fds")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--ref-bytes", type=int, default=16 << 20)
     ap.add_argument("--cpu-bytes", type=int, default=16 << 20)

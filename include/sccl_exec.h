@@ -50,6 +50,7 @@ typedef struct {
   int tile_bytes;     /* pipeline stage / copy tile bytes, multiple of 16 in [256, 65536]; 0 = auto  */
   int protocol;       /* 0 = auto, 1 = simple (TMA bulk + counters), 2 = LL (flag in data)          */
   int64_t timeout_ms; /* peer-wait watchdog; 0 = default (10 s), <0 = disabled                        */
+  int mem_handles;    /* multi-process region sharing: 0 = CUDA IPC handles, 1 = VMM (cuMem) POSIX FDs */
 } sccl_plan_opts;
 
 void sccl_plan_opts_init(sccl_plan_opts* o);
@@ -99,6 +100,15 @@ int sccl_plan_create_loopback(const char* schedule_json, size_t bytes_per_rank, 
  * gather every rank's blob (e.g. torch.distributed all_gather), bind. */
 int sccl_plan_export_handles(sccl_plan* plan, void* blob, size_t* len);
 int sccl_plan_bind_peers(sccl_plan* plan, const void* const* peer_blobs, size_t blob_len);
+
+/* VMM variant (opts.mem_handles = 1): the plan region is a cuMemCreate
+ * allocation shared as a POSIX file descriptor (the allocation path NCCL's
+ * cuMem mode and torch symmetric memory use).  export_fd returns a new fd
+ * the caller passes to the peers (e.g. SCM_RIGHTS over a Unix socket) and
+ * closes; bind_peers_fd validates the blobs like sccl_plan_bind_peers and
+ * maps peer r's region from fds[r] (fds[rank] is ignored). */
+int sccl_plan_export_fd(sccl_plan* plan, int* fd);
+int sccl_plan_bind_peers_fd(sccl_plan* plan, const void* const* peer_blobs, size_t blob_len, const int* fds);
 
 /* The registered (peer-writable) receive buffer of a multi-process plan.
  * Passing it as recvbuf to sccl_launch is zero-copy; any other recvbuf gets

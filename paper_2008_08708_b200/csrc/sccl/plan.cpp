@@ -1,7 +1,9 @@
 // Plans and the C-ABI (include/sccl_exec.h).
 #include "plan.hpp"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -88,6 +90,62 @@ bool loopback_sys() {  // SCCL_LOOPBACK_SYS=1: loopback launches use system scop
     return e && std::atoi(e) != 0;
   }();
   return v;
+}
+
+// Driver-API VMM entry points, resolved at run time through the runtime
+// (no link-time dependency on libcuda: the library must load on GPU-less
+// build hosts).
+struct Vmm {
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemExportToShareableHandle) export_handle = nullptr;
+  decltype(&cuMemImportFromShareableHandle) import_handle = nullptr;
+};
+const Vmm& vmm_api() {
+  static Vmm v;
+  static bool done = false;
+  if (!done) {
+    auto get = [](const char* name, auto& fn) {
+      void* f = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+        throw sccl::cuda_error(std::string("driver entry point ") + name + " unavailable");
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(f);
+    };
+    get("cuMemCreate", v.create);
+    get("cuMemGetAllocationGranularity", v.granularity);
+    get("cuMemAddressReserve", v.reserve);
+    get("cuMemAddressFree", v.addr_free);
+    get("cuMemMap", v.map);
+    get("cuMemUnmap", v.unmap);
+    get("cuMemSetAccess", v.set_access);
+    get("cuMemRelease", v.release);
+    get("cuMemExportToShareableHandle", v.export_handle);
+    get("cuMemImportFromShareableHandle", v.import_handle);
+    done = true;
+  }
+  return v;
+}
+void cu_check(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw sccl::cuda_error(std::string(what) + " failed (CUresult " + std::to_string(int(r)) + ")");
+}
+// map `handle` (size bytes) at a fresh VA range readable and writable by `device`
+char* vmm_map(const Vmm& v, CUmemGenericAllocationHandle handle, size_t size, int device) {
+  CUdeviceptr va = 0;
+  cu_check(v.reserve(&va, size, 0, 0, 0), "cuMemAddressReserve");
+  cu_check(v.map(va, size, 0, handle, 0), "cuMemMap");
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  cu_check(v.set_access(va, size, &acc, 1), "cuMemSetAccess");
+  return reinterpret_cast<char*>(va);
 }
 
 struct IpcBlob {
@@ -440,7 +498,23 @@ void plan_device_setup(sccl_plan& p) {
   cuda_check(cudaMalloc(&p.d_epochs, ne * sizeof(uint64_t)), "cudaMalloc(epochs)");
   cuda_check(cudaMemset(p.d_epochs, 0, ne * sizeof(uint64_t)), "memset(epochs)");
   size_t total = p.region_bytes * size_t(nlaunch);
-  cuda_check(cudaMalloc(&p.d_region, total), "cudaMalloc(region)");
+  if (p.vmm) {  // shareable cuMem allocation (POSIX fd)
+    const Vmm& v = vmm_api();
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = p.device;
+    prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    size_t gran = 0;
+    cu_check(v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+    p.vmm_size = (total + gran - 1) / gran * gran;
+    CUmemGenericAllocationHandle h = 0;
+    cu_check(v.create(&h, p.vmm_size, &prop, 0), "cuMemCreate");
+    p.vmm_handle = uint64_t(h);
+    p.d_region = vmm_map(v, h, p.vmm_size, p.device);
+  } else {
+    cuda_check(cudaMalloc(&p.d_region, total), "cudaMalloc(region)");
+  }
   cuda_check(cudaMemset(p.d_region, 0, total), "memset(region)");
   cuda_check(cudaHostAlloc(&p.h_err, 64 * sizeof(int), cudaHostAllocMapped), "cudaHostAlloc(err)");
   std::memset(p.h_err, 0, 64 * sizeof(int));
@@ -506,6 +580,7 @@ void sccl_plan_opts_init(sccl_plan_opts* o) {
   o->tile_bytes = 0;
   o->protocol = 0;
   o->timeout_ms = 0;
+  o->mem_handles = 0;
 }
 
 const char* sccl_last_error(void) { return g_err.c_str(); }
@@ -613,6 +688,8 @@ static int create_common(const char* json, int rank, int nranks, size_t bytes, i
       if (loopback && p->nch * p->nranks > p->resident_cap)
         throw invalid_argument_error("loopback needs P*nchannels <= resident CTAs (" +
                                      std::to_string(p->resident_cap) + ")");
+      if (o.mem_handles < 0 || o.mem_handles > 1) throw invalid_argument_error("mem_handles must be 0 (CUDA IPC) or 1 (VMM fd)");
+      p->vmm = !loopback && o.mem_handles == 1;
       if (!p->host_only) plan_device_setup(*p);
     } catch (...) {
       sccl_plan_destroy(p);
@@ -651,7 +728,7 @@ int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
     b.kb = p->kb;
     b.tile = p->tile;
     b.region_bytes = p->region_bytes;
-    if (!p->host_only) {
+    if (!p->host_only && !p->vmm) {
       cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
       cuda_check(cudaIpcGetMemHandle(&b.handle, p->d_region), "cudaIpcGetMemHandle");
     }
@@ -660,25 +737,31 @@ int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
   });
 }
 
+static std::vector<IpcBlob> check_blobs(sccl_plan* p, const void* const* blobs, size_t blob_len) {
+  if (!p || !blobs) throw invalid_argument_error("NULL argument");
+  if (p->loopback) throw invalid_argument_error("loopback plans have no peers");
+  if (p->bound) throw invalid_argument_error("plan already bound");
+  if (blob_len < sizeof(IpcBlob)) throw invalid_argument_error("blob too short");
+  std::vector<IpcBlob> bs(p->nranks);
+  for (int r = 0; r < p->nranks; ++r) {
+    if (!blobs[r]) throw invalid_argument_error("missing blob for rank " + std::to_string(r));
+    std::memcpy(&bs[r], blobs[r], sizeof(IpcBlob));
+    const IpcBlob& b = bs[r];
+    if (std::memcmp(b.magic, "SCCLIPC1", 8)) throw invalid_argument_error("bad blob magic from rank " + std::to_string(r));
+    if (b.rank != r || b.nranks != p->nranks)
+      throw invalid_argument_error("blob " + std::to_string(r) + " has rank/nranks mismatch");
+    if (std::strncmp(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1))
+      throw invalid_argument_error("rank " + std::to_string(r) + " lowered a different program (fingerprint mismatch)");
+    if (b.nch != p->nch || b.kc != p->kc || b.kb != p->kb || b.tile != p->tile || b.region_bytes != p->region_bytes)
+      throw invalid_argument_error("rank " + std::to_string(r) + " uses different channels/tile/region size");
+  }
+  return bs;
+}
+
 int sccl_plan_bind_peers(sccl_plan* p, const void* const* blobs, size_t blob_len) {
   return guarded([&] {
-    if (!p || !blobs) throw invalid_argument_error("NULL argument");
-    if (p->loopback) throw invalid_argument_error("loopback plans have no peers");
-    if (p->bound) throw invalid_argument_error("plan already bound");
-    if (blob_len < sizeof(IpcBlob)) throw invalid_argument_error("blob too short");
-    std::vector<IpcBlob> bs(p->nranks);
-    for (int r = 0; r < p->nranks; ++r) {
-      if (!blobs[r]) throw invalid_argument_error("missing blob for rank " + std::to_string(r));
-      std::memcpy(&bs[r], blobs[r], sizeof(IpcBlob));
-      const IpcBlob& b = bs[r];
-      if (std::memcmp(b.magic, "SCCLIPC1", 8)) throw invalid_argument_error("bad blob magic from rank " + std::to_string(r));
-      if (b.rank != r || b.nranks != p->nranks)
-        throw invalid_argument_error("blob " + std::to_string(r) + " has rank/nranks mismatch");
-      if (std::strncmp(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1))
-        throw invalid_argument_error("rank " + std::to_string(r) + " lowered a different program (fingerprint mismatch)");
-      if (b.nch != p->nch || b.kc != p->kc || b.kb != p->kb || b.tile != p->tile || b.region_bytes != p->region_bytes)
-        throw invalid_argument_error("rank " + std::to_string(r) + " uses different channels/tile/region size");
-    }
+    const std::vector<IpcBlob> bs = check_blobs(p, blobs, blob_len);
+    if (p->vmm) throw invalid_argument_error("VMM plan: bind with sccl_plan_bind_peers_fd");
     if (!p->host_only) {
       cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
       for (int r = 0; r < p->nranks; ++r) {
@@ -686,6 +769,42 @@ int sccl_plan_bind_peers(sccl_plan* p, const void* const* blobs, size_t blob_len
         void* ptr = nullptr;
         cuda_check(cudaIpcOpenMemHandle(&ptr, bs[r].handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
         p->peer_region[r] = static_cast<char*>(ptr);
+      }
+    }
+    p->bound = true;
+  });
+}
+
+int sccl_plan_export_fd(sccl_plan* p, int* fd) {
+  return guarded([&] {
+    if (!p || !fd) throw invalid_argument_error("NULL argument");
+    if (!p->vmm) throw invalid_argument_error("plan was not created with mem_handles = 1 (VMM)");
+    if (p->host_only) throw invalid_argument_error("host-only plan has no device region");
+    const Vmm& v = vmm_api();
+    int out = -1;
+    cu_check(v.export_handle(&out, CUmemGenericAllocationHandle(p->vmm_handle), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+             "cuMemExportToShareableHandle");
+    *fd = out;
+  });
+}
+
+int sccl_plan_bind_peers_fd(sccl_plan* p, const void* const* blobs, size_t blob_len, const int* fds) {
+  return guarded([&] {
+    const std::vector<IpcBlob> bs = check_blobs(p, blobs, blob_len);
+    if (!p->vmm) throw invalid_argument_error("plan was not created with mem_handles = 1 (VMM)");
+    if (!fds) throw invalid_argument_error("NULL fds");
+    if (!p->host_only) {
+      cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+      const Vmm& v = vmm_api();
+      p->peer_vmm.assign(p->nranks, 0);
+      for (int r = 0; r < p->nranks; ++r) {
+        if (r == p->rank) continue;
+        if (fds[r] < 0) throw invalid_argument_error("missing fd for rank " + std::to_string(r));
+        CUmemGenericAllocationHandle h = 0;
+        cu_check(v.import_handle(&h, reinterpret_cast<void*>(uintptr_t(fds[r])), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+                 "cuMemImportFromShareableHandle");
+        p->peer_vmm[r] = uint64_t(h);
+        p->peer_region[r] = vmm_map(v, h, p->vmm_size, p->device);
       }
     }
     p->bound = true;
@@ -830,15 +949,34 @@ int sccl_plan_destroy(sccl_plan* p) {
   if (!p) return SCCL_OK;
   if (!p->host_only && p->device >= 0) {
     cudaSetDevice(p->device);
-    for (size_t r = 0; r < p->peer_region.size(); ++r)
-      if (int(r) != p->rank && p->peer_region[r]) cudaIpcCloseMemHandle(p->peer_region[r]);
+    if (p->vmm) {
+      const Vmm& v = vmm_api();
+      for (size_t r = 0; r < p->peer_region.size(); ++r)
+        if (int(r) != p->rank && p->peer_region[r]) {
+          v.unmap(CUdeviceptr(p->peer_region[r]), p->vmm_size);
+          v.addr_free(CUdeviceptr(p->peer_region[r]), p->vmm_size);
+          if (r < p->peer_vmm.size() && p->peer_vmm[r]) v.release(CUmemGenericAllocationHandle(p->peer_vmm[r]));
+        }
+    } else {
+      for (size_t r = 0; r < p->peer_region.size(); ++r)
+        if (int(r) != p->rank && p->peer_region[r]) cudaIpcCloseMemHandle(p->peer_region[r]);
+    }
     cudaFree(p->d_ops);
     cudaFree(p->d_ins);
     cudaFree(p->d_outs);
     cudaFree(p->d_prog);
     cudaFree(p->d_nwin);
     cudaFree(p->d_epochs);
-    cudaFree(p->d_region);
+    if (p->vmm) {
+      if (p->d_region) {
+        const Vmm& v = vmm_api();
+        v.unmap(CUdeviceptr(p->d_region), p->vmm_size);
+        v.addr_free(CUdeviceptr(p->d_region), p->vmm_size);
+        v.release(CUmemGenericAllocationHandle(p->vmm_handle));
+      }
+    } else {
+      cudaFree(p->d_region);
+    }
     if (p->h_err) cudaFreeHost(p->h_err);
   }
   delete p;

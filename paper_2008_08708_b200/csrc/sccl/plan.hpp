@@ -46,6 +46,11 @@ struct sccl_plan {
   size_t region_bytes = 0, flags_bytes = 0, scratch_off = 0, recv_off = 0;
   int entry_base = 0;
   std::vector<char*> peer_region;  // multi-process: every rank's region (own included)
+  // VMM mode (opts.mem_handles = 1): cuMem allocation handles (CUmemGenericAllocationHandle)
+  bool vmm = false;
+  uint64_t vmm_handle = 0;
+  size_t vmm_size = 0;
+  std::vector<uint64_t> peer_vmm;  // imported handles, 0 = none
   bool bound = false;
 
   int* h_err = nullptr;  // host-mapped watchdog record

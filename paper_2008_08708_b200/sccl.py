@@ -41,7 +41,8 @@ class PeerTimeoutError(SCCLError):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("nchannels", ctypes.c_int), ("chunk_groups", ctypes.c_int),
-                ("tile_bytes", ctypes.c_int), ("protocol", ctypes.c_int), ("timeout_ms", ctypes.c_int64)]
+                ("tile_bytes", ctypes.c_int), ("protocol", ctypes.c_int), ("timeout_ms", ctypes.c_int64),
+                ("mem_handles", ctypes.c_int)]
 
 
 _lib = None
@@ -69,6 +70,8 @@ def lib():
                                                 ctypes.POINTER(_Opts), ctypes.POINTER(c_p)]
         L.sccl_plan_export_handles.argtypes = [c_p, c_p, ctypes.POINTER(c_sz)]
         L.sccl_plan_bind_peers.argtypes = [c_p, ctypes.POINTER(c_p), c_sz]
+        L.sccl_plan_export_fd.argtypes = [c_p, ctypes.POINTER(ctypes.c_int)]
+        L.sccl_plan_bind_peers_fd.argtypes = [c_p, ctypes.POINTER(c_p), c_sz, ctypes.POINTER(ctypes.c_int)]
         L.sccl_plan_recv_buffer.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_sz)]
         L.sccl_launch.argtypes = [c_p, c_p, c_p, c_p]
         L.sccl_launch_loopback.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
@@ -163,9 +166,12 @@ def version() -> str:
 PROTOCOLS = {"auto": 0, "simple": 1, "ll": 2}
 
 
+MEM_HANDLES = {"ipc": 0, "vmm": 1}
+
+
 def _opts(device: int, nchannels: int, tile_bytes: int, timeout_ms: int, chunk_groups: int = 0,
-          protocol: str = "auto") -> _Opts:
-    return _Opts(device, nchannels, chunk_groups, tile_bytes, PROTOCOLS[protocol], timeout_ms)
+          protocol: str = "auto", mem_handles: str = "ipc") -> _Opts:
+    return _Opts(device, nchannels, chunk_groups, tile_bytes, PROTOCOLS[protocol], timeout_ms, MEM_HANDLES[mem_handles])
 
 
 def _ptr(x) -> int:
@@ -260,13 +266,16 @@ class LoopbackPlan(_PlanBase):
 
 
 class Plan(_PlanBase):
-    """One rank of a one-process-per-GPU execution (peers over CUDA IPC)."""
+    """One rank of a one-process-per-GPU execution.  Peers' plan regions are
+    mapped through CUDA IPC handles (mem_handles="ipc") or VMM cuMem
+    allocations shared as POSIX file descriptors (mem_handles="vmm")."""
 
     def __init__(self, schedule, rank: int, nranks: int, bytes_per_rank: int, dtype: int = U8,
                  device: int = 0, nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0,
-                 chunk_groups: int = 0, protocol: str = "auto"):
+                 chunk_groups: int = 0, protocol: str = "auto", mem_handles: str = "ipc"):
         super().__init__()
-        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol)
+        self.mem_handles = mem_handles
+        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol, mem_handles)
         rc = lib().sccl_plan_create(_text(schedule), rank, nranks, bytes_per_rank, dtype, SUM,
                                     ctypes.byref(o), ctypes.byref(self._h))
         _raise(rc)
@@ -287,12 +296,34 @@ class Plan(_PlanBase):
         arr = (ctypes.c_void_p * len(bufs))(*[ctypes.addressof(b) for b in bufs])
         _raise(lib().sccl_plan_bind_peers(self._h, arr, len(blobs[0])))
 
+    def export_fd(self) -> int:
+        """VMM plans: a new POSIX fd of this rank's region (the caller closes it)."""
+        fd = ctypes.c_int(-1)
+        _raise(lib().sccl_plan_export_fd(self._h, ctypes.byref(fd)))
+        return fd.value
+
+    def bind_peers_fd(self, blobs: Sequence[bytes], fds: Sequence[int]):
+        bufs = [ctypes.create_string_buffer(b, len(b)) for b in blobs]
+        arr = (ctypes.c_void_p * len(bufs))(*[ctypes.addressof(b) for b in bufs])
+        fa = (ctypes.c_int * len(fds))(*fds)
+        _raise(lib().sccl_plan_bind_peers_fd(self._h, arr, len(blobs[0]), fa))
+
     def bind_with(self, group=None):
-        """Exchange handles through torch.distributed (all_gather_object)."""
+        """Exchange handles through torch.distributed (all_gather_object);
+        VMM plans also pass their region fds over Unix sockets (SCM_RIGHTS)."""
         import torch.distributed as dist
         blobs: List[Optional[bytes]] = [None] * self.nranks
         dist.all_gather_object(blobs, self.export_handles(), group=group)
-        self.bind_peers(blobs)
+        if self.mem_handles != "vmm":
+            self.bind_peers(blobs)
+            return
+        fds = _exchange_fds(self.rank, self.nranks, self.export_fd(), group)
+        try:
+            self.bind_peers_fd(blobs, fds)
+        finally:
+            for r, fd in enumerate(fds):
+                if r != self.rank and fd >= 0:
+                    os.close(fd)
 
     def recv_buffer(self):
         p = ctypes.c_void_p(0)
@@ -303,6 +334,48 @@ class Plan(_PlanBase):
     def launch(self, sendbuf, recvbuf=None, stream=None):
         _raise(lib().sccl_launch(self._h, ctypes.c_void_p(_ptr(sendbuf)), ctypes.c_void_p(_ptr(recvbuf)),
                                  ctypes.c_void_p(_stream_ptr(stream))))
+
+
+def _exchange_fds(rank: int, nranks: int, my_fd: int, group=None) -> List[int]:
+    """All-to-all of one file descriptor per rank over Linux abstract Unix
+    sockets (SCM_RIGHTS); the socket names travel through torch.distributed.
+    Returns fds[r] = a local fd for rank r's descriptor (fds[rank] = -1).
+    Consumes (closes) my_fd."""
+    import socket
+    import threading
+    import uuid
+    import torch.distributed as dist
+    name = f"\0sccl-{uuid.uuid4().hex}-{rank}"
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    srv.bind(name)
+    srv.listen(nranks)
+    names: List[Optional[str]] = [None] * nranks
+    dist.all_gather_object(names, name, group=group)
+    fds = [-1] * nranks
+
+    def send_all():
+        for r in range(nranks):
+            if r == rank:
+                continue
+            c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            c.connect(names[r])
+            socket.send_fds(c, [rank.to_bytes(4, "little")], [my_fd])
+            c.close()
+
+    t = threading.Thread(target=send_all)
+    t.start()
+    try:
+        for _ in range(nranks - 1):
+            conn, _ = srv.accept()
+            msg, got, _, _ = socket.recv_fds(conn, 4, 1)
+            fds[int.from_bytes(msg, "little")] = got[0]
+            conn.close()
+    finally:
+        t.join()
+        srv.close()
+        os.close(my_fd)
+    dist.barrier(group=group)
+    return fds
 
 
 class AutoLoopbackPlan:

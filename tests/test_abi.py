@@ -130,3 +130,55 @@ def test_gloo_two_process_handle_exchange(tmp_path, mode):
         assert len(fps) == 1
     else:
         assert text.count("MISMATCH") == 2
+
+
+_FD_WORKER = r"""
+import os, sys
+sys.path.insert(0, {root!r})
+import torch.distributed as dist
+from paper_2008_08708_b200 import sccl
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=int(sys.argv[1]), world_size=3)
+r = dist.get_rank()
+fd0 = os.memfd_create("sccl-test")  # stands in for a cuMem region fd: any descriptor travels the same way
+os.write(fd0, b"rank%d" % r)
+fds = sccl._exchange_fds(r, 3, fd0)
+for q, fd in enumerate(fds):
+    if q == r:
+        assert fd == -1
+    else:
+        assert os.pread(fd, 16, 0) == b"rank%d" % q, (r, q)
+        os.close(fd)
+print("FDS_OK", r, flush=True)
+dist.destroy_process_group()
+"""
+
+
+def test_fd_exchange_three_processes(tmp_path):
+    """VMM handle path, host side: every rank's file descriptor reaches every
+    other rank over abstract Unix sockets (SCM_RIGHTS), world size 3, gloo."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = tmp_path / "fd.py"
+    script.write_text(_FD_WORKER.format(root=ROOT, port=port))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    procs = [subprocess.Popen(["python", str(script), str(r)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                              text=True, env=env) for r in range(3)]
+    outs = [p.communicate(timeout=120) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e
+    assert "".join(o for o, _ in outs).count("FDS_OK") == 3
+
+
+def test_vmm_plan_host_only_errors():
+    js = S.to_json(S.one_shot_allgather(2))
+    p = sccl.Plan(js, 0, 2, 4096, sccl.U8, device=-1, mem_handles="vmm")
+    with pytest.raises(sccl.InvalidArgumentError, match="host-only"):
+        p.export_fd()
+    ipc = sccl.Plan(js, 0, 2, 4096, sccl.U8, device=-1)
+    with pytest.raises(sccl.InvalidArgumentError, match="VMM"):
+        ipc.export_fd()
+    blobs = [p.export_handles(), sccl.Plan(js, 1, 2, 4096, sccl.U8, device=-1, mem_handles="vmm").export_handles()]
+    with pytest.raises(sccl.InvalidArgumentError, match="bind_peers_fd"):
+        p.bind_peers(blobs)

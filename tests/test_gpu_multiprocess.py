@@ -24,6 +24,7 @@ import numpy as np, torch, torch.distributed as dist
 import oracle as O
 from paper_2008_08708_b200 import sccl, schedules as S
 rank, W = int(sys.argv[1]), int(sys.argv[2])
+MEM = sys.argv[3] if len(sys.argv) > 3 else "ipc"
 dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=W)
 torch.cuda.set_device(0)
 if W == 2:
@@ -56,7 +57,7 @@ for case in cases:
     d = json.loads(js)
     ins = O.seeded_inputs(d["collective"], W, nb, dt, 17)
     ref = O.execute(d, ins, nb, dt)
-    plan = sccl.Plan(js, rank, W, nb, dt, device=0, protocol=proto, timeout_ms=120000)
+    plan = sccl.Plan(js, rank, W, nb, dt, device=0, protocol=proto, timeout_ms=120000, mem_handles=MEM)
     plan.bind_with()
     send = torch.from_numpy(ins[rank]).cuda()
     for it in range(3):  # back-to-back launches: entry handshake + epochs
@@ -72,15 +73,18 @@ dist.destroy_process_group()
 """
 
 
+@pytest.mark.parametrize("mem", ["ipc", "vmm"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_processes_one_gpu(tmp_path, world):
+def test_processes_one_gpu(tmp_path, world, mem):
+    """world processes, one rank each, all on cuda:0: peers' regions mapped
+    through CUDA IPC handles or VMM (cuMem) POSIX fds passed over Unix sockets."""
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     script = tmp_path / "w.py"
     script.write_text(WORKER.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"), port=port))
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
-    procs = [subprocess.Popen([sys.executable, str(script), str(r), str(world)], stdout=subprocess.PIPE,
+    procs = [subprocess.Popen([sys.executable, str(script), str(r), str(world), mem], stdout=subprocess.PIPE,
                               stderr=subprocess.PIPE, text=True, env=env) for r in range(world)]
     try:
         outs = [p.communicate(timeout=600) for p in procs]
