@@ -337,7 +337,9 @@ def run_loopback(args):
     dsend = [send, [torch.empty_like(x) for x in send]]
     drecv = [recv, [torch.empty_like(x) for x in recv]]
     s_h2d, s_k, s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    e2e_steps = max(4, min(args.steps, 12))
+    # enough steps that the pipeline fill (one H2D before the first D2H) is
+    # a small part of the timed region
+    e2e_steps = max(8, min(2 * args.steps, 32))
 
     def e2e_run(nsteps):
         ev_in = [torch.cuda.Event() for _ in range(nsteps)]
