@@ -156,6 +156,18 @@ __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
 // without the L1 invalidation (CCTL.IVALL) that fence.acq_rel adds: every
 // use here is a release pattern, the acquire side uses ld.acquire.
 template <bool SYS>
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  if (SYS) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+template <bool SYS>
+__device__ __forceinline__ void fence_acq() {  // after a relaxed load that observed a release
+  if (SYS) asm volatile("fence.acquire.sys;" ::: "memory");
+  else asm volatile("fence.acquire.gpu;" ::: "memory");
+}
+template <bool SYS>
 __device__ __forceinline__ void fence_rel() {
   if (SYS) asm volatile("fence.release.sys;" ::: "memory");
   else asm volatile("fence.release.gpu;" ::: "memory");
@@ -235,13 +247,16 @@ __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p
                             int slot) {
   uint64_t v = ld_acquire<SYS>(f);
   if (v >= target) return v;
+  // poll with relaxed (strong) loads -- no L1 invalidation per poll -- and
+  // acquire once the target is reached
   uint64_t t0 = globaltimer();
   uint32_t spins = 0;
-  while ((v = ld_acquire<SYS>(f)) < target) {
+  while ((v = ld_relaxed<SYS>(f)) < target) {
     if (++spins > 64) __nanosleep(32);
     if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
       watchdog_fire(p, rank, ch, op, slot, target, v);
   }
+  fence_acq<SYS>();
   return v;
 }
 
