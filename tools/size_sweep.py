@@ -72,7 +72,8 @@ def gpu_sweep(cfg, coll, scheds, dtypes, sizes):
     for name, js in scheds:
         for dt, dtn in dtypes:
             for sz in sizes:
-                row = {"cfg": cfg, "collective": coll, "schedule": name, "dtype": dtn, "bytes_per_rank": sz}
+                row = {"cfg": cfg, "collective": coll, "schedule": name, "dtype": dtn, "bytes_per_rank": sz,
+                       "total_bytes": P * sz}  # nccl-tests' size convention (all ranks)
                 try:
                     plan = sccl.LoopbackPlan(js, sz, dt, device=0)
                 except sccl.SCCLError as e:
