@@ -98,9 +98,11 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint
                "r"(bytes)
                : "memory");
 }
-// L2 eviction policies for bulk copies: receipts that a later op of the
-// receiver reads (forwards, reduce inputs) are kept; data read or written
-// for the last time is evicted first, so it does not push those out.
+// L2 eviction policies for bulk copies: data read or written for the last
+// time is evicted first, so it does not push out receipts that a later op
+// of the receiver reads (forwards, reduce inputs).  Those are stored with
+// the default policy, or evict-last when the plan discards them after use
+// (kL2RelayPlain clear).
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -710,7 +712,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             else elem_op<DT>(in, op.nin, out, op.nout, int64_t(lo + nv), n - nv, 0, 1);
           }
           if (outp && nv) {
-            if (p.l2hint) bulk_store_hint(outp + lo, bufs + size_t(s) * STAGE, nv, every ? pol_last : pol_first);
+            if (p.l2hint && !((p.l2hint & kL2RelayPlain) && every))
+              bulk_store_hint(outp + lo, bufs + size_t(s) * STAGE, nv, every ? pol_last : pol_first);
             else bulk_store(outp + lo, bufs + size_t(s) * STAGE, nv);
           }
           bulk_commit();

@@ -13,6 +13,7 @@ constexpr int kMaxOpOut = 32;   // destinations of one op
 constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
 constexpr int kMaxTile = 65536; // one TMA pipeline stage (bytes)
 constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
+constexpr int kL2RelayPlain = 2;  // KParams::l2hint: re-read receipts stored with the default L2 policy
 constexpr int kStageBudget = 196608;  // bytes of stages per CTA (nstage * tile)
 constexpr int kThreads = 352;   // producer, kStorerWarps storer warps, signaler + 6 compute warps
 constexpr int kSmemHdr = 8192;  // simple kernel: shared-memory header (barriers, rings, signaler window) ahead of the stages
@@ -72,7 +73,7 @@ struct KParams {
   int selfpub;           // 1: storer warps release their own counters (latency-bound plans)
   uint32_t window;       // simple protocol: bytes of an op a CTA moves before the next op (0 = whole op)
   const uint32_t* nwin;  // [launched CTAs] windows of each CTA's program
-  int l2hint;            // 1: L2 eviction hints on bulk copies (launch traffic >> L2)
+  int l2hint;            // bit 0: L2 eviction hints on bulk copies (launch traffic >> L2); | kL2RelayPlain
   int discard;           // 1: drop consumed scratch receipts of reduce tiles from L2 (no write-back)
 };
 

@@ -391,8 +391,14 @@ void encode_program(sccl_plan& p) {
 //    direct alltoall) stay op-major: the per-window descriptor reloads
 //    would only cost.  Below kStreamBytes: AR at 16 MiB/rank was 3-5 %
 //    slower with windows and hints.
-//  * L2 hints: receipts a later op re-reads are stored evict-last,
-//    single-use loads and stores evict-first (tools/gpu_runs/l2hint_round1t.sh).
+//  * L2 hints: single-use loads and stores evict-first
+//    (tools/gpu_runs/l2hint_round1t.sh).  Receipts a later op re-reads are
+//    stored with the default policy: evict-last cost 1.5-3 % on relays and
+//    reduce chains (AG (7,7,7) 128 MiB 1945 -> 1888 us, AR (56,14,14)
+//    663 -> 654, ring AR 616 -> 600; tools/gpu_runs/l2mode2_round1w.sh).
+//    Only plans that discard the receipts after use keep evict-last (one-shot
+//    AR: 572 vs 578 us).  Demoting a relay to evict_normal with
+//    applypriority after its last load cost 7-17 % (the instructions).
 //  * discards: wide reductions (fan-in >= 4) drop consumed scratch receipts
 //    from L2 (discard.global.L2: no write-back of dead bytes): (8,2,2) at
 //    64/128 MiB 321 -> 296 / 614 -> 560 us; chains of 2-input reduces lost
@@ -409,10 +415,11 @@ void choose_streaming(sccl_plan& p, const ProgramStats& st, bool loopback) {
     const long w = std::atol(env);
     p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
   }
-  p.l2hint = streams;
+  p.l2hint = streams ? 1 : 0;
   if (const char* env = std::getenv("SCCL_L2HINT")) p.l2hint = std::atoi(env) != 0;
   p.discard = p.l2hint && st.max_fanin >= 4;
   if (const char* env = std::getenv("SCCL_DISCARD")) p.discard = std::atoi(env) != 0 && !p.ll;
+  if (p.l2hint && !p.discard) p.l2hint |= kL2RelayPlain;
   // windows of each launched CTA's program
   const int nl = loopback ? p.sched.P : 1;
   p.nwin.assign(size_t(nl) * p.nch, 1u);
@@ -549,7 +556,7 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.outs = p.d_outs;
   k.prog = p.d_prog;
   k.window = p.window;
-  k.l2hint = p.l2hint ? 1 : 0;
+  k.l2hint = p.l2hint;
   k.discard = p.discard ? 1 : 0;
   k.nwin = p.d_nwin;
   k.epochs = p.d_epochs;
@@ -935,7 +942,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

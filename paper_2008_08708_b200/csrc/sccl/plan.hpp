@@ -29,7 +29,7 @@ struct sccl_plan {
   std::vector<sccl::DevOut> outs;
   std::vector<uint32_t> prog;  // [P*kc+1]: op range per (rank, chunk group)
   uint32_t window = 0;         // simple protocol: window-major byte window (0 = op-major)
-  bool l2hint = false;         // L2 eviction hints on bulk copies
+  int l2hint = 0;              // L2 eviction hints on bulk copies (bit 0; bits 1-2: experiments)
   bool discard = false;        // drop consumed scratch receipts of reduce tiles from L2
   std::vector<uint32_t> nwin;  // [launched CTAs] windows of each CTA's program
 

@@ -65,6 +65,13 @@ def test_l2_hints_above_one_gigabyte():
     assert info("ag777", 1 << 20, protocol="simple")["l2hint"] == 0
 
 
+def test_relays_evict_last_only_when_discarded():
+    assert info("ag777", 128 << 20, protocol="simple")["relay_evict_last"] == 0
+    assert info("ar56", 128 << 20, protocol="simple")["relay_evict_last"] == 0
+    assert info("ar822", 128 << 20, protocol="simple")["relay_evict_last"] == 1  # discarded after the reduce
+    assert info("ar822", 16 << 20, protocol="simple")["relay_evict_last"] == 0   # no hints at all
+
+
 def test_discard_only_for_wide_streaming_reductions():
     assert info("ar822", 128 << 20, protocol="simple")["discard"] == 1   # fan-in 8
     assert info("ar56", 128 << 20, protocol="simple")["discard"] == 0    # 2-input reduce chain

@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Loopback tuning matrix on one GPU: for each (schedule, size, knob set)
 time the executor (CUDA events) and print one JSON line.  Knobs: tile,
-stage budget (env SCCL_STAGE_BUDGET), chunk groups, byte parts, protocol."""
+stage budget (env SCCL_STAGE_BUDGET), chunk groups, byte parts, protocol,
+and "env": any SCCL_* plan variable set for that plan only."""
 import itertools
 import json
 import os
@@ -37,6 +38,26 @@ def time_plan(plan, send, recv, iters):
     return a.elapsed_time(b) * 1e3 / iters
 
 
+def cudart():
+    import ctypes
+    import glob
+    import nvidia.cuda_runtime as m
+    return ctypes.CDLL(glob.glob(os.path.join(m.__path__[0], "lib", "libcudart.so*"))[0])
+
+
+def set_persisting_l2(nbytes):
+    """cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize): the L2 set-aside
+    that evict_last accesses may occupy."""
+    import ctypes
+    rt = cudart()
+    rc = rt.cudaDeviceSetLimit(ctypes.c_int(0x06), ctypes.c_size_t(nbytes))
+    v = ctypes.c_size_t(0)
+    rt.cudaDeviceGetLimit(ctypes.byref(v), ctypes.c_int(0x06))
+    mx = ctypes.c_int(0)
+    rt.cudaDeviceGetAttribute(ctypes.byref(mx), ctypes.c_int(108), ctypes.c_int(0))
+    return rc, v.value, mx.value
+
+
 def main():
     P = 8
     ag = S.hamiltonian_allgather(P)
@@ -61,6 +82,9 @@ def main():
             os.environ["SCCL_SEND_ORDER"] = kn["order"]
         else:
             os.environ.pop("SCCL_SEND_ORDER", None)
+        persist = set_persisting_l2(kn.get("persist", 0))
+        for k, v in kn.get("env", {}).items():  # e.g. {"SCCL_WINDOW": "32768"}: read at plan creation
+            os.environ[k] = str(v)
         if "budget" in kn:
             os.environ["SCCL_STAGE_BUDGET"] = str(kn["budget"])
         else:
@@ -71,6 +95,8 @@ def main():
         except sccl.SCCLError as e:
             print(json.dumps({"sched": name, "bytes": sz, "knobs": kn, "error": str(e)[:100]}), flush=True)
             continue
+        for k in kn.get("env", {}):
+            os.environ.pop(k, None)
         rb = plan.recv_bytes
         us = time_plan(plan, [x[:sz] for x in send], [x[:rb] for x in recv], 20 if sz >= (16 << 20) else 100)
         info = plan.info()
@@ -80,7 +106,8 @@ def main():
         print(json.dumps({"sched": name, "bytes": sz, "knobs": kn, "us": round(us, 2),
                           "hbm_TBps": round(hbm / us / 1e6, 3), "kc": info["chunk_groups"], "kb": info["byte_parts"],
                           "tile": info["tile_bytes"], "nstage": info["nstage"], "proto": info["protocol"],
-                          "grid": info["grid"]}), flush=True)
+                          "grid": info["grid"], "window": info["window"],
+                          "persist_l2": persist}), flush=True)
         plan.close()
 
 
