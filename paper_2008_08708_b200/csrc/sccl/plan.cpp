@@ -399,6 +399,10 @@ void encode_program(sccl_plan& p) {
 //    Only plans that discard the receipts after use keep evict-last (one-shot
 //    AR: 572 vs 578 us).  Demoting a relay to evict_normal with
 //    applypriority after its last load cost 7-17 % (the instructions).
+//    Discarding chain receipts from the signaler warp once their tile's
+//    writes landed (off the compute path) still cost 1-3 % on (56,14,14)
+//    and ring AR, and 5 % on (8,2,2) against the compute warps
+//    (tools/gpu_runs/discard3_round1w.sh).
 //  * discards: wide reductions (fan-in >= 4) drop consumed scratch receipts
 //    from L2 (discard.global.L2: no write-back of dead bytes): (8,2,2) at
 //    64/128 MiB 321 -> 296 / 614 -> 560 us; chains of 2-input reduces lost
@@ -416,10 +420,12 @@ void choose_streaming(sccl_plan& p, const ProgramStats& st, bool loopback) {
     p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
   }
   p.l2hint = streams ? 1 : 0;
-  if (const char* env = std::getenv("SCCL_L2HINT")) p.l2hint = std::atoi(env) != 0;
+  const char* hint_env = std::getenv("SCCL_L2HINT");  // 0, 1, or 3 (| kL2RelayPlain)
+  if (hint_env) p.l2hint = std::atoi(hint_env) & 3;
+  if (p.l2hint == kL2RelayPlain) p.l2hint = 0;
   p.discard = p.l2hint && st.max_fanin >= 4;
   if (const char* env = std::getenv("SCCL_DISCARD")) p.discard = std::atoi(env) != 0 && !p.ll;
-  if (p.l2hint && !p.discard) p.l2hint |= kL2RelayPlain;
+  if (p.l2hint && !p.discard && !hint_env) p.l2hint |= kL2RelayPlain;
   // windows of each launched CTA's program
   const int nl = loopback ? p.sched.P : 1;
   p.nwin.assign(size_t(nl) * p.nch, 1u);
