@@ -59,11 +59,19 @@ __host__ __device__ constexpr size_t smem_bytes(int tile, int nstage) { return S
 struct DPart {
   int64_t off, len;
 };
-__device__ __forceinline__ DPart dsplit16(int64_t L, int64_t K, int64_t i) {
-  int64_t Uu = L >> 4;
-  int64_t lo = (i * Uu / K) << 4;
-  int64_t hi = (i == K - 1) ? L : (((i + 1) * Uu / K) << 4);
+// byte part i of K of an L-byte range in 16-byte units (the host's split16),
+// with x / K = umulhi(x, ceil(2^64 / K)), exact for x < 2^64 / K (here
+// x < K * L / 16): no 64-bit divide on the per-op path
+__device__ __forceinline__ DPart dsplit16m(int64_t L, int K, uint64_t magic, int i) {
+  if (K == 1) return {0, L};
+  const uint64_t Uu = uint64_t(L) >> 4;
+  const int64_t lo = int64_t(__umul64hi(uint64_t(i) * Uu, magic) << 4);
+  const int64_t hi = (i == K - 1) ? L : int64_t(__umul64hi(uint64_t(i + 1) * Uu, magic) << 4);
   return {lo, hi - lo};
+}
+// tiles of T bytes covering n bytes
+__device__ __forceinline__ uint32_t ntiles_of(uint64_t n, uint32_t T) {
+  return n >> 31 ? uint32_t((n + T - 1) / T) : (uint32_t(n) + T - 1) / T;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -530,7 +538,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   const uint32_t nwin = s_nwin;
   auto item = [&](const DevOp& op, uint32_t w, DPart& q, uint64_t& wlo, uint64_t& whi) -> bool {
     if (op.kind == 2 || int(op.chunk % uint32_t(p.kc)) != cg) return false;
-    q = dsplit16(int64_t(op.len), p.kb, cb);
+    q = dsplit16m(int64_t(op.len), p.kb, p.kb_magic, cb);
     if (q.len == 0) return false;  // empty sub-range: nothing sent, nothing awaited
     wlo = W ? uint64_t(w) * W : 0;
     if (wlo >= uint64_t(q.len)) return false;
@@ -547,7 +555,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           for (int i = lane; i < op.nin; i += 32) {
             const DevIn in = p.ins[op.in_begin + i];
             if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
-            const DPart q = dsplit16(int64_t(in.len), p.kb, cb);
+            const DPart q = dsplit16m(int64_t(in.len), p.kb, p.kb_magic, cb);
             if (q.len) wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, e * uint64_t(q.len), p, rank, ch,
                                     int(oi - ob), in.flag);
           }
@@ -595,7 +603,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
 
       // ---- pipelined op: tiles of this window ----
       const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
-      const uint32_t ntiles = uint32_t((whi - wlo + T - 1) / T);
+      const uint32_t ntiles = ntiles_of(whi - wlo, T);
 
       if (warp == 0) {
         // ================= producer =================
@@ -780,7 +788,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         }
         const uint32_t em = __ballot_sync(0xffffffffu, every);
         const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
-        const uint32_t nt = uint32_t((whi - wlo + T - 1) / T);
+        const uint32_t nt = ntiles_of(whi - wlo, T);
         if (lane == 0) {
           x.fbase = (e - 1) * uint64_t(q.len);
           x.qlen = uint64_t(q.len);
@@ -1006,7 +1014,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
       for (int i = 0; i < op.nin; ++i) {
         const DevIn in = p.ins[op.in_begin + i];
         if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
-        const DPart q = dsplit16(int64_t(in.len), p.kb, cb);
+        const DPart q = dsplit16m(int64_t(in.len), p.kb, p.kb_magic, cb);
         const char* slot = p.base[in.rank][in.space] + in.off + 2 * q.off;
         const int64_t npair = (q.len + 7) / 8;
         for (int64_t k = tid; k < npair; k += LL_NT)
@@ -1015,7 +1023,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
       continue;
     }
     if (int(op.chunk % uint32_t(p.kc)) != cg) continue;
-    const DPart q = dsplit16(int64_t(op.len), p.kb, cb);
+    const DPart q = dsplit16m(int64_t(op.len), p.kb, p.kb_magic, cb);
     if (q.len == 0) continue;
     if (tid < op.nin) {
       const DevIn in = p.ins[op.in_begin + tid];

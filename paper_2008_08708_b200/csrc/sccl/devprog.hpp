@@ -63,6 +63,7 @@ struct KParams {
   long long timeout_ns;
   int P, nch, rank0, nranks_launch;
   int kc, kb;            // nch = kc * kb: chunk groups x byte parts per chunk
+  uint64_t kb_magic;     // ceil(2^64 / kb) (0 if kb == 1): byte-part split without a 64-bit divide
   int tile;              // copy tile = pipeline stage bytes (<= kMaxTile); reduce tiles tile/nin
   int nstage;            // pipeline stages (<= kMaxStages, a multiple of kStorerWarps)
   int entry_base;        // index of the entry-handshake flags in FLAGS

@@ -572,6 +572,7 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.nch = p.nch;
   k.kc = p.kc;
   k.kb = p.kb;
+  k.kb_magic = p.kb > 1 ? ~uint64_t(0) / uint64_t(p.kb) + 1 : 0;
   k.tile = p.tile;
   k.nstage = p.nstage;
   k.ll = p.ll ? 1 : 0;
