@@ -54,7 +54,8 @@ constexpr int NPART = NT - 32;       // threads of the unaligned path (all but t
 constexpr int SIGQ = 64;             // tile completion ring (storers -> signaler), indexed by tile number
 constexpr int NSTAGE = kMaxStages;   // barrier sets; stages in use = KParams::nstage (a multiple of NSW)
 constexpr int SIGWIN = 8;            // ops the signaler keeps prepared ahead of their completion
-constexpr size_t SMEM_HDR = kSmemHdr;  // mbarriers, completion ring, signaler op window, discard records
+constexpr size_t SMEM_HDR = kSmemHdr;
+constexpr int kDescCache = 11264;    // bytes of descriptors cached per CTA  // mbarriers, completion ring, signaler op window, discard records
 __host__ __device__ constexpr size_t smem_bytes(int tile, int nstage) { return SMEM_HDR + size_t(nstage) * tile; }
 struct DPart {
   int64_t off, len;
@@ -443,6 +444,10 @@ struct Smem {
   uint32_t published;    // tiles < published are complete and their counters released (in tile order)
   uint32_t entry_mask;   // peers whose entry handshake this CTA has seen
   uint32_t trace_n;      // debug trace records written by this CTA
+  // this CTA's op / in / out descriptors, copied in the prologue when they
+  // fit (otherwise read from global memory): the per-op descriptor loads of
+  // every role hit shared memory instead of L1/L2
+  alignas(16) uint8_t dcache[kDescCache];
 };
 static_assert(sizeof(Smem) <= SMEM_HDR, "smem header");
 
@@ -503,6 +508,30 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < SIGQ; i += NT) S.done[i] = 0;
+  const uint4 d0 = reinterpret_cast<const uint4*>(p.dtab)[(rank * p.kc + cg) * 2],
+              d1 = reinterpret_cast<const uint4*>(p.dtab)[(rank * p.kc + cg) * 2 + 1];
+  const uint32_t ob = d0.x, oe = d0.y, ib = d0.z, xb = d1.x;
+  const uint32_t nb_ops = (oe - ob) * uint32_t(sizeof(DevOp)), nb_ins = (d0.w - ib) * uint32_t(sizeof(DevIn));
+  const uint32_t nb_all = nb_ops + nb_ins + (d1.y - xb) * uint32_t(sizeof(DevOut));
+  const bool cached = nb_all <= uint32_t(kDescCache) && p.dcache_min_ops && oe - ob >= uint32_t(p.dcache_min_ops);
+  if (cached)  // every thread copies 16-byte words; the three ranges load in parallel
+    for (uint32_t w = tid; w < nb_all / 16; w += NT) {
+      const uint32_t o = w * 16;
+      const uint4* src = o < nb_ops ? reinterpret_cast<const uint4*>(p.ops + ob) + w
+                         : o < nb_ops + nb_ins ? reinterpret_cast<const uint4*>(p.ins + ib) + (o - nb_ops) / 16
+                                               : reinterpret_cast<const uint4*>(p.outs + xb) + (o - nb_ops - nb_ins) / 16;
+      reinterpret_cast<uint4*>(S.dcache)[w] = *src;
+    }
+  // indexed like p.ops / p.ins / p.outs (biased by this CTA's range
+  // starts); kept in shared memory, not in registers (80 per thread)
+  __shared__ const DevOp* OPS;
+  __shared__ const DevIn* INS;
+  __shared__ const DevOut* OUTS;
+  if (tid == 0) {
+    OPS = (cached ? reinterpret_cast<const DevOp*>(S.dcache) : p.ops + ob) - ob;
+    INS = (cached ? reinterpret_cast<const DevIn*>(S.dcache + nb_ops) : p.ins + ib) - ib;
+    OUTS = (cached ? reinterpret_cast<const DevOut*>(S.dcache + nb_ops + nb_ins) : p.outs + xb) - xb;
+  }
   __syncthreads();
   if (tid == 0) trace_ev(p, &S.trace_n, TR_START, 0, 0);
   const uint64_t e = s_e;
@@ -513,7 +542,6 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[t][SP_FLAGS_IDX]) + p.entry_base + rank * p.nch + ch, e);
       }
 
-  const uint32_t ob = p.prog[rank * p.kc + cg], oe = p.prog[rank * p.kc + cg + 1];
   uint32_t it = 0;  // tile number (same sequence in every role)
   const uint32_t my_stage_class = uint32_t(warp - 1);  // storer warps
   // bit s = parity of stage s's next phase of a barrier that only some uses
@@ -549,11 +577,11 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   if (warp != SIGW) {
     for (uint32_t w = 0; w < nwin; ++w)
     for (uint32_t oi = ob; oi < oe; ++oi) {
-      const DevOp op = p.ops[oi];
+      const DevOp op = OPS[oi];
       if (op.kind == 2) {  // end-of-program waits (after the last window): every receipt has landed
         if (warp == 0 && w + 1 == nwin)
           for (int i = lane; i < op.nin; i += 32) {
-            const DevIn in = p.ins[op.in_begin + i];
+            const DevIn in = INS[op.in_begin + i];
             if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
             const DPart q = dsplit16m(int64_t(in.len), p.kb, p.kb_magic, cb);
             if (q.len) wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, e * uint64_t(q.len), p, rank, ch,
@@ -573,14 +601,14 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         const int ptid = tid < 32 * SIGW ? tid : tid - 32;
         named_sync(1);
         if (tid < op.nin) {
-          const DevIn in = p.ins[op.in_begin + tid];
+          const DevIn in = INS[op.in_begin + tid];
           s_inp[tid] = p.base[in.rank][in.space] + in.off;
           if (in.flag >= 0)
             wait_ge<SYS>(myflags + uint64_t(in.flag) * p.nch + ch, fbase + uint64_t(q.len), p, rank, ch,
                          int(oi - ob), in.flag);
         }
         if (tid < op.nout) {
-          const DevOut d = p.outs[op.out_begin + tid];
+          const DevOut d = OUTS[op.out_begin + tid];
           s_outp[tid] = p.base[d.rank][d.space] + d.off;
           if (p.multiprocess && d.rank != rank) await_entry(d.rank, int(oi - ob));
         }
@@ -591,7 +619,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         if (tid == 32) {
           fence_rel<SYS>();
           for (int o = 0; o < op.nout; ++o) {
-            const DevOut d = p.outs[op.out_begin + o];
+            const DevOut d = OUTS[op.out_begin + o];
             if (d.flag >= 0)
               st_relaxed<SYS>(reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch,
                               fbase + uint64_t(q.len));
@@ -612,7 +640,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         int32_t flag = -1;
         bool dead_after = false;  // a scratch receipt: consumed by this read
         if (lane < op.nin) {
-          const DevIn in = p.ins[op.in_begin + lane];
+          const DevIn in = INS[op.in_begin + lane];
           src = p.base[in.rank][in.space] + in.off + q.off;
           flag = in.flag;
           dead_after = p.discard && in.dead_after;
@@ -681,7 +709,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         uint64_t* sig = nullptr;  // output `lane`'s counter at its destination, if it has one
         bool every = false;
         if (lane < op.nout) {
-          const DevOut d = p.outs[op.out_begin + lane];
+          const DevOut d = OUTS[op.out_begin + lane];
           outp = p.base[d.rank][d.space] + d.off + q.off;
           if (d.flag >= 0) {
             sig = reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) + uint64_t(d.flag) * p.nch + ch;
@@ -709,11 +737,11 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             const char* in[kMaxOpIn];
             char* out[kMaxOpOut];
             for (int k = 0; k < op.nin; ++k) {
-              const DevIn x = p.ins[op.in_begin + k];
+              const DevIn x = INS[op.in_begin + k];
               in[k] = p.base[x.rank][x.space] + x.off + q.off;
             }
             for (int o = 0; o < op.nout; ++o) {
-              const DevOut d = p.outs[op.out_begin + o];
+              const DevOut d = OUTS[op.out_begin + o];
               out[o] = p.base[d.rank][d.space] + d.off + q.off;
             }
             if (op.kind == 0) elem_op<0>(in, 1, out, op.nout, int64_t(lo + nv), n - nv, 0, 1);
@@ -773,14 +801,14 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           ++nw;
         }
         if (oi >= oe) continue;
-        const DevOp op = p.ops[oi];
+        const DevOp op = OPS[oi];
         DPart q;
         uint64_t wlo, whi;
         if (!op.vec || !item(op, w, q, wlo, whi)) continue;
         SigOp& x = S.win[wt % SIGWIN];
         bool every = false;
         if (lane < op.nout) {
-          const DevOut d = p.outs[op.out_begin + lane];
+          const DevOut d = OUTS[op.out_begin + lane];
           x.sig[lane] = d.flag >= 0 ? reinterpret_cast<uint64_t*>(p.base[d.rank][SP_FLAGS_IDX]) +
                                           uint64_t(d.flag) * p.nch + ch
                                     : nullptr;

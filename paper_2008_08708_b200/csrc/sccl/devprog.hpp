@@ -16,7 +16,7 @@ constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
 constexpr int kL2RelayPlain = 2;  // KParams::l2hint: re-read receipts stored with the default L2 policy
 constexpr int kStageBudget = 196608;  // bytes of stages per CTA (nstage * tile)
 constexpr int kThreads = 352;   // producer, kStorerWarps storer warps, signaler + 6 compute warps
-constexpr int kSmemHdr = 8192;  // simple kernel: shared-memory header (barriers, rings, signaler window) ahead of the stages
+constexpr int kSmemHdr = 16384;  // simple kernel: shared-memory header (barriers, rings, signaler window) ahead of the stages
 constexpr int kStorerWarps = 3; // simple protocol: stage s is stored by warp 1 + s % 3 (nstage % 3 == 0)
 constexpr int kLLThreads = 256; // LL kernel
 constexpr int64_t kLLPart = 4096;       // LL: bytes of a chunk one CTA owns
@@ -58,6 +58,8 @@ struct KParams {
   const DevIn* ins;
   const DevOut* outs;
   const uint32_t* prog;  // [P*kc+1] op ranges per (rank, chunk group)
+  const uint32_t* dtab;  // [P*kc][8]: op begin, op end, in begin, in end, out begin, out end, 0, 0
+  int dcache_min_ops;    // cache a CTA's descriptors in shared memory from this many ops up (0 = never)
   uint64_t* epochs;      // [nranks_launch * nch] per-CTA launch counters
   int* errinfo;          // host-mapped watchdog record
   long long timeout_ns;

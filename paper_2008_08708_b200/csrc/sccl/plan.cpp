@@ -378,6 +378,16 @@ void encode_program(sccl_plan& p) {
       }
     }
   p.prog[size_t(P) * p.kc] = uint32_t(p.ops.size());
+  // per (rank, chunk group): its contiguous op / in / out descriptor ranges
+  // (the simple kernel copies them into shared memory in its prologue)
+  p.dtab.assign(size_t(P) * p.kc * 8, 0);
+  for (size_t g = 0; g < size_t(P) * p.kc; ++g) {
+    const uint32_t b = p.prog[g], e = p.prog[g + 1];
+    uint32_t* t = &p.dtab[g * 8];
+    t[0] = b, t[1] = e;
+    t[2] = b < e ? p.ops[b].in_begin : 0, t[3] = b < e ? p.ops[e - 1].in_begin + p.ops[e - 1].nin : 0;
+    t[4] = b < e ? p.ops[b].out_begin : 0, t[5] = b < e ? p.ops[e - 1].out_begin + p.ops[e - 1].nout : 0;
+  }
 }
 
 // Streaming policies (launches over kStreamBytes):
@@ -426,6 +436,8 @@ void choose_streaming(sccl_plan& p, const ProgramStats& st, bool loopback) {
   p.discard = p.l2hint && st.max_fanin >= 4;
   if (const char* env = std::getenv("SCCL_DISCARD")) p.discard = std::atoi(env) != 0 && !p.ll;
   if (p.l2hint && !p.discard && !hint_env) p.l2hint |= kL2RelayPlain;
+  p.dcache_min_ops = 4;  // SCCL_DCACHE=<n> overrides (0 = off)
+  if (const char* env = std::getenv("SCCL_DCACHE")) p.dcache_min_ops = std::max(0, std::atoi(env));
   // windows of each launched CTA's program
   const int nl = loopback ? p.sched.P : 1;
   p.nwin.assign(size_t(nl) * p.nch, 1u);
@@ -505,6 +517,7 @@ void plan_device_setup(sccl_plan& p) {
   upload(p.ins, &p.d_ins);
   upload(p.outs, &p.d_outs);
   upload(p.prog, &p.d_prog);
+  upload(p.dtab, &p.d_dtab);
   upload(p.nwin, &p.d_nwin);
   int nlaunch = p.loopback ? p.nranks : 1;
   size_t ne = size_t(nlaunch) * p.nch;
@@ -561,6 +574,8 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.ins = p.d_ins;
   k.outs = p.d_outs;
   k.prog = p.d_prog;
+  k.dtab = p.d_dtab;
+  k.dcache_min_ops = p.dcache_min_ops;
   k.window = p.window;
   k.l2hint = p.l2hint;
   k.discard = p.discard ? 1 : 0;
@@ -979,6 +994,7 @@ int sccl_plan_destroy(sccl_plan* p) {
     cudaFree(p->d_ins);
     cudaFree(p->d_outs);
     cudaFree(p->d_prog);
+    cudaFree(p->d_dtab);
     cudaFree(p->d_nwin);
     cudaFree(p->d_epochs);
     if (p->vmm) {

@@ -28,6 +28,8 @@ struct sccl_plan {
   std::vector<sccl::DevIn> ins;
   std::vector<sccl::DevOut> outs;
   std::vector<uint32_t> prog;  // [P*kc+1]: op range per (rank, chunk group)
+  int dcache_min_ops = 4;      // simple kernel: descriptors cached in smem from this many ops per CTA
+  std::vector<uint32_t> dtab;  // [P*kc][8]: op / in / out ranges per (rank, chunk group)
   uint32_t window = 0;         // simple protocol: window-major byte window (0 = op-major)
   int l2hint = 0;              // L2 eviction hints on bulk copies (bit 0; bits 1-2: experiments)
   bool discard = false;        // drop consumed scratch receipts of reduce tiles from L2
@@ -38,6 +40,7 @@ struct sccl_plan {
   sccl::DevIn* d_ins = nullptr;
   sccl::DevOut* d_outs = nullptr;
   uint32_t* d_prog = nullptr;
+  uint32_t* d_dtab = nullptr;
   uint32_t* d_nwin = nullptr;
   uint64_t* d_epochs = nullptr;
 
