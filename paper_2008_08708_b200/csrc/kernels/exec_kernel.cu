@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   const uint32_t W = p.window;
   const uint32_t nwin = s_nwin;
   auto item = [&](const DevOp& op, uint32_t w, DPart& q, uint64_t& wlo, uint64_t& whi) -> bool {
-    if (op.kind == 2 || int(op.chunk % uint32_t(p.kc)) != cg) return false;
+    if (op.kind == 2) return false;  // (a CTA's program holds only its chunk group's ops)
     q = dsplit16m(int64_t(op.len), p.kb, p.kb_magic, cb);
     if (q.len == 0) return false;  // empty sub-range: nothing sent, nothing awaited
     wlo = W ? uint64_t(w) * W : 0;
@@ -574,7 +574,10 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
     return true;
   };
 
+  // copy-only aligned programs: the compute warps go straight to the final
+  // barrier instead of walking the program (they would only take issue slots)
   if (warp != SIGW) {
+    if (!(warp >= CW0 && d1.z))
     for (uint32_t w = 0; w < nwin; ++w)
     for (uint32_t oi = ob; oi < oe; ++oi) {
       const DevOp op = OPS[oi];

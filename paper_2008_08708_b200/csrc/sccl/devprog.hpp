@@ -58,7 +58,7 @@ struct KParams {
   const DevIn* ins;
   const DevOut* outs;
   const uint32_t* prog;  // [P*kc+1] op ranges per (rank, chunk group)
-  const uint32_t* dtab;  // [P*kc][8]: op begin, op end, in begin, in end, out begin, out end, 0, 0
+  const uint32_t* dtab;  // [P*kc][8]: op begin, op end, in begin, in end, out begin, out end, compute idle, 0
   int dcache_min_ops;    // cache a CTA's descriptors in shared memory from this many ops up (0 = never)
   uint64_t* epochs;      // [nranks_launch * nch] per-CTA launch counters
   int* errinfo;          // host-mapped watchdog record

@@ -387,6 +387,9 @@ void encode_program(sccl_plan& p) {
     t[0] = b, t[1] = e;
     t[2] = b < e ? p.ops[b].in_begin : 0, t[3] = b < e ? p.ops[e - 1].in_begin + p.ops[e - 1].nin : 0;
     t[4] = b < e ? p.ops[b].out_begin : 0, t[5] = b < e ? p.ops[e - 1].out_begin + p.ops[e - 1].nout : 0;
+    bool idle = true;  // t[6]: the compute warps have nothing to do (no REDUCE, no unaligned op)
+    for (uint32_t o = b; o < e; ++o) idle &= p.ops[o].kind == OP_WAIT || (p.ops[o].kind == OP_COPY && p.ops[o].vec);
+    t[6] = idle ? 1 : 0;
   }
 }
 
