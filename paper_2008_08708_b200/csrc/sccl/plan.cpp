@@ -73,15 +73,16 @@ int esize_of(int dtype) {
 
 // predicted time (us) of a lowered program, see plan_build_host.  sys:
 // system-scope signalling (multi-process mode), whose release fences make
-// every bulk-protocol step ~1.7 us dearer (fit with SCCL_LOOPBACK_SYS=1).
+// every bulk-protocol step ~3.6 us dearer (fit with SCCL_LOOPBACK_SYS=1).
 double predict_us(const sccl::Program& pg, int steps, bool ll, bool sys = false) {
   double mb = 0;
   for (auto& rp : pg.ranks)
     for (auto& op : rp.ops)
       if (op.kind != sccl::OP_WAIT) mb += double(op.len) * double(op.ins.size() + op.outs.size());
   mb /= 1e6;
-  if (ll) return sys ? 5.10 + 0.562 * steps + 0.408 * mb : 4.80 + 0.544 * steps + 0.410 * mb;
-  return sys ? 4.31 + 4.28 * steps + 0.156 * mb : 4.26 + 2.61 * steps + 0.143 * mb;
+  // tools/fit_protocol.py over tools/gpu_runs/proto_refit_round1w.sh
+  if (ll) return sys ? 4.79 + 0.520 * steps + 0.353 * mb : 4.80 + 0.522 * steps + 0.353 * mb;
+  return sys ? 5.00 + 6.33 * steps + 0.163 * mb : 4.50 + 2.72 * steps + 0.126 * mb;
 }
 
 bool loopback_sys() {  // SCCL_LOOPBACK_SYS=1: loopback launches use system scope (measurement only)
