@@ -435,8 +435,11 @@ def _reduce_py(dtype: int, acc: Optional[np.ndarray], ins: List[np.ndarray]) -> 
         return a.view(np.uint8)
     if dtype == F32:
         a = acc.view(np.float32).copy() if acc is not None else vals[0].copy()
-        for v in (vals if acc is not None else vals[1:]):
-            a = (a + v).astype(np.float32)
+        with np.errstate(invalid="ignore", over="ignore"):
+            for v in (vals if acc is not None else vals[1:]):
+                a = (a + v).astype(np.float32)
+        a = a.view(np.uint32)
+        a[np.isnan(a.view(np.float32))] = 0x7FFFFFFF  # canonical NaN, as GPU arithmetic returns it
         return a.view(np.uint8)
     # bf16 / f16: widen to f32, add in order, round once
     def widen(x):
@@ -444,14 +447,18 @@ def _reduce_py(dtype: int, acc: Optional[np.ndarray], ins: List[np.ndarray]) -> 
             return (x.astype(np.uint32) << 16).view(np.float32)
         return x.astype(np.float32)
     a = widen(acc.view(dt)) if acc is not None else widen(vals[0])
-    for v in (vals if acc is not None else vals[1:]):
-        a = (a + widen(v)).astype(np.float32)
+    with np.errstate(invalid="ignore", over="ignore"):
+        for v in (vals if acc is not None else vals[1:]):
+            a = (a + widen(v)).astype(np.float32)
     if dtype == BF16:
         u = a.view(np.uint32).astype(np.uint64)
         r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
         r[np.isnan(a)] = 0x7FFF
         return r.view(np.uint8)
-    return a.astype(np.float16).view(np.uint8)
+    with np.errstate(invalid="ignore", over="ignore"):
+        r = a.astype(np.float16).view(np.uint16)
+    r[np.isnan(a)] = 0x7FFF  # canonical NaN (PTX cvt)
+    return r.view(np.uint8)
 
 
 def execute_py(sched: dict, inputs: Sequence[np.ndarray], nbytes: int, dtype: int = U8):
@@ -512,14 +519,18 @@ def seeded_inputs(kind: str, P: int, nbytes: int, dtype: int, seed: int,
                   mode: str = "random") -> List[np.ndarray]:
     """Deterministic per-rank input buffers (bytes).  mode 'random' = uniform
     bytes (u8), uniform [-1,1) floats, or full-range ints; 'smallint' =
-    integers in [-16,16] (exact under any summation order)."""
+    integers in [-16,16] (exact under any summation order); 'bits' = uniform
+    bit patterns for the float types (special values included)."""
     sb, _ = buffer_sizes(kind, P, nbytes)
     es = ESIZE[dtype]
     out = []
     for r in range(P):
         rng = np.random.default_rng([seed, r])
         n = sb // es
-        if mode == "smallint":
+        if mode == "bits" and dtype in (F16, BF16, F32):
+            # every bit pattern: subnormals, infinities, NaNs, the largest finite values
+            arr = rng.integers(0, 2**(8 * es), size=n, dtype=np.uint64).astype({2: np.uint16, 4: np.uint32}[es])
+        elif mode == "smallint":
             v = rng.integers(-16, 17, size=n)
             arr = {U8: v.astype(np.uint8), I32: v.astype(np.int32), F32: v.astype(np.float32),
                    F16: v.astype(np.float16),

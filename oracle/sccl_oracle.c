@@ -287,6 +287,10 @@ static void reduce_elems(int dtype, int64_t n, const uint8_t* base,
           memcpy(&b, ins[k] + 4 * i, 4);
           a = a + b;
         }
+        if (a != a) { /* canonical NaN, as GPU arithmetic returns it */
+          const uint32_t q = 0x7fffffffu;
+          memcpy(&a, &q, 4);
+        }
         memcpy(out + 4 * i, &a, 4);
       }
       break;
@@ -313,6 +317,10 @@ static void reduce_elems(int dtype, int64_t n, const uint8_t* base,
           a = a + (float)h;
         }
         h = (_Float16)a;
+        if (a != a) { /* canonical NaN (PTX cvt) */
+          const uint16_t q = 0x7fff;
+          memcpy(&h, &q, 2);
+        }
         memcpy(out + 2 * i, &h, 2);
       }
       break;

@@ -300,6 +300,24 @@ struct Vec<1> {  // i32, two's-complement wrap
   }
   __device__ uint4 out() const { return a; }
 };
+// Two bf16 / f16 inputs: widening both to f32, adding and rounding once
+// equals the correctly rounded 16-bit add (the f32 sum of two such values is
+// exact unless their exponents differ by more than the f32/16-bit precision
+// gap, and then it cannot land on a 16-bit rounding tie), so one packed
+// add.rn per two elements gives the Vec<DT> result bit for bit (NaNs come out
+// canonical, 0x7fff, as in Vec<DT>::out).
+template <int DT>
+__device__ __forceinline__ uint32_t add_pair_w(uint32_t a, uint32_t b) {
+  uint32_t d;
+  if constexpr (DT == 3) asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  else asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+template <int DT>
+__device__ __forceinline__ uint4 add_pair(uint4 a, uint4 b) {
+  return make_uint4(add_pair_w<DT>(a.x, b.x), add_pair_w<DT>(a.y, b.y), add_pair_w<DT>(a.z, b.z),
+                    add_pair_w<DT>(a.w, b.w));
+}
 template <>
 struct Vec<2> {  // f32, adds in input order
   float a[4];
@@ -689,6 +707,10 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             const uint64_t lo = wlo + uint64_t(t) * T;
             const uint32_t nv = uint32_t(min(uint64_t(T), whi - lo)) >> 4;
             uint4* b0 = reinterpret_cast<uint4*>(bufs + size_t(s) * STAGE);
+            if ((DT == 3 || DT == 4) && op.nin == 2) {  // bf16 / f16 pair: one packed add per 2 elements
+              const uint4* b1 = reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(T));
+              for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) b0[v] = add_pair<DT>(b0[v], b1[v]);
+            } else
             for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
               Vec<DT> acc;
               acc.init(b0[v]);

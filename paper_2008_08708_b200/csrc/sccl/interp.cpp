@@ -32,6 +32,12 @@ inline uint16_t f2bf16(float f) {
   u += 0x7fffu + ((u >> 16) & 1u);
   return uint16_t(u >> 16);
 }
+inline float canon_nan_f32() {
+  const uint32_t u = 0x7fffffffu;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
 
 void elem_range(int dtype, const char* const* in, int nin, char* const* out, int nout, int64_t off, int64_t nbytes) {
   const int es = dtype == 0 ? 1 : (dtype == 3 || dtype == 4) ? 2 : 4;
@@ -58,6 +64,7 @@ void elem_range(int dtype, const char* const* in, int nin, char* const* out, int
         std::memcpy(&x, in[k] + b, 4);
         a = a + x;
       }
+      if (a != a) a = canon_nan_f32();  // canonical NaN (GPU arithmetic)
       std::memcpy(tmp, &a, 4);
     } else if (dtype == 3) {
       uint16_t h;
@@ -78,7 +85,10 @@ void elem_range(int dtype, const char* const* in, int nin, char* const* out, int
         a = a + float(h);
       }
       h = _Float16(a);
-      std::memcpy(tmp, &h, 2);
+      uint16_t u;
+      std::memcpy(&u, &h, 2);
+      if (a != a) u = 0x7fff;  // canonical NaN (PTX cvt)
+      std::memcpy(tmp, &u, 2);
     }
     for (int o = 0; o < nout; ++o) std::memcpy(out[o] + b, tmp, es);
   }

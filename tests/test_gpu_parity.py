@@ -116,6 +116,18 @@ def test_channels_and_tiles(name, nch, tile):
     run_gpu(js, 3 * 65536 + 1024, dt, nch=nch, tile=tile)
 
 
+@pytest.mark.parametrize("dt", [O.BF16, O.F16, O.F32])
+@pytest.mark.parametrize("name,nbytes", [("ar_ring", 1 << 20), ("ar_56_14_14", 1 << 20), ("ar_822", 1 << 20),
+                                         ("rs_ring8", 1 << 18)])
+@pytest.mark.parametrize("protocol", ["simple", "ll"])
+def test_reduce_special_values(name, nbytes, dt, protocol):
+    """Float reductions over uniformly random bit patterns (subnormals,
+    infinities, NaNs, overflow to infinity): bit-exact with the oracle's
+    widen / add in order / round once / canonical NaN rule, for 2-input
+    chain reduces and wide one-shot reduces."""
+    run_gpu(SCHED[name], nbytes, dt, mode="bits", protocol=protocol, repeats=2)
+
+
 def test_back_to_back_launches_advance_epochs():
     run_gpu(SCHED["ar_56_14_14"], 1 << 18, O.F32, repeats=5)
     run_gpu(SCHED["ag_777"], 1 << 18, O.U8, repeats=5, tile=4096)

@@ -56,6 +56,20 @@ def test_interpreter_matches_oracle(name, nbytes):
         run_interp(js, nbytes, dt, nch=2, tile=256)
 
 
+@pytest.mark.parametrize("name", ["ar_b4", "ar_ring", "ar_ham", "rs_ring", "reduce"])
+@pytest.mark.parametrize("dt", [O.F32, O.BF16, O.F16])
+def test_special_values_all_restatements(name, dt):
+    """Uniformly random bit patterns (NaN, inf, subnormals, overflow): the
+    C oracle, the pure-Python oracle and the host interpreter agree bit for
+    bit (canonical NaN rule of DESIGN.md section 2)."""
+    js = CASES[name]
+    d = json.loads(js)
+    ins = O.seeded_inputs(d["collective"], d["P"], 4096, dt, 11, "bits")
+    a, b = O.execute(d, ins, 4096, dt), O.execute_py(d, ins, 4096, dt)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    run_interp(js, 4096, dt, nch=2, tile=256, seed=11, mode="bits")
+
+
 @pytest.mark.parametrize("nch,tile", [(1, 256), (3, 272), (5, 4096)])
 def test_interpreter_channels_tiles(nch, tile):
     for name in ("ham8", "ar_ham", "rs_ring", "a2a_k2"):
