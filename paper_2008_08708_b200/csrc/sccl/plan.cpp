@@ -222,14 +222,18 @@ bool choose_ll(sccl_plan& p, int64_t bytes, int es, int protocol, bool loopback)
 // >= 4) that fit L2: 3 x 64 KiB at 1 CTA/SM (8 KiB per input at fan-in 8);
 // streaming ones run window-major with receipt discards and do better at
 // 2 CTAs/SM with 3 x 32 KiB (AR (8,2,2) 64 MiB 298 -> 280 us, 256 MiB
-// 1109 -> 1081 us).  Small chunks: the smallest power of two that holds
-// one.  Stages come in multiples of the storer-warp count (each storer warp
-// owns the stages s with s % kStorerWarps == its index): 3 or 6.
+// 1109 -> 1081 us); with chunks up to 256 KiB they use 16 KiB tiles.
+// Small chunks: the smallest power of two that holds one.  Stages come in
+// multiples of the storer-warp count (each storer warp owns the stages s
+// with s % kStorerWarps == its index): 3 or 6.
 void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const ChannelRequest& req) {
   const bool wide = st.max_fanin >= 4 && !(st.bytes > kStreamBytes && !p.ll);
   int tile = req.tile;
   if (tile <= 0) {
-    tile = wide ? kMaxTile : 32768;
+    // wide reductions with small chunks: 16 KiB tiles (6 stages, 2 CTAs/SM)
+    // put twice the CTAs on the chunks (AR (8,2,2) 512 KiB-2 MiB per rank:
+    // -13..-26 %, tools/gpu_runs/midtile2_round1w.sh)
+    tile = wide ? (maxlen <= (256 << 10) ? 16384 : kMaxTile) : 32768;
     if (maxlen < tile) {
       tile = 1024;
       while (tile < maxlen) tile *= 2;
