@@ -234,6 +234,10 @@ void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const C
     // put twice the CTAs on the chunks (AR (8,2,2) 512 KiB-2 MiB per rank:
     // -13..-26 %, tools/gpu_runs/midtile2_round1w.sh)
     tile = wide ? (maxlen <= (256 << 10) ? 16384 : kMaxTile) : 32768;
+    // one-shot copies (one fan-out op per rank, nothing re-read) up to
+    // 512 KiB: two 16 KiB tiles per CTA overlap the load of one with the
+    // stores of the other (AG (1,1,1) 256 / 512 KiB: -27 / -16 %)
+    if (!st.rereads && !st.reduces && st.nops_rank0 <= 2 && maxlen <= (512 << 10)) tile = 16384;
     if (maxlen < tile) {
       tile = 1024;
       while (tile < maxlen) tile *= 2;
