@@ -25,7 +25,7 @@ struct DevIn {
   uint64_t off;   // byte offset of the chunk start in (rank, space)
   uint64_t len;   // chunk length (used by WAIT ops; equal to op len otherwise)
   int32_t flag;   // receipt slot at the executing rank, -1 = none
-  uint32_t chunk; // chunk id (WAIT ops filter by chunk group)
+  uint32_t chunk; // chunk group of the chunk (WAIT ops filter by it)
   uint8_t rank, space;
   uint8_t dead_after;  // a scratch receipt this op is the only reader of (its bytes are dead once read)
   uint8_t pad1;
@@ -40,7 +40,7 @@ struct DevOut {
 
 struct DevOp {
   uint64_t len;   // chunk length in bytes
-  uint32_t chunk; // chunk id: CTA channel (g, b) runs ops with chunk % kc == g
+  uint32_t chunk; // chunk group of the op's chunk: CTA channel (g, b) runs ops with chunk % kc == g
   uint32_t pad2;
   uint32_t in_begin, out_begin;
   uint16_t nin, nout;

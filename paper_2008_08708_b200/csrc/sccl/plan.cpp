@@ -290,6 +290,70 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
   p.resident_cap = loopback ? resident : 0;
 }
 
+// Chunk groups: every rank's CTA (rank, channel) runs the ops of the chunks
+// in its group, and a chunk's group must be the same at every rank (its
+// receipt counters are per channel).  `chunk % kc` put all of a rank's
+// alltoall chunks (ids i*P + rank) into one group whenever kc divided P;
+// such plans assign chunks greedily, largest first, to the group that keeps
+// the busiest (rank, group) lightest (A2A 4 MiB per rank: 17.7 -> 12.8 us).
+// The modulo map stays unless it loads some (rank, group) 25 % above the
+// mean and the greedy map is 3 % better: the (7,7,7) allgather at 128 MiB
+// (modulo 1.09x the mean, greedy 1.03x) ran 1.3 % slower greedy -- it is
+// HBM-bound, and the modulo order is the one its L2 reuse was tuned on
+// (tools/gpu_runs/groups_ab_round1w.sh, groups2_ab_round1w.sh).
+void assign_groups(sccl_plan& p) {
+  const int P = int(p.pg.ranks.size());
+  int maxc = 0;
+  for (auto& rp : p.pg.ranks)
+    for (auto& op : rp.ops) {
+      maxc = std::max(maxc, op.chunk);
+      for (auto& in : op.ins) maxc = std::max(maxc, in.chunk);
+    }
+  p.group_of.assign(size_t(maxc) + 1, 0);
+  for (int c = 0; c <= maxc; ++c) p.group_of[size_t(c)] = c % p.kc;
+  if (p.kc == 1) return;
+  std::vector<double> w(size_t(maxc + 1) * P, 0.0);  // [chunk][rank] bytes moved
+  for (int r = 0; r < P; ++r)
+    for (auto& op : p.pg.ranks[size_t(r)].ops)
+      if (op.kind != OP_WAIT)
+        w[size_t(std::max(0, op.chunk)) * P + r] += double(op.len) * double(op.ins.size() + op.outs.size());
+  std::vector<int> order(size_t(maxc) + 1);
+  for (int c = 0; c <= maxc; ++c) order[size_t(c)] = c;
+  auto peak = [&](int c) { return *std::max_element(w.begin() + size_t(c) * P, w.begin() + size_t(c + 1) * P); };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return peak(a) > peak(b); });
+  std::vector<double> load(size_t(p.kc) * P, 0.0);  // [group][rank]
+  for (int c = 0; c <= maxc; ++c)
+    for (int r = 0; r < P; ++r) load[size_t(c % p.kc) * P + r] += w[size_t(c) * P + r];
+  const double modulo_max = *std::max_element(load.begin(), load.end());
+  std::fill(load.begin(), load.end(), 0.0);
+  std::vector<int> greedy(p.group_of);
+  for (int c : order) {
+    if (peak(c) <= 0) continue;  // no work (WAIT-only chunk ids keep c % kc)
+    int best = 0;
+    double best_max = 0, best_sum = 0;
+    for (int g = 0; g < p.kc; ++g) {
+      double mx = 0, sum = 0;
+      for (int r = 0; r < P; ++r) {
+        mx = std::max(mx, load[size_t(g) * P + r] + w[size_t(c) * P + r]);
+        sum += load[size_t(g) * P + r];
+      }
+      if (g == 0 || mx < best_max || (mx == best_max && sum < best_sum)) best = g, best_max = mx, best_sum = sum;
+    }
+    greedy[size_t(c)] = best;
+    for (int r = 0; r < P; ++r) load[size_t(best) * P + r] += w[size_t(c) * P + r];
+  }
+  double total = 0;
+  for (double x : w) total += x;
+  const double mean = total / double(size_t(p.kc) * P);
+  p.groups_balanced = modulo_max > 1.25 * mean && *std::max_element(load.begin(), load.end()) < 0.97 * modulo_max;
+  if (p.groups_balanced) p.group_of = std::move(greedy);
+}
+
+int group_of(const sccl_plan& p, int chunk) {
+  const int c = std::max(0, chunk);
+  return size_t(c) < p.group_of.size() ? p.group_of[size_t(c)] : c % p.kc;
+}
+
 // Counter release: latency-bound plans (<= 16 tiles per CTA) let each
 // storer warp release its own tile's counters (no hand-off, ~0.3 us less
 // per hop); longer ones keep the fence off the store path in the signaler
@@ -302,7 +366,7 @@ void choose_release(sccl_plan& p, bool loopback) {
     for (int g = 0; g < p.kc; ++g) {
       int64_t n = 0;
       for (auto& op : rp.ops) {
-        if (op.kind == OP_WAIT || std::max(0, op.chunk) % p.kc != g) continue;
+        if (op.kind == OP_WAIT || group_of(p, op.chunk) != g) continue;
         const int64_t part = split16(op.len, p.kb, p.kb - 1).len;  // the last part is the longest
         const int64_t T = op.kind == OP_COPY ? p.tile : std::max<int64_t>(16, (p.tile / int64_t(op.ins.size())) & ~int64_t(15));
         n += (part + T - 1) / T;
@@ -337,7 +401,7 @@ void encode_program(sccl_plan& p) {
       throw invalid_argument_error("op fan-in/fan-out exceeds executor limits (32)");
     DevOp d{};
     d.len = uint64_t(op.len);
-    d.chunk = uint32_t(std::max(0, op.chunk));
+    d.chunk = uint32_t(group_of(p, op.chunk));  // the kernel only needs chunk % kc
     d.kind = uint8_t(op.kind);
     d.in_begin = uint32_t(p.ins.size());
     d.out_begin = uint32_t(p.outs.size());
@@ -350,7 +414,7 @@ void encode_program(sccl_plan& p) {
       x.off = uint64_t(in.loc.off);
       x.len = uint64_t(in.len);
       x.flag = in.flag;
-      x.chunk = uint32_t(std::max(0, in.chunk));
+      x.chunk = uint32_t(group_of(p, in.chunk));
       x.rank = uint8_t(in.loc.rank);
       x.space = uint8_t(in.loc.space);
       x.dead_after = op.kind != OP_WAIT && in.flag >= 0 && in.loc.space == SP_SCRATCH &&
@@ -379,9 +443,9 @@ void encode_program(sccl_plan& p) {
         if (op.kind == OP_WAIT) {
           std::vector<OpIn> mine;
           for (auto& in : op.ins)
-            if (std::max(0, in.chunk) % p.kc == cg) mine.push_back(in);
+            if (group_of(p, in.chunk) == cg) mine.push_back(in);
           if (!mine.empty()) encode(r, op, mine);
-        } else if (std::max(0, op.chunk) % p.kc == cg) {
+        } else if (group_of(p, op.chunk) == cg) {
           encode(r, op, op.ins);
         }
       }
@@ -506,6 +570,7 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   const ProgramStats st = program_stats(p.sched, p.pg, loopback);
   choose_stages(p, st, maxlen, req);
   choose_channels(p, st, maxlen, req, loopback);
+  assign_groups(p);
   choose_release(p, loopback);
   encode_program(p);
   choose_streaming(p, st, loopback);
@@ -976,7 +1041,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"groups_balanced\":" << (p->groups_balanced ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

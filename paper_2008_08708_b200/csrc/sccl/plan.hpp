@@ -29,6 +29,8 @@ struct sccl_plan {
   std::vector<sccl::DevOut> outs;
   std::vector<uint32_t> prog;  // [P*kc+1]: op range per (rank, chunk group)
   int dcache_min_ops = 4;      // simple kernel: descriptors cached in smem from this many ops per CTA
+  std::vector<int> group_of;    // chunk id -> chunk group (balanced over the ranks' work)
+  bool groups_balanced = false; // group_of is the greedy map, not chunk % kc
   std::vector<uint32_t> dtab;  // [P*kc][8]: op / in / out ranges per (rank, chunk group)
   uint32_t window = 0;         // simple protocol: window-major byte window (0 = op-major)
   int l2hint = 0;              // L2 eviction hints on bulk copies (bit 0; bits 1-2: experiments)

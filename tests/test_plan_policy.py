@@ -112,3 +112,10 @@ def test_multiprocess_plans_use_the_sys_scope_model():
     loop = last_ll(lambda sz: sccl.LoopbackPlan(js, sz, dt, device=-1))
     multi = last_ll(lambda sz: sccl.Plan(js, 0, P, sz, dt, device=-1))
     assert multi >= loop > 0
+
+
+def test_chunk_groups_balanced_only_when_modulo_is_lopsided():
+    # alltoall chunk ids are i*P + rank: with kc = 2 every rank's ops would
+    # share one group under chunk % kc
+    assert info("a2a", 4 << 20, protocol="simple")["groups_balanced"] == 1
+    assert info("ag777", 128 << 20, protocol="simple")["groups_balanced"] == 0  # within 25 % of the mean
