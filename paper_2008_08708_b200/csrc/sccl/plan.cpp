@@ -282,6 +282,15 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
       kc = 2;
       kb /= 2;
     }
+    // LL plans whose chunk groups are exhausted (kc = G) but leave CTAs
+    // idle: split the chunks further, down to 2 KiB per CTA, up to 64 CTAs
+    // per rank (a larger LL grid lost: (7,7,7) 16 KiB with 896 CTAs +29 %).
+    // AR (8,2,2) 64 / 128 KiB -28 / -26 %, one-shot AG 4-16 KiB -14..-16 %
+    // (tools/gpu_runs/llpart_round1w.sh, llgrow_round1w.sh).
+    if (p.ll && req.chunk_groups <= 0) {
+      const int grid_cap = loopback ? std::min(cap, 512 / std::max(1, p.sched.P)) : cap;
+      while (2 * kc * kb <= grid_cap && maxlen / (2 * kb) >= 2048) kb *= 2;
+    }
   }
   if (kc < 1 || kb < 1) throw invalid_argument_error("channels must be positive");
   p.kc = kc;
