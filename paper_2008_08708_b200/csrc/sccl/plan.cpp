@@ -282,6 +282,17 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
       kc = 2;
       kb /= 2;
     }
+    // LL relay / reduce chains (>= 4 steps) with many chunks (>= 32) of up
+    // to 40 KiB: one chunk per CTA (kc = G, kb = 1) instead of byte parts of
+    // several chunks, so each CTA forwards one chunk down its chain without
+    // queueing behind the others' hops: (7,7,7) 64-256 KiB -24..-31 %,
+    // (56,14,14) 256 KiB-2 MiB -6..-32 % (tools/gpu_runs/llgrid2_round1w.sh;
+    // at 75 KiB chunks the byte parts win again)
+    if (p.ll && req.chunk_groups <= 0 && st.rereads && st.steps >= 4 && p.pg.G >= 32 && p.pg.G <= cap &&
+        maxlen <= (40 << 10)) {
+      kc = p.pg.G;
+      kb = 1;
+    }
     // LL plans whose chunk groups are exhausted (kc = G) but leave CTAs
     // idle: split the chunks further, down to 2 KiB per CTA, up to 64 CTAs
     // per rank (a larger LL grid lost: (7,7,7) 16 KiB with 896 CTAs +29 %).
