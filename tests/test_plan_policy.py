@@ -119,3 +119,19 @@ def test_chunk_groups_balanced_only_when_modulo_is_lopsided():
     # share one group under chunk % kc
     assert info("a2a", 4 << 20, protocol="simple")["groups_balanced"] == 1
     assert info("ag777", 128 << 20, protocol="simple")["groups_balanced"] == 0  # within 25 % of the mean
+
+
+def test_ll_chains_run_one_chunk_per_cta():
+    # >= 4 steps, >= 32 chunks of <= 40 KiB: kc = G, kb = 1
+    i = info("ag777", 64 << 10, protocol="ll")
+    assert (i["chunk_groups"], i["byte_parts"]) == (56, 1)
+    i = info("ar56", 1 << 20, protocol="ll")
+    assert (i["chunk_groups"], i["byte_parts"]) == (56, 1)
+    # single-step alltoall keeps byte parts
+    assert info("a2a", 256 << 10, protocol="ll")["byte_parts"] > 1
+
+
+def test_ll_splits_chunks_when_groups_run_out():
+    # one-shot allreduce: 8 chunk groups only; 64 KiB -> 8 KiB chunks in 2 KiB parts
+    i = info("ar822", 64 << 10, protocol="ll")
+    assert (i["chunk_groups"], i["byte_parts"]) == (8, 4)
