@@ -43,6 +43,9 @@ else:  # multi-hop relays and combining trees through IPC-mapped peers
         (S.to_json(S.direct_alltoall(4)), 4096, O.U8, "ll"),
         (S.allreduce_from(S.ring_allgather(4)), 8192, O.BF16, "ll"),
         (S.to_json(S.ring_allgather(4)), 8 << 20, O.U8, "simple"),  # windowed signaler, sys scope
+        # chunk % kc would put each rank's alltoall chunks in one group: the
+        # balanced chunk-group map, computed independently in every process
+        (S.to_json(S.direct_alltoall(4)), 1 << 20, O.U8, "simple"),
         # window-major + L2 hints + receipt discards forced (sys scope)
         ("FORCE", S.allreduce_from(S.one_shot_allgather(4)), 4 << 20, O.BF16, "simple"),
     ]
@@ -95,4 +98,4 @@ def test_processes_one_gpu(tmp_path, world, mem):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
     text = "".join(o for o, _ in outs)
-    assert text.count("OK") == (5 if world == 2 else 6) * world, text
+    assert text.count("OK") == (5 if world == 2 else 7) * world, text
