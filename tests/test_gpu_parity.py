@@ -128,6 +128,21 @@ def test_reduce_special_values(name, nbytes, dt, protocol):
     run_gpu(SCHED[name], nbytes, dt, mode="bits", protocol=protocol, repeats=2)
 
 
+@pytest.mark.parametrize("name,nbytes,dt", [
+    ("ag_777", 256 << 10, O.U8),          # LL chain: one 37 KiB chunk per CTA
+    ("ar_56_14_14", 2 << 20, O.BF16),     # LL chain at its largest chunk (37 KiB)
+    ("ar_822", 128 << 10, O.BF16),        # LL: chunks split to 2 KiB parts when groups run out
+    ("ar_822", 1 << 20, O.BF16),          # bulk: wide reduce with 16 KiB tiles
+    ("ag_b4_oneshot8", 256 << 10, O.U8),  # bulk: one-shot copy with 16 KiB tiles
+    ("a2a_b5", 4 << 20, O.U8),            # balanced chunk-group map (chunk % kc is lopsided)
+    ("a2a_b5", 2 << 20, O.U8),
+])
+def test_plan_policy_cases(name, nbytes, dt):
+    """The size-dependent channel / tile rules, at the sizes that trigger
+    them, under the automatic protocol choice: bit-exact, twice in a row."""
+    run_gpu(SCHED[name], nbytes, dt, repeats=2)
+
+
 def test_back_to_back_launches_advance_epochs():
     run_gpu(SCHED["ar_56_14_14"], 1 << 18, O.F32, repeats=5)
     run_gpu(SCHED["ag_777"], 1 << 18, O.U8, repeats=5, tile=4096)
