@@ -160,7 +160,13 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded PRNG bytes)",
             "impl": "reference",
-            "config": {"workload": f"{sname}; CPU reference executor", "ranks": P, "bytes_per_rank": m,
+            # the GPU arm's workload (same schedule, ranks and bytes per rank); each
+            # step runs the CPU executor on a bounded sample of it (sample_bytes_per_rank)
+            "config": {"workload": (f"{sname}; {P} ranks loopback on 1 B200 (all rank buffers in one HBM)"
+                                    if args.gpus == 1 else
+                                    f"{sname}; one rank per GPU, CUDA IPC peers over NVLink"),
+                       "ranks": P, "bytes_per_rank": args.bytes, "schedule": sname,
+                       "sample_bytes_per_rank": m, "executor": "CPU reference (oracle port)",
                        "parallelism": f"{threads} host threads"},
             "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                              "sample": sample},
