@@ -282,6 +282,18 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
       kc = 2;
       kb /= 2;
     }
+    // LL: cap / kb rounding down can leave CTA slots idle (ring AG at
+    // 256 KiB: 1 x 64 of 111 per rank); take the chunk-group count that
+    // fills the most slots (fewest groups on ties) when that is 25 % more:
+    // ring / one-shot AG 256 KiB -22 / -9 % (tools/gpu_runs/llgrid4_round1w.sh)
+    if (p.ll && req.chunk_groups <= 0 && 4 * kc * kb < 3 * cap) {
+      int bc = kc, bb = kb;
+      for (int c = kc + 1; c <= std::min(p.pg.G, cap); ++c) {
+        const int b = std::min(kb, cap / c);
+        if (c * b > bc * bb) bc = c, bb = b;
+      }
+      if (4 * bc * bb >= 5 * kc * kb) kc = bc, kb = bb;
+    }
     // LL relay / reduce chains (>= 4 steps) with many chunks (>= 32) of up
     // to 40 KiB: one chunk per CTA (kc = G, kb = 1) instead of byte parts of
     // several chunks, so each CTA forwards one chunk down its chain without
