@@ -49,8 +49,13 @@ typedef struct {
   int chunk_groups;   /* chunk groups (independent chunks run on different CTAs); 0 = auto          */
   int tile_bytes;     /* pipeline stage / copy tile bytes, multiple of 16 in [256, 65536]; 0 = auto  */
   int protocol;       /* 0 = auto, 1 = simple (TMA bulk + counters), 2 = LL (flag in data)          */
-  int64_t timeout_ms; /* peer-wait watchdog; 0 = default (10 s), <0 = disabled                        */
+  int64_t timeout_ms; /* peer-wait watchdog; 0 = default (loopback 10 s, one rank per GPU 600 s),
+                         <0 = disabled.  Expiry: the launch aborts cooperatively (publishes nothing
+                         more, exits normally; the CUDA context stays usable), sccl_plan_check
+                         returns SCCL_PEER_TIMEOUT and the plan refuses further launches.       */
   int mem_handles;    /* multi-process region sharing: 0 = CUDA IPC handles, 1 = VMM (cuMem) POSIX FDs */
+  int pull;           /* combining sends of untouched inputs read in place by the receiver (no receipt
+                         slot): 0 = auto (loopback plans: on), 1 = on (loopback only), -1 = off        */
 } sccl_plan_opts;
 
 void sccl_plan_opts_init(sccl_plan_opts* o);
@@ -75,10 +80,13 @@ int sccl_schedule_compose_allreduce(const char* rs_json, const char* ag_json, ch
  * implementations"): lowers every candidate schedule (same collective and
  * P, e.g. a Pareto frontier) under both protocols for bytes_per_rank and
  * returns the candidate index and protocol (1 simple, 2 LL) with the
- * smallest predicted time under the fitted B200 model (
- * the same model protocol=auto uses).  predicted_us may be NULL. */
-int sccl_schedule_select(const char* const* schedule_jsons, int n, size_t bytes_per_rank, int dtype, int* index,
-                         int* protocol, double* predicted_us);
+ * smallest predicted time under the fitted B200 model.
+ * multiprocess = 0 prices a loopback plan (gpu-scope constants, pull
+ * lowering), 1 a one-rank-per-GPU plan (system-scope constants, push) --
+ * the same model and lowering protocol=auto uses for that kind of plan.
+ * predicted_us may be NULL. */
+int sccl_schedule_select(const char* const* schedule_jsons, int n, size_t bytes_per_rank, int dtype,
+                         int multiprocess, int* index, int* protocol, double* predicted_us);
 
 /* ---- plans ------------------------------------------------------------------ */
 
@@ -110,10 +118,24 @@ int sccl_plan_bind_peers(sccl_plan* plan, const void* const* peer_blobs, size_t 
 int sccl_plan_export_fd(sccl_plan* plan, int* fd);
 int sccl_plan_bind_peers_fd(sccl_plan* plan, const void* const* peer_blobs, size_t blob_len, const int* fds);
 
-/* The registered (peer-writable) receive buffer of a multi-process plan.
- * Passing it as recvbuf to sccl_launch is zero-copy; any other recvbuf gets
- * a trailing device-to-device copy. */
+/* The plan's own registered (peer-writable) receive buffer.  Passing it, or
+ * a buffer registered with sccl_plan_register_bind, as recvbuf to
+ * sccl_launch is zero-copy; any other recvbuf gets a trailing
+ * device-to-device copy. */
 int sccl_plan_recv_buffer(sccl_plan* plan, void** ptr, size_t* bytes);
+
+/* Zero-copy receive targets (multi-process, CUDA IPC; SURVEY.md 8(b) b4:
+ * "caller owns recvbuf, which must be peer-mapped (registered) for
+ * zero-copy").  Collective, like the plan's own handle exchange: every rank
+ * exports a blob for its buffer (>= the receive size, from cudaMalloc or
+ * torch's caching allocator; any offset inside the allocation), the caller
+ * gathers the blobs, and every rank binds its own buffer with all of them.
+ * A launch whose recvbuf is a registered buffer then has the peers write it
+ * directly (no copy-out); every rank must pass its counterpart registration
+ * in the same launch.  Loopback plans need no registration. */
+int sccl_plan_register_export(sccl_plan* plan, void* buf, size_t bytes, void* blob, size_t* len);
+int sccl_plan_register_bind(sccl_plan* plan, void* buf, const void* const* peer_blobs, size_t blob_len);
+int sccl_plan_deregister(sccl_plan* plan, void* buf);
 
 /* Asynchronous, stream-ordered launch (multi-process). */
 int sccl_launch(sccl_plan* plan, const void* sendbuf, void* recvbuf, void* stream);
@@ -129,7 +151,9 @@ int sccl_launch_loopback_copy_engine(sccl_plan* plan, const void* const* sendbuf
                                      void* stream);
 
 /* After the stream is synchronized: SCCL_PEER_TIMEOUT if the watchdog fired
- * (details in sccl_last_error), else SCCL_OK. */
+ * (details in sccl_last_error), else SCCL_OK.  A timed-out plan is poisoned
+ * (its launch counters are out of step with its peers'): launches return
+ * SCCL_PEER_TIMEOUT; destroy it.  Peers that waited on it time out too. */
 int sccl_plan_check(sccl_plan* plan);
 
 /* Lowered program summary (JSON): ops per rank, channels, tile, scratch. */

@@ -15,9 +15,26 @@ based on the input size" of PAPER.md:1037.
 from __future__ import annotations
 
 from fractions import Fraction
-from typing import Dict, Iterable, List, Optional, Sequence, Tuple
+from typing import Dict, Iterable, List, NamedTuple, Optional, Sequence, Tuple
 
-Tuple3 = Tuple[int, int, int]  # (C, S, R)
+
+class Algo(NamedTuple):
+    """A k-synchronous schedule's cost coordinates in the reference's order
+    (SPEC.md:473-484: time(S, R, C, ...), crossover(a: (S,R,C), b: (S,R,C)))."""
+    S: int
+    R: int
+    C: int
+
+
+Tuple3 = Tuple[int, int, int]  # (S, R, C), as in the reference
+
+
+def _algo(x) -> Algo:
+    """(S, R, C) tuple or Algo; a mapping with S/R/C keys also works."""
+    if isinstance(x, dict):
+        return Algo(int(x["S"]), int(x["R"]), int(x["C"]))
+    S, R, C = x
+    return Algo(int(S), int(R), int(C))
 
 
 def _q(x) -> Fraction:
@@ -33,9 +50,9 @@ def time(S: int, R: int, C: int, alpha, beta, L) -> Fraction:
 
 def crossover(a: Tuple3, b: Tuple3, alpha, beta) -> Optional[Fraction]:
     """Size where time_a == time_b, or None for parallel / dominated lines
-    (SPEC.md:476-484).  a, b are (C, S, R)."""
-    Ca, Sa, Ra = a
-    Cb, Sb, Rb = b
+    (SPEC.md:476-484).  a, b are (S, R, C), the reference's order."""
+    Sa, Ra, Ca = _algo(a)
+    Sb, Rb, Cb = _algo(b)
     slope = (Fraction(Ra, Ca) - Fraction(Rb, Cb)) * _q(beta)
     icpt = (Sb - Sa) * _q(alpha)
     if slope == 0:
@@ -45,29 +62,29 @@ def crossover(a: Tuple3, b: Tuple3, alpha, beta) -> Optional[Fraction]:
 
 
 def best_for_size(frontier: Sequence[Tuple3], alpha, beta, sizes: Iterable) -> List[Tuple[object, Tuple3]]:
-    """Per size, the entry minimizing time; ties -> fewer steps."""
+    """Per size, the entry minimizing time; ties -> fewer steps
+    (SPEC.md:485-493).  Entries are (S, R, C); each is returned as given."""
     if not frontier:
         raise ValueError("empty frontier")
     out = []
     for L in sizes:
-        best = min(frontier, key=lambda e: (time(e[1], e[2], e[0], alpha, beta, L), e[1]))
+        best = min(frontier, key=lambda e: (time(*_algo(e), alpha, beta, L), _algo(e).S))
         out.append((L, best))
     return out
 
 
 def fit(points: Sequence[Tuple[int, int, int, float, float]]) -> Tuple[float, float]:
-    """Least-squares (alpha, beta) from measurements (C, S, R, bytes, seconds)."""
+    """Least-squares (alpha, beta) from measurements (S, R, C, bytes, seconds)."""
     import numpy as np
-    A = np.array([[S, R / C * L] for C, S, R, L, _ in points], dtype=float)
+    A = np.array([[S, R / C * L] for S, R, C, L, _ in points], dtype=float)
     y = np.array([t for *_, t in points], dtype=float)
     sol, *_ = np.linalg.lstsq(A, y, rcond=None)
     return float(max(sol[0], 0.0)), float(max(sol[1], 0.0))
 
 
 def select(candidates: Dict[str, Tuple3], alpha: float, beta: float, nbytes: int) -> str:
-    """Name of the candidate schedule the model predicts fastest for nbytes
-    (per-rank buffer; L = nbytes)."""
-    return min(candidates, key=lambda k: (time(candidates[k][1], candidates[k][2], candidates[k][0],
-                                                Fraction(alpha).limit_denominator(10**12),
-                                                Fraction(beta).limit_denominator(10**18), nbytes),
-                                           candidates[k][1]))
+    """Name of the candidate schedule (S, R, C) the model predicts fastest
+    for nbytes (per-rank buffer; L = nbytes)."""
+    a = Fraction(alpha).limit_denominator(10**12)
+    b = Fraction(beta).limit_denominator(10**18)
+    return min(candidates, key=lambda k: (time(*_algo(candidates[k]), a, b, nbytes), _algo(candidates[k]).S))

@@ -217,8 +217,22 @@ __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
   return v;
 }
 
-// Watchdog: the diagnostic goes to host-mapped memory and the kernel traps
-// (the host maps it to SCCL_PEER_TIMEOUT).
+// Cooperative abort.  A wait that outlives timeout_ns records a diagnostic
+// in host-mapped memory (the host maps it to SCCL_PEER_TIMEOUT), sets the
+// launch-wide abort word (device memory) and this CTA's abort flag, and
+// returns as if satisfied.  From then on the CTA publishes nothing -- no
+// stores to peers or outputs, no counters, no LL words -- so no peer ever
+// consumes a value computed from data that never arrived: ranks that depend
+// on this one time out in turn (every slow wait also polls the abort word,
+// so they give up at once).  Every role still walks its program to the end,
+// so the mbarrier pipeline drains and the kernel exits normally: no trap,
+// the CUDA context stays usable.  The plan itself is poisoned (its epochs
+// and counters are out of step); the host refuses further launches.
+__shared__ uint32_t cta_abort;  // per CTA
+__device__ __forceinline__ bool cta_aborted() { return *reinterpret_cast<volatile uint32_t*>(&cta_abort) != 0; }
+__device__ __forceinline__ bool launch_aborted(const KParams& p) {
+  return p.abort && *reinterpret_cast<volatile int*>(p.abort) != 0;
+}
 __device__ __noinline__ void watchdog_fire(const KParams& p, int rank, int ch, int op, int slot, uint64_t target,
                                            uint64_t seen) {
   volatile int* e = p.errinfo;
@@ -233,18 +247,33 @@ __device__ __noinline__ void watchdog_fire(const KParams& p, int rank, int ch, i
     e[0] = ERR_TIMEOUT;
     __threadfence_system();
   }
-  __trap();
+  *reinterpret_cast<volatile uint32_t*>(&cta_abort) = 1u;
+  if (p.abort) *reinterpret_cast<volatile int*>(p.abort) = 1;
+}
+// an abort raised elsewhere in the launch: give up this wait too
+__device__ __forceinline__ bool join_abort(const KParams& p) {
+  if (cta_aborted()) return true;
+  if (launch_aborted(p)) {
+    *reinterpret_cast<volatile uint32_t*>(&cta_abort) = 1u;
+    return true;
+  }
+  return false;
 }
 
 // mbarrier phase wait bounded by the watchdog: a pipeline hand-off that
-// never completes (a bug, not a peer) traps instead of hanging the GPU.
+// never completes (a bug, not a peer) aborts instead of hanging the GPU.
 __device__ __noinline__ void mbar_wait_slow(uint64_t* b, uint32_t parity, const KParams& p, int rank, int ch,
                                             int op) {
   const uint64_t t0 = globaltimer();
   for (uint32_t spins = 1;; ++spins) {
     if (mbar_try(b, parity)) return;
-    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
-      watchdog_fire(p, rank, ch, op, -4, parity, 0);
+    if ((spins & 1023) == 0) {
+      if (join_abort(p)) return;
+      if (p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+        watchdog_fire(p, rank, ch, op, -4, parity, 0);
+        return;
+      }
+    }
   }
 }
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* b, uint32_t parity, const KParams& p, int rank, int ch,
@@ -258,14 +287,20 @@ __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p
                             int slot) {
   uint64_t v = ld_acquire<SYS>(f);
   if (v >= target) return v;
+  if (join_abort(p)) return target;
   // poll with relaxed (strong) loads -- no L1 invalidation per poll -- and
   // acquire once the target is reached
   uint64_t t0 = globaltimer();
   uint32_t spins = 0;
   while ((v = ld_relaxed<SYS>(f)) < target) {
     if (++spins > 64) __nanosleep(32);
-    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
-      watchdog_fire(p, rank, ch, op, slot, target, v);
+    if ((spins & 1023) == 0) {
+      if (join_abort(p)) return target;
+      if (p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+        watchdog_fire(p, rank, ch, op, slot, target, v);
+        return target;
+      }
+    }
   }
   fence_acq<SYS>();
   return v;
@@ -397,34 +432,34 @@ struct Vec<4> {  // f16: widen, add in f32 in input order, round once
   }
 };
 
-// element-wise path (unaligned ops, the < 16 B chunk tail): global -> global
-template <int DT>
-__device__ void elem_op(const char* const* in, int nin, char* const* out, int nout, int64_t off, int64_t nbytes,
-                        int tid, int nthr) {
+// element-wise path (unaligned ops, the < 16 B chunk tail): global -> global.
+// in(k) / out(o) return input k's / output o's base address.
+template <int DT, class In, class Out>
+__device__ void elem_op(In in, int nin, Out out, int nout, int64_t off, int64_t nbytes, int tid, int nthr) {
   constexpr int ES = (DT == 0) ? 1 : (DT == 3 || DT == 4) ? 2 : 4;
   for (int64_t i = tid; i < nbytes / ES; i += nthr) {
     const int64_t b = off + i * ES;
     if (DT == 0) {
-      uint8_t a = *(const volatile uint8_t*)(in[0] + b);
-      for (int k = 1; k < nin; ++k) a = uint8_t(a + *(const volatile uint8_t*)(in[k] + b));
-      for (int o = 0; o < nout; ++o) *(volatile uint8_t*)(out[o] + b) = a;
+      uint8_t a = *(const volatile uint8_t*)(in(0) + b);
+      for (int k = 1; k < nin; ++k) a = uint8_t(a + *(const volatile uint8_t*)(in(k) + b));
+      for (int o = 0; o < nout; ++o) *(volatile uint8_t*)(out(o) + b) = a;
     } else if (DT == 1) {
-      uint32_t a = *(const volatile uint32_t*)(in[0] + b);
-      for (int k = 1; k < nin; ++k) a += *(const volatile uint32_t*)(in[k] + b);
-      for (int o = 0; o < nout; ++o) *(volatile uint32_t*)(out[o] + b) = a;
+      uint32_t a = *(const volatile uint32_t*)(in(0) + b);
+      for (int k = 1; k < nin; ++k) a += *(const volatile uint32_t*)(in(k) + b);
+      for (int o = 0; o < nout; ++o) *(volatile uint32_t*)(out(o) + b) = a;
     } else if (DT == 2) {
-      float a = __int_as_float(*(const volatile int*)(in[0] + b));
-      for (int k = 1; k < nin; ++k) a = __fadd_rn(a, __int_as_float(*(const volatile int*)(in[k] + b)));
-      for (int o = 0; o < nout; ++o) *(volatile int*)(out[o] + b) = __float_as_int(a);
+      float a = __int_as_float(*(const volatile int*)(in(0) + b));
+      for (int k = 1; k < nin; ++k) a = __fadd_rn(a, __int_as_float(*(const volatile int*)(in(k) + b)));
+      for (int o = 0; o < nout; ++o) *(volatile int*)(out(o) + b) = __float_as_int(a);
     } else {
       auto widen = [](uint16_t h) -> float {
         if (DT == 3) return __uint_as_float(uint32_t(h) << 16);
         return __half2float(__ushort_as_half(h));
       };
-      float a = widen(*(const volatile uint16_t*)(in[0] + b));
-      for (int k = 1; k < nin; ++k) a = __fadd_rn(a, widen(*(const volatile uint16_t*)(in[k] + b)));
+      float a = widen(*(const volatile uint16_t*)(in(0) + b));
+      for (int k = 1; k < nin; ++k) a = __fadd_rn(a, widen(*(const volatile uint16_t*)(in(k) + b)));
       uint16_t r = (DT == 3) ? __bfloat16_as_ushort(__float2bfloat16_rn(a)) : __half_as_ushort(__float2half_rn(a));
-      for (int o = 0; o < nout; ++o) *(volatile uint16_t*)(out[o] + b) = r;
+      for (int o = 0; o < nout; ++o) *(volatile uint16_t*)(out(o) + b) = r;
     }
   }
 }
@@ -516,6 +551,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       mbar_init(&S.empty[s], 1);
     }
     S.published = S.trace_n = 0;
+    cta_abort = 0;
     for (int s = 0; s < NSTAGE; ++s) {
       S.dsn[s] = 0;
       for (int k = 0; k < 32; ++k) S.dsc[s][k] = nullptr;
@@ -634,10 +670,14 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           if (p.multiprocess && d.rank != rank) await_entry(d.rank, int(oi - ob));
         }
         named_sync(1);
-        if (op.kind == 0) elem_op<0>(s_inp, 1, s_outp, op.nout, q.off, q.len, ptid, NPART);
-        else elem_op<DT>(s_inp, op.nin, s_outp, op.nout, q.off, q.len, ptid, NPART);
+        if (!cta_aborted()) {
+          auto in = [&](int k) { return s_inp[k]; };
+          auto out = [&](int o) { return s_outp[o]; };
+          if (op.kind == 0) elem_op<0>(in, 1, out, op.nout, q.off, q.len, ptid, NPART);
+          else elem_op<DT>(in, op.nin, out, op.nout, q.off, q.len, ptid, NPART);
+        }
         named_sync(1);
-        if (tid == 32) {
+        if (tid == 32 && !cta_aborted()) {
           fence_rel<SYS>();
           for (int o = 0; o < op.nout; ++o) {
             const DevOut d = OUTS[op.out_begin + o];
@@ -758,21 +798,18 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             if (lane == 0) trace_ev(p, &S.trace_n, TR_FULL, oi, t);
           }
           if (lane == 0) trace_ev(p, &S.trace_n, TR_READY, oi, t);
-          if (n > nv && lane == 0) {  // < 16 B chunk tail: element-wise, global -> global
-            const char* in[kMaxOpIn];
-            char* out[kMaxOpOut];
-            for (int k = 0; k < op.nin; ++k) {
-              const DevIn x = INS[op.in_begin + k];
-              in[k] = p.base[x.rank][x.space] + x.off + q.off;
-            }
-            for (int o = 0; o < op.nout; ++o) {
-              const DevOut d = OUTS[op.out_begin + o];
-              out[o] = p.base[d.rank][d.space] + d.off + q.off;
-            }
+          const bool ab = cta_aborted();  // aborted: publish nothing (see watchdog_fire)
+          if (n > nv && lane == 0 && !ab) {  // < 16 B chunk tail: element-wise, global -> global
+            // addresses from the descriptors per element (no pointer arrays on the stack)
+            const DevIn* ins = INS + op.in_begin;
+            const DevOut* outs = OUTS + op.out_begin;
+            const int64_t qo = q.off;
+            auto in = [&](int k) -> const char* { return p.base[ins[k].rank][ins[k].space] + ins[k].off + qo; };
+            auto out = [&](int o) -> char* { return p.base[outs[o].rank][outs[o].space] + outs[o].off + qo; };
             if (op.kind == 0) elem_op<0>(in, 1, out, op.nout, int64_t(lo + nv), n - nv, 0, 1);
             else elem_op<DT>(in, op.nin, out, op.nout, int64_t(lo + nv), n - nv, 0, 1);
           }
-          if (outp && nv) {
+          if (outp && nv && !ab) {
             if (p.l2hint && !((p.l2hint & kL2RelayPlain) && every))
               bulk_store_hint(outp + lo, bufs + size_t(s) * STAGE, nv, every ? pol_last : pol_first);
             else bulk_store(outp + lo, bufs + size_t(s) * STAGE, nv);
@@ -791,7 +828,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
               }
             }
             __syncwarp();
-            if (sig && (every || lo + n == uint64_t(q.len))) {
+            if (sig && (every || lo + n == uint64_t(q.len)) && !ab) {
               fence_rel<SYS>();
               st_relaxed<SYS>(sig, fbase + lo + n);
             }
@@ -864,6 +901,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       k = __shfl_sync(0xffffffffu, k, 0);
       if (k == 0) continue;
       fence_rel<SYS>();
+      const bool ab = cta_aborted();  // aborted: advance, publish nothing
       for (uint32_t left = k; left;) {
         const SigOp& x = S.win[wh % SIGWIN];
         const uint32_t take = min(left, x.ntiles - t0);
@@ -873,7 +911,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         const bool last = end == x.qlen;  // the op's final byte
         if (lane < int(x.nout)) {
           uint64_t* f = x.sig[lane];
-          if (f && (((x.every >> lane) & 1u) || last)) st_relaxed<SYS>(f, x.fbase + end);
+          if (f && (((x.every >> lane) & 1u) || last) && !ab) st_relaxed<SYS>(f, x.fbase + end);
         }
         if (lane == 0) trace_ev(p, &S.trace_n, TR_PUB, x.oi, uint32_t(end));
         t0 += take;
@@ -979,21 +1017,28 @@ __device__ __forceinline__ void st_ll(void* p, uint2 d, uint32_t f) {
 }
 
 // 8 data bytes of an LL slot at pair index; waits for the epoch flag of
-// every valid word
+// every valid word (gives up under the watchdog / an abort: the caller then
+// stores nothing, cta_abort is set)
 template <bool SYS>
 __device__ uint2 ll_read(const char* slot, int64_t pair, bool two, uint32_t ef, const KParams& p, int rank, int ch,
                          int op) {
   const char* a = slot + pair * 16;
   uint4 v = ld_ll(a);
   if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
+  if (join_abort(p)) return make_uint2(0, 0);
   const uint64_t t0 = globaltimer();
   uint32_t spins = 0;
   for (;;) {
     v = ld_ll(a);
     if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
     if (++spins > 32) __nanosleep(20);
-    if ((spins & 1023) == 0 && p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns)
-      watchdog_fire(p, rank, ch, op, -3, ef, v.y);
+    if ((spins & 1023) == 0) {
+      if (join_abort(p)) return make_uint2(0, 0);
+      if (p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+        watchdog_fire(p, rank, ch, op, -3, ef, v.y);
+        return make_uint2(0, 0);
+      }
+    }
   }
 }
 
@@ -1040,6 +1085,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
     trace_ev(p, &s_trace_n, TR_START, 0, 0);
     s_e = p.epochs[blockIdx.x] + 1;
     s_entry_mask = 1u << rank;
+    cta_abort = 0;
   }
   if (tid == PF) {
     const uint32_t b = p.prog[rank * p.kc + cg], en = p.prog[rank * p.kc + cg + 1];
@@ -1110,6 +1156,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
                             : ld_plain8(s_inp[i] + 8 * k, n, op.vec));
         v = acc.out();
       }
+      if (cta_aborted()) continue;  // a read above gave up: publish nothing (see watchdog_fire)
       for (int o = 0; o < op.nout; ++o) {
         if (s_outll[o]) st_ll(s_outp[o] + 16 * k, v, ef);
         else st_plain8(s_outp[o] + 8 * k, v, n, op.vec);

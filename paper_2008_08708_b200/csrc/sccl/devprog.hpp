@@ -62,6 +62,7 @@ struct KParams {
   int dcache_min_ops;    // cache a CTA's descriptors in shared memory from this many ops up (0 = never)
   uint64_t* epochs;      // [nranks_launch * nch] per-CTA launch counters
   int* errinfo;          // host-mapped watchdog record
+  int* abort;            // device word: set by the first watchdog expiry of the launch (cooperative abort)
   long long timeout_ns;
   int P, nch, rank0, nranks_launch;
   int kc, kb;            // nch = kc * kb: chunk groups x byte parts per chunk

@@ -55,7 +55,7 @@ bool writes_loc(const Op& op, const Loc& L) {
 
 }  // namespace
 
-Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
+Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll, bool pull) {
   auto viol = verify(s);
   if (!viol.empty())
     throw invalid_argument_error("executing an unverified schedule is rejected (SPEC.md:420): " + viol[0].str() +
@@ -72,6 +72,7 @@ Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
 
   Program pg;
   pg.ll = ll;
+  pg.pull = pull;
   pg.kind = s.kind;
   pg.P = P;
   pg.G = G;
@@ -127,6 +128,12 @@ Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
         for (auto& u : upd) b.cur[u.c * P + u.n] = {u.loc, u.slot, true};
       }
     } else {
+      // nodes that receive a contribution of chunk c in this phase reduce
+      // it into their accumulator (RECV, which an in-place caller aliases
+      // with SEND): their input is pulled only if they never do, so no
+      // reader can race the owner's own write
+      std::vector<uint8_t> receives(size_t(G) * P, 0);
+      for (auto& t : ph.sends) receives[size_t(t.chunk) * P + t.dst] = 1;
       for (int st = 0; st < ph.S; ++st) {
         struct Rc {
           int src, slot;
@@ -137,6 +144,12 @@ Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
           if (t.step != st) continue;
           const Cur& src = b.cur[t.chunk * P + t.src];
           if (!src.valid) throw invalid_argument_error("internal: sender holds no contribution after verification");
+          if (pull && src.loc.space == SP_SEND && src.flag < 0 && !receives[size_t(t.chunk) * P + t.src]) {
+            // pull: the sender's value at V_s is its untouched input, so the
+            // receiver's reduce reads it in place (no receipt slot, no copy)
+            recv[{t.dst, t.chunk}].push_back({t.src, -1, src.loc});
+            continue;
+          }
           const int64_t len = pg.geo[t.chunk].len;
           Loc dst{t.dst, SP_SCRATCH, b.scratch_alloc(t.dst, ll ? ll_bytes(len) : len), t.chunk};
           int slot = b.new_slot(t.dst);
@@ -289,7 +302,8 @@ Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll) {
     pg.scratch_bytes = std::max(pg.scratch_bytes, rp.scratch_bytes);
   }
   // fingerprint: every rank must lower the identical program
-  std::string text = serialize(s) + "|" + std::to_string(nbytes) + "|" + std::to_string(esize) + (ll ? "|ll" : "");
+  std::string text = serialize(s) + "|" + std::to_string(nbytes) + "|" + std::to_string(esize) + (ll ? "|ll" : "") +
+                     (pull ? "|pull" : "");
   uint64_t h = 0xcbf29ce484222325ull;
   for (unsigned char ch : text) {
     h ^= ch;
@@ -305,8 +319,8 @@ std::string Program::summary_json() const {
   std::ostringstream o;
   o << "{\"collective\":\"" << kind_name(kind) << "\",\"P\":" << P << ",\"G\":" << G << ",\"bytes\":" << nbytes
     << ",\"send_bytes\":" << send_bytes << ",\"recv_bytes\":" << recv_bytes << ",\"max_slots\":" << max_slots
-    << ",\"scratch_bytes\":" << scratch_bytes << ",\"protocol\":\"" << (ll ? "ll" : "simple")
-    << "\",\"fingerprint\":\"" << fingerprint << "\",\"ranks\":[";
+    << ",\"scratch_bytes\":" << scratch_bytes << ",\"protocol\":\"" << (ll ? "ll" : "simple") << "\",\"pull\":" << (pull ? 1 : 0)
+    << ",\"fingerprint\":\"" << fingerprint << "\",\"ranks\":[";
   static const char* sp[] = {"send", "recv", "scratch", "flags"};
   for (int r = 0; r < P; ++r) {
     o << (r ? "," : "") << "{\"nslots\":" << ranks[r].nslots << ",\"ops\":[";

@@ -75,6 +75,7 @@ struct Program {
   int max_slots = 0;
   int64_t scratch_bytes = 0;  // symmetric per-rank scratch size
   bool ll = false;            // low-latency protocol: every receipt is an LL slot in scratch
+  bool pull = false;          // combining sends of untouched inputs are read in place by the receiver
   std::string fingerprint;    // hash of (canonical schedule, sizes, dtype, protocol)
 
   std::string summary_json() const;
@@ -85,7 +86,14 @@ struct Program {
 // scratch slot encoded as (4 data bytes, 4 flag bytes) words (2x the chunk),
 // so the receiver polls the data itself; post entries then get a local
 // unpacking copy, fused with the forward of the same receipt.
-Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll = false);
+//
+// pull = combining sends whose sender still holds its untouched input (the
+// one-shot reduce-scatter, the first hop of every reduction chain) become
+// reads of the sender's SEND buffer by the receiver's REDUCE: no receipt
+// slot in scratch, no copy op, no flag.  Same reduction order and operands,
+// so the same bits.  Only where every rank's SEND is addressable and
+// unchanged for the whole launch (loopback).
+Program lower(const Schedule& s, int64_t nbytes, int esize, bool ll = false, bool pull = false);
 
 // bytes of an LL slot for a chunk of len bytes
 inline int64_t ll_bytes(int64_t len) { return 2 * ((len + 15) / 16 * 16); }

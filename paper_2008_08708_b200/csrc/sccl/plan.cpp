@@ -107,6 +107,7 @@ struct Vmm {
   decltype(&cuMemRelease) release = nullptr;
   decltype(&cuMemExportToShareableHandle) export_handle = nullptr;
   decltype(&cuMemImportFromShareableHandle) import_handle = nullptr;
+  decltype(&cuMemGetAddressRange) address_range = nullptr;
 };
 const Vmm& vmm_api() {
   static Vmm v;
@@ -129,6 +130,7 @@ const Vmm& vmm_api() {
     get("cuMemRelease", v.release);
     get("cuMemExportToShareableHandle", v.export_handle);
     get("cuMemImportFromShareableHandle", v.import_handle);
+    get("cuMemGetAddressRange", v.address_range);
     done = true;
   }
   return v;
@@ -153,7 +155,17 @@ struct IpcBlob {
   char magic[8];
   char fingerprint[24];
   int32_t rank, nranks, nch, kc, kb, tile;
+  int32_t dtype, redop;  // the program fingerprint covers the element size, not the format
   uint64_t region_bytes;
+  cudaIpcMemHandle_t handle;
+};
+
+// A caller buffer registered as a multi-process plan's receive target: the
+// CUDA IPC handle of the allocation that holds it plus the offset inside.
+struct RegBlob {
+  char magic[8];
+  int32_t rank, pad;
+  uint64_t bytes, offset;
   cudaIpcMemHandle_t handle;
 };
 
@@ -202,15 +214,15 @@ constexpr double kStreamBytes = 1e9;
 // to the B200 loopback crossover sweep (tools/gpu_runs/proto_round1i.sh:
 // 7 schedules x 16 KiB-16 MiB x both protocols; mean regret vs the
 // per-point best 1.9 %); system scope uses its own fit.
-bool choose_ll(sccl_plan& p, int64_t bytes, int es, int protocol, bool loopback) {
+bool choose_ll(sccl_plan& p, int64_t bytes, int es, int protocol, bool loopback, bool pull) {
   if (protocol < 0 || protocol > 2) throw invalid_argument_error("protocol must be 0 (auto), 1 (simple), 2 (ll)");
   if (protocol != 0) {
-    p.pg = lower(p.sched, bytes, es, protocol == 2);
+    p.pg = lower(p.sched, bytes, es, protocol == 2, pull);
     return protocol == 2;
   }
   int steps = 0;
   for (auto* ph : p.sched.flat()) steps += ph->S;
-  Program a = lower(p.sched, bytes, es, true), b = lower(p.sched, bytes, es, false);
+  Program a = lower(p.sched, bytes, es, true, pull), b = lower(p.sched, bytes, es, false, pull);
   const bool sys = !loopback || loopback_sys();
   const bool ll = predict_us(a, steps, true, sys) < predict_us(b, steps, false, sys);
   p.pg = ll ? std::move(a) : std::move(b);
@@ -268,7 +280,14 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
                   : p.ll ? 2048 / kLLThreads
                          : std::max(1, std::min(2, int((227 << 10) / (p.nstage * p.tile + kSmemHdr))));
   const int resident = std::max(1, req.sms * std::max(1, bps));
-  const int cap = loopback ? std::max(1, resident / p.sched.P) : 32;
+  // pull-lowered wide reductions (every input read in place, no receipt
+  // re-read): each CTA streams nin reads and nout writes, and one CTA per SM
+  // keeps DRAM busiest (AR (8,2,2) bf16 at 64 MiB/rank: 144 CTAs 182 us,
+  // 192: 199, 296: 190, 96: 232; 256 MiB: 714 / 769 / -- / 893 us;
+  // tools/gpu_runs/r02/abort_reg.sh)
+  const bool pull_stream = loopback && !p.ll && p.pg.pull && st.reduces && !st.rereads && st.max_fanin >= 4 &&
+                           st.bytes >= kStreamBytes / 8;  // (small launches are latency-bound: more CTAs)
+  const int cap = loopback ? std::max(1, (pull_stream ? req.sms : resident) / p.sched.P) : 32;
   const int64_t part = p.ll ? kLLPart : p.tile;
   int kb, kc;
   if (req.nchannels > 0) {
@@ -441,7 +460,9 @@ void encode_program(sccl_plan& p) {
     d.nout = uint16_t(op.outs.size());
     bool vec = true;
     for (auto& in : ins) {
-      if (in.loc.rank != r) throw invalid_argument_error("internal: op reads remote memory");
+      // remote reads only of untouched SEND buffers, and only in pull mode
+      if (in.loc.rank != r && !(p.pg.pull && in.loc.space == SP_SEND && in.flag < 0))
+        throw invalid_argument_error("internal: op reads remote memory");
       DevIn x{};
       x.off = uint64_t(in.loc.off);
       x.len = uint64_t(in.len);
@@ -541,7 +562,9 @@ void choose_streaming(sccl_plan& p, const ProgramStats& st, bool loopback) {
   const char* hint_env = std::getenv("SCCL_L2HINT");  // 0, 1, or 3 (| kL2RelayPlain)
   if (hint_env) p.l2hint = std::atoi(hint_env) & 3;
   if (p.l2hint == kL2RelayPlain) p.l2hint = 0;
-  p.discard = p.l2hint && st.max_fanin >= 4;
+  bool any_dead = false;  // scratch receipts with one reader (pull plans of one-shot reductions have none)
+  for (auto& x : p.ins) any_dead |= x.dead_after != 0;
+  p.discard = p.l2hint && st.max_fanin >= 4 && any_dead;
   if (const char* env = std::getenv("SCCL_DISCARD")) p.discard = std::atoi(env) != 0 && !p.ll;
   if (p.l2hint && !p.discard && !hint_env) p.l2hint |= kL2RelayPlain;
   p.dcache_min_ops = 4;  // SCCL_DCACHE=<n> overrides (0 = off)
@@ -589,7 +612,14 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   int64_t maxlen = 0;  // the largest chunk
   for (auto& g : chunk_geometry(p.sched.kind, p.sched.P, p.sched.flat().back()->G, bytes)) maxlen = std::max(maxlen, g.len);
 
-  p.ll = choose_ll(p, bytes, es, req.protocol, loopback);
+  // pull (combining sends of untouched inputs read in place by the
+  // receiver): loopback only -- every rank's SEND is addressable there and
+  // read-only for the whole launch.  Multi-process plans push: peers'
+  // sendbufs are not mapped, and over NVLink the bytes per direction are
+  // the same either way.
+  if (req.pull > 0 && !loopback) throw invalid_argument_error("pull needs a loopback plan (peers' send buffers are not mapped)");
+  const bool pull = loopback && req.pull >= 0;
+  p.ll = choose_ll(p, bytes, es, req.protocol, loopback, pull);
   p.rank = loopback ? 0 : rank;
   p.nranks = p.sched.P;
   p.loopback = loopback;
@@ -597,7 +627,14 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   p.redop = redop;
   p.device = device;
   p.host_only = device < 0;
-  p.timeout_ns = timeout_ms < 0 ? 0 : (timeout_ms == 0 ? 10000LL : timeout_ms) * 1000000LL;
+  // watchdog default: 10 s in loopback (every rank is in the one launch, so
+  // a wait that long is a bug); 600 s for one rank per GPU, where a peer may
+  // legitimately enter the collective late (checkpointing, evaluation, a
+  // data-loader stall) -- the same order as torch.distributed's default
+  // collective timeout.  An expiry aborts cooperatively (status 5, the CUDA
+  // context stays usable, the plan is poisoned).
+  const int64_t def_ms = loopback ? 10000 : 600000;
+  p.timeout_ns = timeout_ms < 0 ? 0 : (timeout_ms == 0 ? def_ms : timeout_ms) * 1000000LL;
 
   const ProgramStats st = program_stats(p.sched, p.pg, loopback);
   choose_stages(p, st, maxlen, req);
@@ -654,6 +691,8 @@ void plan_device_setup(sccl_plan& p) {
   cuda_check(cudaHostAlloc(&p.h_err, 64 * sizeof(int), cudaHostAllocMapped), "cudaHostAlloc(err)");
   std::memset(p.h_err, 0, 64 * sizeof(int));
   cuda_check(cudaHostGetDevicePointer(&p.d_err, p.h_err, 0), "cudaHostGetDevicePointer");
+  cuda_check(cudaMalloc(&p.d_abort, 256), "cudaMalloc(abort)");
+  cuda_check(cudaMemset(p.d_abort, 0, 256), "memset(abort)");
   cuda_check(cudaDeviceSynchronize(), "plan setup");
   if (!p.loopback) {
     p.peer_region.assign(p.nranks, nullptr);
@@ -670,6 +709,13 @@ int occ_fn(void* ctx, int tile, int nstage) {
   int bps = 0;
   cuda_check(exec_occupancy(c->dtype, c->sys, tile, nstage, &bps), "occupancy");
   return bps;
+}
+
+// A launch whose watchdog expired leaves the plan's epochs and counters out
+// of step with its peers': the plan cannot run again (destroy it).
+void refuse_if_poisoned(const sccl_plan& p) {
+  if (p.h_err && reinterpret_cast<volatile int*>(p.h_err)[0] != 0)
+    throw timeout_error("plan aborted by an earlier peer timeout (watchdog); destroy it and create a new one");
 }
 
 void check_aligned(const void* p, const char* what) {
@@ -691,6 +737,7 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.nwin = p.d_nwin;
   k.epochs = p.d_epochs;
   k.errinfo = p.d_err;
+  k.abort = p.d_abort;
   k.timeout_ns = p.timeout_ns;
   k.P = p.nranks;
   k.nch = p.nch;
@@ -719,6 +766,7 @@ void sccl_plan_opts_init(sccl_plan_opts* o) {
   o->protocol = 0;
   o->timeout_ms = 0;
   o->mem_handles = 0;
+  o->pull = 0;
 }
 
 const char* sccl_last_error(void) { return g_err.c_str(); }
@@ -764,8 +812,8 @@ int sccl_schedule_compose_allreduce(const char* rs, const char* ag, char* out, s
   });
 }
 
-int sccl_schedule_select(const char* const* jsons, int n, size_t bytes, int dtype, int* index, int* protocol,
-                         double* predicted_us) {
+int sccl_schedule_select(const char* const* jsons, int n, size_t bytes, int dtype, int multiprocess, int* index,
+                         int* protocol, double* predicted_us) {
   return guarded([&] {
     if (!jsons || n <= 0 || !index || !protocol) throw invalid_argument_error("NULL argument or no candidates");
     const int es = esize_of(dtype);
@@ -784,7 +832,8 @@ int sccl_schedule_select(const char* const* jsons, int n, size_t bytes, int dtyp
       int steps = 0;
       for (auto* ph : s.flat()) steps += ph->S;
       for (int ll = 0; ll < 2; ++ll) {  // lower() verifies and throws on invalid input
-        const double t = predict_us(lower(s, int64_t(bytes), es, ll != 0), steps, ll != 0);
+        const bool mp = multiprocess != 0;
+        const double t = predict_us(lower(s, int64_t(bytes), es, ll != 0, !mp), steps, ll != 0, mp || loopback_sys());
         if (bi < 0 || t < best) {
           best = t;
           bi = i;
@@ -813,6 +862,7 @@ static int create_common(const char* json, int rank, int nranks, size_t bytes, i
       req.chunk_groups = o.chunk_groups;
       req.tile = o.tile_bytes;
       req.protocol = o.protocol;
+      req.pull = o.pull;
       OccCtx occ{dtype, !loopback};
       if (o.device >= 0) {
         cudaDeviceProp prop{};
@@ -857,7 +907,7 @@ int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
       return;
     }
     IpcBlob b{};
-    std::memcpy(b.magic, "SCCLIPC1", 8);
+    std::memcpy(b.magic, "SCCLIPC2", 8);
     std::strncpy(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1);
     b.rank = p->rank;
     b.nranks = p->nranks;
@@ -865,6 +915,8 @@ int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
     b.kc = p->kc;
     b.kb = p->kb;
     b.tile = p->tile;
+    b.dtype = p->dtype;
+    b.redop = p->redop;
     b.region_bytes = p->region_bytes;
     if (!p->host_only && !p->vmm) {
       cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
@@ -885,13 +937,16 @@ static std::vector<IpcBlob> check_blobs(sccl_plan* p, const void* const* blobs, 
     if (!blobs[r]) throw invalid_argument_error("missing blob for rank " + std::to_string(r));
     std::memcpy(&bs[r], blobs[r], sizeof(IpcBlob));
     const IpcBlob& b = bs[r];
-    if (std::memcmp(b.magic, "SCCLIPC1", 8)) throw invalid_argument_error("bad blob magic from rank " + std::to_string(r));
+    if (std::memcmp(b.magic, "SCCLIPC2", 8)) throw invalid_argument_error("bad blob magic from rank " + std::to_string(r));
     if (b.rank != r || b.nranks != p->nranks)
       throw invalid_argument_error("blob " + std::to_string(r) + " has rank/nranks mismatch");
     if (std::strncmp(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1))
       throw invalid_argument_error("rank " + std::to_string(r) + " lowered a different program (fingerprint mismatch)");
     if (b.nch != p->nch || b.kc != p->kc || b.kb != p->kb || b.tile != p->tile || b.region_bytes != p->region_bytes)
       throw invalid_argument_error("rank " + std::to_string(r) + " uses different channels/tile/region size");
+    if (b.dtype != p->dtype || b.redop != p->redop)
+      throw invalid_argument_error("rank " + std::to_string(r) + " uses a different dtype/redop (dtype " +
+                                   std::to_string(b.dtype) + " vs " + std::to_string(p->dtype) + ")");
   }
   return bs;
 }
@@ -949,6 +1004,96 @@ int sccl_plan_bind_peers_fd(sccl_plan* p, const void* const* blobs, size_t blob_
   });
 }
 
+int sccl_plan_register_export(sccl_plan* p, void* buf, size_t bytes, void* blob, size_t* len) {
+  return guarded([&] {
+    if (!p || !len) throw invalid_argument_error("NULL argument");
+    if (p->loopback) throw invalid_argument_error("loopback plans write caller buffers directly (nothing to register)");
+    if (!blob || *len < sizeof(RegBlob)) {
+      *len = sizeof(RegBlob);
+      if (blob) throw invalid_argument_error("blob buffer too small");
+      return;
+    }
+    if (!buf) throw invalid_argument_error("NULL buffer");
+    check_aligned(buf, "registered buffer");
+    if (bytes < size_t(p->pg.recv_bytes))
+      throw invalid_argument_error("registered buffer smaller than the plan's receive size (" +
+                                   std::to_string(p->pg.recv_bytes) + " bytes)");
+    RegBlob b{};
+    std::memcpy(b.magic, "SCCLREG1", 8);
+    b.rank = p->rank;
+    b.bytes = bytes;
+    if (!p->host_only) {
+      cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+      CUdeviceptr base = 0;
+      size_t sz = 0;
+      cu_check(vmm_api().address_range(&base, &sz, CUdeviceptr(buf)), "cuMemGetAddressRange");
+      b.offset = uint64_t(CUdeviceptr(buf) - base);
+      if (b.offset + bytes > sz) throw invalid_argument_error("registered buffer runs past its allocation");
+      cuda_check(cudaIpcGetMemHandle(&b.handle, reinterpret_cast<void*>(base)),
+                 "cudaIpcGetMemHandle (registered buffers must come from cudaMalloc / the torch caching allocator)");
+    }
+    std::memcpy(blob, &b, sizeof b);
+    *len = sizeof b;
+  });
+}
+
+int sccl_plan_register_bind(sccl_plan* p, void* buf, const void* const* blobs, size_t blob_len) {
+  return guarded([&] {
+    if (!p || !buf || !blobs) throw invalid_argument_error("NULL argument");
+    if (p->loopback) throw invalid_argument_error("loopback plans have no peers");
+    if (!p->bound) throw invalid_argument_error("bind the plan's peers first (sccl_plan_bind_peers)");
+    if (blob_len < sizeof(RegBlob)) throw invalid_argument_error("blob too short");
+    for (auto& g : p->regs)
+      if (g.local == buf) throw invalid_argument_error("buffer already registered with this plan");
+    sccl_plan::RegBuf reg;
+    reg.local = static_cast<char*>(buf);
+    reg.peer.assign(p->nranks, nullptr);
+    reg.peer[p->rank] = reg.local;
+    for (int r = 0; r < p->nranks; ++r) {
+      if (!blobs[r]) throw invalid_argument_error("missing registration blob for rank " + std::to_string(r));
+      RegBlob b;
+      std::memcpy(&b, blobs[r], sizeof b);
+      if (std::memcmp(b.magic, "SCCLREG1", 8) || b.rank != r)
+        throw invalid_argument_error("bad registration blob from rank " + std::to_string(r));
+      if (b.bytes < uint64_t(p->pg.recv_bytes))
+        throw invalid_argument_error("rank " + std::to_string(r) + " registered a buffer smaller than the receive size");
+      if (r == p->rank) {
+        reg.bytes = size_t(b.bytes);
+        continue;
+      }
+      if (p->host_only) continue;
+      // one mapping per peer allocation (torch's caching allocator carves many
+      // tensors out of one cudaMalloc segment; a handle opens once per process)
+      const std::string key = std::to_string(r) + "|" + std::string(reinterpret_cast<const char*>(&b.handle), sizeof b.handle);
+      char* base = nullptr;
+      for (auto& kv : p->ipc_open)
+        if (kv.first == key) base = kv.second;
+      if (!base) {
+        cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+        void* ptr = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess),
+                   "cudaIpcOpenMemHandle (registered buffer)");
+        base = static_cast<char*>(ptr);
+        p->ipc_open.push_back({key, base});
+      }
+      reg.peer[r] = base + b.offset;
+    }
+    p->regs.push_back(std::move(reg));
+  });
+}
+
+int sccl_plan_deregister(sccl_plan* p, void* buf) {
+  return guarded([&] {
+    if (!p || !buf) throw invalid_argument_error("NULL argument");
+    for (size_t i = 0; i < p->regs.size(); ++i)
+      if (p->regs[i].local == buf) {
+        p->regs.erase(p->regs.begin() + long(i));
+        return;  // peer mappings stay open until the plan is destroyed (other registrations may share them)
+      }
+    throw invalid_argument_error("buffer is not registered with this plan");
+  });
+}
+
 int sccl_plan_recv_buffer(sccl_plan* p, void** ptr, size_t* bytes) {
   return guarded([&] {
     if (!p || !ptr) throw invalid_argument_error("NULL argument");
@@ -968,12 +1113,16 @@ int sccl_launch(sccl_plan* p, const void* sendbuf, void* recvbuf, void* stream) 
     check_aligned(sendbuf, "sendbuf");
     char* reg = p->d_region + p->recv_off;
     if (recvbuf) check_aligned(recvbuf, "recvbuf");
+    refuse_if_poisoned(*p);
+    const sccl_plan::RegBuf* target = nullptr;  // a registered caller buffer: peers write it directly
+    for (auto& g : p->regs)
+      if (recvbuf && g.local == recvbuf) target = &g;
     KParams k;
     fill_common(*p, k);
     for (int r = 0; r < p->nranks; ++r) {
       char* reg_r = p->peer_region[r];
       k.base[r][SP_SEND] = r == p->rank ? const_cast<char*>(static_cast<const char*>(sendbuf)) : nullptr;
-      k.base[r][SP_RECV] = reg_r + p->recv_off;
+      k.base[r][SP_RECV] = target ? target->peer[r] : reg_r + p->recv_off;
       k.base[r][SP_SCRATCH] = reg_r + p->scratch_off;
       k.base[r][SP_FLAGS] = reg_r;
     }
@@ -984,7 +1133,7 @@ int sccl_launch(sccl_plan* p, const void* sendbuf, void* recvbuf, void* stream) 
     cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
     cuda_check(launch_exec(k, p->dtype, true, st), "launch");
     p->launches++;
-    if (recvbuf && recvbuf != reg && p->pg.recv_bytes)
+    if (!target && recvbuf && recvbuf != reg && p->pg.recv_bytes)
       cuda_check(cudaMemcpyAsync(recvbuf, reg, size_t(p->pg.recv_bytes), cudaMemcpyDeviceToDevice, st),
                  "copy-out of the registered receive buffer");
   });
@@ -995,6 +1144,7 @@ int sccl_launch_loopback(sccl_plan* p, const void* const* sendbufs, void* const*
     if (!p || !sendbufs || !recvbufs) throw invalid_argument_error("NULL argument");
     if (!p->loopback) throw invalid_argument_error("not a loopback plan");
     if (p->host_only) throw invalid_argument_error("host-only plan cannot launch (no CUDA device)");
+    refuse_if_poisoned(*p);
     KParams k;
     fill_common(*p, k);
     for (int r = 0; r < p->nranks; ++r) {
@@ -1059,7 +1209,7 @@ int sccl_launch_loopback_copy_engine(sccl_plan* p, const void* const* sendbufs, 
 int sccl_plan_check(sccl_plan* p) {
   return guarded([&] {
     if (!p) throw invalid_argument_error("NULL plan");
-    if (p->h_err && p->h_err[0] == ERR_TIMEOUT) {
+    if (p->h_err && p->h_err[0] != 0) {
       volatile int* e = p->h_err;
       throw timeout_error("peer timeout: rank " + std::to_string(e[1]) + " channel " + std::to_string(e[2]) +
                           " op " + std::to_string(e[3]) + " slot " + std::to_string(e[4]) + " waited for " +
@@ -1073,7 +1223,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"groups_balanced\":" << (p->groups_balanced ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"groups_balanced\":" << (p->groups_balanced ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"pull\":" << (p->pg.pull ? 1 : 0) << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";
@@ -1099,6 +1249,7 @@ int sccl_plan_destroy(sccl_plan* p) {
       for (size_t r = 0; r < p->peer_region.size(); ++r)
         if (int(r) != p->rank && p->peer_region[r]) cudaIpcCloseMemHandle(p->peer_region[r]);
     }
+    for (auto& kv : p->ipc_open) cudaIpcCloseMemHandle(kv.second);
     cudaFree(p->d_ops);
     cudaFree(p->d_ins);
     cudaFree(p->d_outs);
@@ -1117,6 +1268,7 @@ int sccl_plan_destroy(sccl_plan* p) {
       cudaFree(p->d_region);
     }
     if (p->h_err) cudaFreeHost(p->h_err);
+    cudaFree(p->d_abort);
   }
   delete p;
   return SCCL_OK;

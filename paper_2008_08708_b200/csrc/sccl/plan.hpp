@@ -57,9 +57,19 @@ struct sccl_plan {
   size_t vmm_size = 0;
   std::vector<uint64_t> peer_vmm;  // imported handles, 0 = none
   bool bound = false;
+  // caller buffers registered as zero-copy receive targets (multi-process):
+  // local pointer, size, every rank's mapping of its counterpart
+  struct RegBuf {
+    char* local = nullptr;
+    size_t bytes = 0;
+    std::vector<char*> peer;
+  };
+  std::vector<RegBuf> regs;
+  std::vector<std::pair<std::string, char*>> ipc_open;  // opened peer allocations (rank|handle -> base)
 
   int* h_err = nullptr;  // host-mapped watchdog record
   int* d_err = nullptr;
+  int* d_abort = nullptr;  // device abort word (cooperative watchdog abort)
   int64_t launches = 0;
   uint64_t* d_trace = nullptr;  // debug trace buffer (caller-owned), sccl_debug_set_trace
   int trace_cap = 0;
@@ -72,6 +82,7 @@ namespace sccl {
 // capacity per SM as a function of the tile (shared-memory stage) size.
 struct ChannelRequest {
   int nchannels = 0, chunk_groups = 0, tile = 0, protocol = 0, stage_budget = 0;
+  int pull = 0;  // 0 auto (loopback: on), 1 on (loopback only), -1 off
   int sms = 148;
   int (*blocks_per_sm)(void* ctx, int tile, int nstage) = nullptr;
   void* ctx = nullptr;

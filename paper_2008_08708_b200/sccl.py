@@ -42,7 +42,7 @@ class PeerTimeoutError(SCCLError):
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("nchannels", ctypes.c_int), ("chunk_groups", ctypes.c_int),
                 ("tile_bytes", ctypes.c_int), ("protocol", ctypes.c_int), ("timeout_ms", ctypes.c_int64),
-                ("mem_handles", ctypes.c_int)]
+                ("mem_handles", ctypes.c_int), ("pull", ctypes.c_int)]
 
 
 _lib = None
@@ -62,7 +62,7 @@ def lib():
             getattr(L, name).argtypes = [ctypes.c_char_p, c_p, ctypes.POINTER(c_sz)]
         L.sccl_schedule_compose_allreduce.argtypes = [ctypes.c_char_p, ctypes.c_char_p, c_p, ctypes.POINTER(c_sz)]
         L.sccl_schedule_select.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_int, c_sz, ctypes.c_int,
-                                           ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                           ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                            ctypes.POINTER(ctypes.c_double)]
         L.sccl_plan_create.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, c_sz, ctypes.c_int,
                                        ctypes.c_int, ctypes.POINTER(_Opts), ctypes.POINTER(c_p)]
@@ -73,6 +73,9 @@ def lib():
         L.sccl_plan_export_fd.argtypes = [c_p, ctypes.POINTER(ctypes.c_int)]
         L.sccl_plan_bind_peers_fd.argtypes = [c_p, ctypes.POINTER(c_p), c_sz, ctypes.POINTER(ctypes.c_int)]
         L.sccl_plan_recv_buffer.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_sz)]
+        L.sccl_plan_register_export.argtypes = [c_p, c_p, c_sz, c_p, ctypes.POINTER(c_sz)]
+        L.sccl_plan_register_bind.argtypes = [c_p, c_p, ctypes.POINTER(c_p), c_sz]
+        L.sccl_plan_deregister.argtypes = [c_p, c_p]
         L.sccl_launch.argtypes = [c_p, c_p, c_p, c_p]
         L.sccl_launch_loopback.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
         L.sccl_launch_loopback_copy_engine.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
@@ -146,14 +149,16 @@ def compose_allreduce(rs, ag) -> str:
     return _string_call(lib().sccl_schedule_compose_allreduce, _text(rs), _text(ag))
 
 
-def select(schedules: Sequence, bytes_per_rank: int, dtype: int = U8):
+def select(schedules: Sequence, bytes_per_rank: int, dtype: int = U8, multiprocess: bool = False):
     """Per-size algorithm + protocol choice among candidate schedules of one
     collective (e.g. a Pareto frontier) by the fitted B200 cost model
-    (PAPER.md:1037).  Returns (index, protocol name,
-    predicted microseconds)."""
+    (PAPER.md:1037).  multiprocess prices one-rank-per-GPU
+    plans (system-scope constants, push lowering) instead of loopback ones.
+    Returns (index, protocol name, predicted microseconds)."""
     arr = (ctypes.c_char_p * len(schedules))(*[_text(x) for x in schedules])
     idx, proto, us = ctypes.c_int(-1), ctypes.c_int(0), ctypes.c_double(0.0)
-    _raise(lib().sccl_schedule_select(arr, len(schedules), bytes_per_rank, dtype, ctypes.byref(idx),
+    _raise(lib().sccl_schedule_select(arr, len(schedules), bytes_per_rank, dtype, int(bool(multiprocess)),
+                                      ctypes.byref(idx),
                                       ctypes.byref(proto), ctypes.byref(us)))
     return idx.value, {1: "simple", 2: "ll"}[proto.value], us.value
 
@@ -169,9 +174,13 @@ PROTOCOLS = {"auto": 0, "simple": 1, "ll": 2}
 MEM_HANDLES = {"ipc": 0, "vmm": 1}
 
 
+PULL = {"auto": 0, "on": 1, "off": -1}
+
+
 def _opts(device: int, nchannels: int, tile_bytes: int, timeout_ms: int, chunk_groups: int = 0,
-          protocol: str = "auto", mem_handles: str = "ipc") -> _Opts:
-    return _Opts(device, nchannels, chunk_groups, tile_bytes, PROTOCOLS[protocol], timeout_ms, MEM_HANDLES[mem_handles])
+          protocol: str = "auto", mem_handles: str = "ipc", pull: str = "auto") -> _Opts:
+    return _Opts(device, nchannels, chunk_groups, tile_bytes, PROTOCOLS[protocol], timeout_ms, MEM_HANDLES[mem_handles],
+                 PULL[pull])
 
 
 def _ptr(x) -> int:
@@ -228,9 +237,9 @@ class LoopbackPlan(_PlanBase):
 
     def __init__(self, schedule, bytes_per_rank: int, dtype: int = U8, device: int = 0,
                  nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0, chunk_groups: int = 0,
-                 protocol: str = "auto"):
+                 protocol: str = "auto", pull: str = "auto"):
         super().__init__()
-        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol)
+        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol, pull=pull)
         rc = lib().sccl_plan_create_loopback(_text(schedule), bytes_per_rank, dtype, SUM,
                                              ctypes.byref(o), ctypes.byref(self._h))
         _raise(rc)
@@ -272,10 +281,10 @@ class Plan(_PlanBase):
 
     def __init__(self, schedule, rank: int, nranks: int, bytes_per_rank: int, dtype: int = U8,
                  device: int = 0, nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0,
-                 chunk_groups: int = 0, protocol: str = "auto", mem_handles: str = "ipc"):
+                 chunk_groups: int = 0, protocol: str = "auto", mem_handles: str = "ipc", pull: str = "auto"):
         super().__init__()
         self.mem_handles = mem_handles
-        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol, mem_handles)
+        o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol, mem_handles, pull)
         rc = lib().sccl_plan_create(_text(schedule), rank, nranks, bytes_per_rank, dtype, SUM,
                                     ctypes.byref(o), ctypes.byref(self._h))
         _raise(rc)
@@ -324,6 +333,27 @@ class Plan(_PlanBase):
             for r, fd in enumerate(fds):
                 if r != self.rank and fd >= 0:
                     os.close(fd)
+
+    def register(self, buf, group=None, nbytes: Optional[int] = None):
+        """Register a caller device buffer (torch tensor or pointer) as a
+        zero-copy receive target: collective over torch.distributed; every
+        rank registers its own buffer.  Launches with recvbuf=buf then have
+        the peers write it directly."""
+        import torch.distributed as dist
+        ptr = _ptr(buf)
+        nb = nbytes if nbytes is not None else buf.numel() * buf.element_size()
+        n = ctypes.c_size_t(0)
+        lib().sccl_plan_register_export(self._h, ctypes.c_void_p(ptr), nb, None, ctypes.byref(n))
+        mine = ctypes.create_string_buffer(n.value)
+        _raise(lib().sccl_plan_register_export(self._h, ctypes.c_void_p(ptr), nb, mine, ctypes.byref(n)))
+        blobs: List[Optional[bytes]] = [None] * self.nranks
+        dist.all_gather_object(blobs, mine.raw[:n.value], group=group)
+        bufs = [ctypes.create_string_buffer(b, len(b)) for b in blobs]
+        arr = (ctypes.c_void_p * len(bufs))(*[ctypes.addressof(b) for b in bufs])
+        _raise(lib().sccl_plan_register_bind(self._h, ctypes.c_void_p(ptr), arr, len(blobs[0])))
+
+    def deregister(self, buf):
+        _raise(lib().sccl_plan_deregister(self._h, ctypes.c_void_p(_ptr(buf))))
 
     def recv_buffer(self):
         p = ctypes.c_void_p(0)

@@ -192,23 +192,49 @@ def diameter(topo: str) -> int:
     return best
 
 
-def bandwidth_lower_bound(kind: str, topo: str) -> "Fraction":
-    """Per-node ingress bound on R/C (the paper's §2.4
-    argument): a node that must receive X chunks per per-node chunk over
-    ingress bandwidth B needs R/C >= X / B.  (The exhaustive cut bounds of
-    SPEC.md:100 are not restated; the per-node bound is sound.)"""
+def bandwidth_lower_bound(kind: str, topo: str, root: int = 0) -> "Fraction":
+    """Per-node bound on R/C (the paper's section 2.4
+    argument): a node that must receive X chunks (per per-node chunk) over
+    ingress bandwidth B, or send X over egress bandwidth B, needs
+    R/C >= X / B.  Gather concentrates the (P-1) receipts on the root's
+    ingress, scatter and broadcast the root's sends on its egress.  (The
+    exhaustive cut bounds of SPEC.md:100 are not restated; the per-node bound
+    is sound.)  Always > 0 for P > 1."""
     from fractions import Fraction
     P, groups = topology_edges(topo)
-    need = {"allgather": P - 1, "alltoall": Fraction(P - 1, P), "broadcast": 1, "gather": 0,
-            "scatter": 0}[kind]
+    others = [n for n in range(P) if n != root]
+    need_in = {n: Fraction(0) for n in range(P)}
+    need_out = {n: Fraction(0) for n in range(P)}
+    if kind == "allgather":
+        need_in = {n: Fraction(P - 1) for n in range(P)}
+    elif kind == "alltoall":
+        need_in = {n: Fraction(P - 1, P) for n in range(P)}
+    elif kind == "broadcast":
+        need_in.update({n: Fraction(1) for n in others})
+        need_out[root] = Fraction(1)
+    elif kind == "gather":
+        need_in[root] = Fraction(P - 1)
+    elif kind == "scatter":
+        need_out[root] = Fraction(P - 1)
+    else:
+        raise ValueError(f"no bandwidth bound for {kind}")
+
+    def cap(n, inbound):
+        side = (lambda e: e[1] == n) if inbound else (lambda e: e[0] == n)
+        c = sum(b for es, b in groups for e in es if side(e) and len(es) == 1)
+        for es, b in groups:  # grouped ingress / egress constraints (switch model)
+            if len(es) > 1 and all(side(e) for e in es):
+                c = b if c == 0 else min(c, b)
+        return c
+
     best = Fraction(0)
     for n in range(P):
-        ingress = sum(b for es, b in groups for (a, d) in es if d == n and len(es) == 1)
-        for es, b in groups:  # grouped ingress constraints (switch model)
-            if len(es) > 1 and all(d == n for (_, d) in es):
-                ingress = b if ingress == 0 else min(ingress, b)
-        if need and ingress:
-            best = max(best, Fraction(need) / ingress)
+        for need, inbound in ((need_in[n], True), (need_out[n], False)):
+            c = cap(n, inbound)
+            if need and c:
+                best = max(best, need / c)
+    if best <= 0:
+        raise ValueError(f"{kind} on {topo}: no positive bandwidth bound (P = {P})")
     return best
 
 
@@ -219,7 +245,7 @@ def pareto_synthesize(kind: str, topo: str, k: int, max_steps: int = 8, timeout:
     S; stop once R/C reaches b_l."""
     from fractions import Fraction
     a_l = diameter(topo)
-    b_l = bandwidth_lower_bound(kind, topo)
+    b_l = bandwidth_lower_bound(kind, topo, root)  # > 0, so every (R, C) scan below ends
     frontier: List[dict] = []
     best_ratio = None
     for S in range(a_l, max_steps + 1):

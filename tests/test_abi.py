@@ -182,3 +182,44 @@ def test_vmm_plan_host_only_errors():
     blobs = [p.export_handles(), sccl.Plan(js, 1, 2, 4096, sccl.U8, device=-1, mem_handles="vmm").export_handles()]
     with pytest.raises(sccl.InvalidArgumentError, match="bind_peers_fd"):
         p.bind_peers(blobs)
+
+
+def test_register_buffer_host_only():
+    """sccl_plan_register_export / _bind on host-only plans (no CUDA): the
+    size and alignment checks, the blob exchange, double registration."""
+    import ctypes
+    js = S.allreduce_from(S.one_shot_allgather(2))
+    plans = [sccl.Plan(js, r, 2, 4096, sccl.F32, device=-1) for r in range(2)]
+    blobs = [p.export_handles() for p in plans]
+    for p in plans:
+        p.bind_peers(blobs)
+    L = sccl.lib()
+    bufs = [ctypes.create_string_buffer(4096 + 16) for _ in range(2)]
+    ptrs = [(ctypes.addressof(b) + 15) // 16 * 16 for b in bufs]
+    n = ctypes.c_size_t(0)
+    assert L.sccl_plan_register_export(plans[0]._h, ctypes.c_void_p(ptrs[0]), 4096, None, ctypes.byref(n)) == 0
+    regs = []
+    for p, ptr in zip(plans, ptrs):
+        blob = ctypes.create_string_buffer(n.value)
+        m = ctypes.c_size_t(n.value)
+        assert L.sccl_plan_register_export(p._h, ctypes.c_void_p(ptr), 4096, blob, ctypes.byref(m)) == 0
+        regs.append(blob)
+        small = ctypes.create_string_buffer(n.value)
+        assert L.sccl_plan_register_export(p._h, ctypes.c_void_p(ptr), 1024, small,
+                                           ctypes.byref(ctypes.c_size_t(n.value))) == sccl.INVALID_ARGUMENT
+    arr = (ctypes.c_void_p * 2)(*[ctypes.addressof(b) for b in regs])
+    for p, ptr in zip(plans, ptrs):
+        assert L.sccl_plan_register_bind(p._h, ctypes.c_void_p(ptr), arr, n.value) == 0
+        assert L.sccl_plan_register_bind(p._h, ctypes.c_void_p(ptr), arr, n.value) == sccl.INVALID_ARGUMENT
+        assert L.sccl_plan_deregister(p._h, ctypes.c_void_p(ptr)) == 0
+        assert L.sccl_plan_deregister(p._h, ctypes.c_void_p(ptr)) == sccl.INVALID_ARGUMENT
+
+
+def test_bind_rejects_dtype_mismatch():
+    """Ranks that lowered the same program for different element formats
+    (bf16 vs f16: same element size, same fingerprint) must not bind."""
+    js = S.allreduce_from(S.one_shot_allgather(2))
+    a = sccl.Plan(js, 0, 2, 4096, sccl.BF16, device=-1)
+    b = sccl.Plan(js, 1, 2, 4096, sccl.F16, device=-1)
+    with pytest.raises(sccl.InvalidArgumentError, match="dtype"):
+        a.bind_peers([a.export_handles(), b.export_handles()])

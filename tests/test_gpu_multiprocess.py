@@ -72,6 +72,41 @@ for case in cases:
         dist.barrier()
     plan.close()
     print("OK", rank, d["collective"], proto, flush=True)
+# caller buffers registered as zero-copy receive targets (peers write them
+# directly, no copy-out): a slice at an offset inside a larger torch
+# allocation, and an in-place allreduce (sendbuf == recvbuf == registered)
+for proto in ("simple", "ll"):
+    js = S.allreduce_from(S.one_shot_allgather(W)) if W == 2 else S.allreduce_from(S.ring_allgather(W))
+    nb = (1 << 20) if proto == "simple" else 8192
+    d = json.loads(js)
+    plan = sccl.Plan(js, rank, W, nb, O.F32, device=0, protocol=proto, timeout_ms=120000, mem_handles=MEM)
+    plan.bind_with()
+    big = torch.zeros(nb + 8192, dtype=torch.uint8, device="cuda")
+    target = big[4096:4096 + nb]
+    plan.register(target)
+    inplace = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+    plan.register(inplace)
+    for it in range(3):
+        ins = O.seeded_inputs("allreduce", W, nb, O.F32, 30 + it)
+        ref = O.execute(d, ins, nb, O.F32)
+        send = torch.from_numpy(ins[rank]).cuda()
+        target.fill_(0xEE)
+        plan.launch(send, target)
+        torch.cuda.synchronize()
+        plan.check()
+        assert np.array_equal(target.cpu().numpy(), ref[rank]), ("registered", proto, it)
+        assert int(big[:4096].max()) == 0 and int(big[4096 + nb:].max()) == 0, "wrote outside the registered slice"
+        inplace.copy_(send)
+        torch.cuda.synchronize()
+        dist.barrier()
+        plan.launch(inplace, inplace)
+        torch.cuda.synchronize()
+        plan.check()
+        assert np.array_equal(inplace.cpu().numpy(), ref[rank]), ("in-place registered", proto, it)
+        dist.barrier()
+    plan.deregister(target)
+    plan.close()
+    print("OK", rank, "registered", proto, flush=True)
 dist.destroy_process_group()
 """
 
@@ -98,4 +133,4 @@ def test_processes_one_gpu(tmp_path, world, mem):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
     text = "".join(o for o, _ in outs)
-    assert text.count("OK") == (5 if world == 2 else 7) * world, text
+    assert text.count("OK") == (5 if world == 2 else 7) * world + 2 * world, text

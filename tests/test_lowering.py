@@ -92,13 +92,47 @@ def test_program_structure_one_shot_allgather():
 
 
 def test_program_structure_fused_allreduce():
-    """(8,2,2): per rank 7 pushes into peers' receipt slots, then one fused
-    receive-reduce-broadcast op (8 inputs, 8 outputs)."""
-    plan = sccl.LoopbackPlan(CASES["ar_b4"], 1 << 20, sccl.BF16, device=-1, protocol="simple")
+    """(8,2,2) push lowering: per rank 7 pushes into peers' receipt slots,
+    then one fused receive-reduce-broadcast op (8 inputs, 8 outputs)."""
+    plan = sccl.LoopbackPlan(CASES["ar_b4"], 1 << 20, sccl.BF16, device=-1, protocol="simple", pull="off")
+    assert plan.info()["pull"] == 0
     for rk in plan.info()["program"]["ranks"]:
         red = [op for op in rk["ops"] if op["kind"] == "reduce"]
         assert len(red) == 1 and len(red[0]["ins"]) == 8 and len(red[0]["outs"]) == 8
         assert sum(op["kind"] == "copy" for op in rk["ops"]) == 7
+
+
+def test_program_structure_pull_allreduce():
+    """(8,2,2) pull lowering (loopback default): the reduce-scatter sends of
+    untouched inputs become in-place reads of the peers' SEND buffers by the
+    home rank's reduce -- no copies, no receipt slots, no scratch; inputs in
+    the schedule's order (own value first, then sources ascending)."""
+    plan = sccl.LoopbackPlan(CASES["ar_b4"], 1 << 20, sccl.BF16, device=-1, protocol="simple")
+    info = plan.info()
+    assert info["pull"] == 1 and info["program"]["scratch_bytes"] == 0
+    for r, rk in enumerate(info["program"]["ranks"]):
+        assert [op["kind"] for op in rk["ops"]] == ["reduce", "wait"]
+        red = rk["ops"][0]
+        assert [i[0] for i in red["ins"]] == [r] + [s for s in range(8) if s != r]
+        assert all(i[1] == "send" and i[3] == -1 for i in red["ins"])
+        assert len(red["outs"]) == 8
+
+
+def test_pull_first_hop_of_chains():
+    """Reduction chains pull only their first hop (the sender's untouched
+    input); later hops read partial sums, which still travel as receipts."""
+    push = sccl.LoopbackPlan(CASES["ar_ring"], 1 << 16, sccl.F32, device=-1, protocol="simple", pull="off").info()
+    pull = sccl.LoopbackPlan(CASES["ar_ring"], 1 << 16, sccl.F32, device=-1, protocol="simple").info()
+    ncopy = lambda info: sum(op["kind"] == "copy" for rk in info["program"]["ranks"] for op in rk["ops"])
+    remote = [i for rk_i, rk in enumerate(pull["program"]["ranks"]) for op in rk["ops"] if op["kind"] == "reduce"
+              for i in op["ins"] if i[0] != rk_i]
+    assert remote and all(i[1] == "send" for i in remote)
+    assert ncopy(pull) == ncopy(push) - 8  # one first-hop send per chunk
+
+
+def test_pull_rejected_for_multiprocess():
+    with pytest.raises(sccl.InvalidArgumentError):
+        sccl.Plan(CASES["ar_b4"], 0, 8, 1 << 16, sccl.BF16, device=-1, pull="on")
 
 
 def test_dead_partial_store_elided():

@@ -36,11 +36,13 @@ def test_small_is_ll_large_is_simple(name):
 
 def test_window_major_only_for_streaming_relay_schedules():
     # relays / reductions re-read receipts: window-major above 1 GB per launch
-    for name in ("ag777", "ring", "ar56", "ar822"):
+    for name in ("ag777", "ring", "ar56"):
         assert info(name, 128 << 20, protocol="simple")["window"] > 0, name
         assert info(name, 4 << 20, protocol="simple")["window"] == 0, name
-    # nothing is re-read: op-major at any size
-    for name in ("ag111", "a2a"):
+    assert info("ar822", 128 << 20, protocol="simple", pull="off")["window"] > 0
+    # nothing is re-read: op-major at any size (the pull-lowered one-shot
+    # allreduce reads peers' inputs in place, it has no receipts to re-read)
+    for name in ("ag111", "a2a", "ar822"):
         assert info(name, 128 << 20, protocol="simple")["window"] == 0, name
 
 
@@ -68,12 +70,13 @@ def test_l2_hints_above_one_gigabyte():
 def test_relays_evict_last_only_when_discarded():
     assert info("ag777", 128 << 20, protocol="simple")["relay_evict_last"] == 0
     assert info("ar56", 128 << 20, protocol="simple")["relay_evict_last"] == 0
-    assert info("ar822", 128 << 20, protocol="simple")["relay_evict_last"] == 1  # discarded after the reduce
+    assert info("ar822", 128 << 20, protocol="simple", pull="off")["relay_evict_last"] == 1  # discarded after use
     assert info("ar822", 16 << 20, protocol="simple")["relay_evict_last"] == 0   # no hints at all
 
 
 def test_discard_only_for_wide_streaming_reductions():
-    assert info("ar822", 128 << 20, protocol="simple")["discard"] == 1   # fan-in 8
+    assert info("ar822", 128 << 20, protocol="simple", pull="off")["discard"] == 1   # fan-in 8
+    assert info("ar822", 128 << 20, protocol="simple")["discard"] == 0   # pull: no receipts
     assert info("ar56", 128 << 20, protocol="simple")["discard"] == 0    # 2-input reduce chain
     assert info("ar822", 16 << 20, protocol="simple")["discard"] == 0    # fits L2
     assert info("ag777", 128 << 20, protocol="simple")["discard"] == 0   # no reduction

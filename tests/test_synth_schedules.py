@@ -111,3 +111,21 @@ def test_pareto_synthesize_small():
     assert synth.bandwidth_lower_bound("allgather", "dgx1") == Fraction(7, 6)  # PAPER §2.4
     fr = synth.pareto_synthesize("allgather", "ring:4", 1, max_steps=4, timeout=60)
     assert [(e["C"], e["S"], e["R"]) for e in fr] == [(2, 2, 3)]
+
+
+@pytest.mark.skipif(shutil.which(os.environ.get("SCCL_SOLVER", "z3")) is None, reason="no SMT solver")
+@pytest.mark.timeout(120)
+def test_pareto_rooted_kinds_terminate():
+    """Gather concentrates the receipts on the root's ingress, scatter the
+    sends on its egress: the bandwidth bound is positive, so Algorithm 1's
+    (R, C) scan ends (it looped forever with a zero bound)."""
+    from fractions import Fraction
+    from paper_2008_08708_b200 import synth
+    assert synth.bandwidth_lower_bound("gather", "ring:4") == Fraction(3, 2)
+    assert synth.bandwidth_lower_bound("scatter", "full:8") == Fraction(1)
+    assert synth.bandwidth_lower_bound("broadcast", "full:8") == Fraction(1, 7)
+    fr = synth.pareto_synthesize("gather", "ring:4", 0, max_steps=3, timeout=60)
+    assert [(e["C"], e["S"], e["R"]) for e in fr] == [(1, 2, 2), (2, 3, 3)]
+    assert fr[-1]["bandwidth_optimal"]
+    fr = synth.pareto_synthesize("scatter", "full:4", 0, max_steps=3, timeout=60)
+    assert [(e["C"], e["S"], e["R"]) for e in fr] == [(1, 1, 1)]

@@ -53,7 +53,7 @@ def main():
             rows = [r for r in results if r["P"] == P and r["collective"] == coll]
             if not rows:
                 continue
-            pts = [(r["C"], r["S"], r["R"], r["bytes_per_rank"], r["us"] * 1e-6) for r in rows]
+            pts = [(r["S"], r["R"], r["C"], r["bytes_per_rank"], r["us"] * 1e-6) for r in rows]
             alpha, beta = costmodel.fit(pts)
             win = {}
             for sz in SIZES:

@@ -91,7 +91,8 @@ def main():
             os.environ.pop("SCCL_STAGE_BUDGET", None)
         try:
             plan = sccl.LoopbackPlan(js, sz, dt, device=0, nchannels=kn.get("kb", 0), chunk_groups=kn.get("kc", 0),
-                                     tile_bytes=kn.get("tile", 0), protocol=kn.get("protocol", "auto"))
+                                     tile_bytes=kn.get("tile", 0), protocol=kn.get("protocol", "auto"),
+                                     pull=kn.get("pull", "auto"))
         except sccl.SCCLError as e:
             print(json.dumps({"sched": name, "bytes": sz, "knobs": kn, "error": str(e)[:100]}), flush=True)
             continue
@@ -106,7 +107,7 @@ def main():
         print(json.dumps({"sched": name, "bytes": sz, "knobs": kn, "us": round(us, 2),
                           "hbm_TBps": round(hbm / us / 1e6, 3), "kc": info["chunk_groups"], "kb": info["byte_parts"],
                           "tile": info["tile_bytes"], "nstage": info["nstage"], "proto": info["protocol"],
-                          "grid": info["grid"], "window": info["window"],
+                          "grid": info["grid"], "window": info["window"], "pull": info["pull"],
                           "persist_l2": persist}), flush=True)
         plan.close()
 
