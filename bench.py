@@ -1,19 +1,31 @@
 #!/usr/bin/env python3
 """Benchmark: collective bus GB/s of the B200 executor for SCCL-synthesized
-schedules (BASELINE.json metric), with the CPU reference executor beside it.
+schedules (BASELINE.json metric), with the CPU reference executor and (N>1)
+NCCL beside it.
 
-N=1 (default): BASELINE config 2's allgather (C,S,R) = (7,7,7) on full(8),
-all 8 ranks in LOOPBACK on cuda:0 (one launch runs every rank's channel
-program; rank buffers live in the same HBM), 128 MiB per rank.
-N>1 (torchrun): one rank per GPU, peers' buffers mapped through CUDA IPC,
-schedule = (7,7,7) at N=8 else one-shot (1,1,1); NCCL all_gather timed on the
-same buffers for reference.
-
-value   = aggregate bus bytes / s = sum over ranks of (P-1)*m per launch / t
-e2e     = same metric through the public API with the inputs copied from
-          pinned host memory and every rank's output copied back, per step
---impl reference: the CPU reference executor (oracle restatement of
-          SPEC.md:418-426, C + pthreads on all host cores) on a bounded sample.
+Metric convention (nccl-tests busBW): bus GB/s per rank =
+algorithmic bytes each rank sends per launch / time; allgather (P-1)*m.
+`value` is that per-rank figure summed over the GPUs of the job:
+  N = 1   the BASELINE config 2 allgather (C,S,R) = (7,7,7) on full(8) with
+          all 8 ranks in LOOPBACK on cuda:0 (one launch runs every rank's
+          channel program; all rank buffers in one HBM), 128 MiB per rank.
+          One GPU => value = the per-rank bus bandwidth (the 8-rank sum is
+          reported beside it as aggregate_GBps), so a 1/2/4/8-GPU series
+          compares per-rank collective speed.
+  N > 1   (torchrun) one rank per GPU, peers' plan regions mapped through
+          CUDA IPC over NVLink/NVSwitch; value = N * per-rank bus GB/s.
+          NCCL is timed on the same buffers (allgather default and
+          NCCL_PROTO=Simple, allreduce Ring/Tree, alltoall as grouped
+          send/recv), plus a <= 64 KB latency sweep and NVML NVLink byte
+          counters around the timed region.
+e2e: the same metric through the public API with host buffers, every step:
+          H2D of every rank's input, the collective, D2H of every rank's
+          whole output.
+--impl reference: the CPU reference executor (oracle/: the C restatement of
+          SPEC.md:418-426, pthreads on all host cores) on the GPU arm's exact
+          workload (same schedule file, ranks, bytes per rank).  It imports
+          nothing from the product package: the schedule comes from the
+          committed file tests/golden/schedules/bench/*.json.
 """
 from __future__ import annotations
 
@@ -27,17 +39,48 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+SCHED_DIR = os.path.join(ROOT, "tests", "golden", "schedules", "bench")
 sys.path.insert(0, ROOT)
 
 METRIC = "collective bus GB/s and latency vs buffer size at 2/4/8 B200 vs NCCL and CPU ref"
+NVLINK_PEAK = 900.0  # GB/s per direction per GPU, NVLink 5 (nominal)
+
+
+def load_schedule(name: str) -> str:
+    with open(os.path.join(SCHED_DIR, name + ".json")) as f:
+        return f.read().strip()
+
+
+def sched_label(name: str) -> str:
+    d = json.loads(load_schedule(name))
+    return f"{d['collective']} ({d['C']},{d['S']},{d['R']}) {name}, {d['topology']['name']}"
+
+
+def workload_schedule(P: int, which: str) -> str:
+    """bench schedule file for the allgather workload at P ranks"""
+    if which == "auto":
+        which = "ham" if P in (2, 8) else "oneshot"
+    return {"ham": f"ag_ham_full{P}", "oneshot": f"ag_oneshot_full{P}", "ring": f"ag_ring_ring{P}"}[which]
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return {"hbm_gbs": 6650.0}, "fallback"
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def _profile_traffic(key: str):
+    """ncu dram__bytes_read+write per launch recorded for this workload by a
+    committed profile (profiles/traffic.json: key -> {bytes, source})."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(key)
+    except Exception:
+        return None, None
+    if isinstance(t, dict):
+        return t.get("bytes"), t.get("source")
+    return t, "profiles/traffic.json"
 
 
 class ClockSampler:
@@ -86,65 +129,44 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def schedule_for(P: int, name: str):
-    from paper_2008_08708_b200 import schedules as S
-    if name == "auto":
-        name = "777" if P == 8 else "oneshot"
-    if name == "777":
-        return S.to_json(S.hamiltonian_allgather(P)), f"allgather ({P-1},{P-1},{P-1}) hamiltonian, full:{P}"
-    if name == "oneshot":
-        return S.to_json(S.one_shot_allgather(P)), f"allgather (1,1,1) one-shot, full:{P}"
-    if name == "ring":
-        return S.to_json(S.ring_allgather(P)), f"allgather (1,{P-1},{P-1}) ring:{P}"
-    raise ValueError(name)
+def busbytes(coll: str, P: int, m: int) -> int:
+    """bytes each rank sends per launch (nccl-tests busBW numerator)"""
+    if coll == "allgather":
+        return (P - 1) * m
+    if coll == "allreduce":
+        return 2 * (P - 1) * m // P
+    return (P - 1) * m // P  # alltoall, reducescatter
 
 
 def hbm_bytes_per_launch(plan) -> int:
-    """Algorithmic HBM bytes of one loopback launch: every lowered op reads
-    each input once and writes each output once."""
+    """Bytes the lowered program reads and writes (every op's inputs and
+    outputs once; loopback: the whole launch)."""
     info = plan.info()["program"]
-    tot = 0
-    for rk in info["ranks"]:
-        for op in rk["ops"]:
-            if op["kind"] == "wait":
-                continue
-            tot += op["len"] * (len(op["ins"]) + len(op["outs"]))
-    return tot
+    return sum(op["len"] * (len(op["ins"]) + len(op["outs"])) for rk in info["ranks"] for op in rk["ops"]
+               if op["kind"] != "wait")
 
 
-# --------------------------------------------------------------------------- CPU reference
-def cpu_reference_run(P: int, js: str, m: int, seconds: float, threads: int):
-    """Time the oracle executor loop (CPU restatement of SPEC.md:418-426) on
-    the same schedule; returns (aggregate bus GB/s, seconds, runs)."""
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    d = json.loads(js)
-    ins = O.seeded_inputs(d["collective"], P, m, O.U8, 0)
-    ex = O.Execution(d, ins, m, O.U8, check=True)
-    ex.run(threads)  # warm-up
-    n, t0 = 0, time.perf_counter()
-    while True:
-        ex.run(threads)
-        n += 1
-        dt = time.perf_counter() - t0
-        if dt >= seconds:
-            break
-    return P * (P - 1) * m * n / dt / 1e9, dt, n
+    return O
 
 
+# --------------------------------------------------------------------------- reference arm (CPU)
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """The reference's own executor (restated in C under
+    oracle/) on the host cores, on the GPU arm's workload.  Rank 0 only."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     P = 8 if args.gpus == 1 else args.gpus
-    js, sname = schedule_for(P, args.schedule)
-    m = min(args.bytes, args.ref_bytes)
+    name = workload_schedule(P, args.schedule)
+    js = load_schedule(name)
+    m = args.ref_bytes if args.ref_bytes > 0 else args.bytes
     threads = os.cpu_count() or 1
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
+    O = _oracle()
     d = json.loads(js)
     ins = O.seeded_inputs(d["collective"], P, m, O.U8, 0)
-    ex = O.Execution(d, ins, m, O.U8, check=True)
+    ex = O.Execution(d, ins, m, O.U8, check=True)  # the oracle's own verify gate
     for _ in range(args.warmup):
         ex.run(threads)
     times = []
@@ -152,26 +174,78 @@ def run_reference(args):
         t0 = time.perf_counter()
         ex.run(threads)
         times.append(time.perf_counter() - t0)
-    tot = sum(times)
-    val = P * (P - 1) * m * args.steps / tot / 1e9
+    want = b"".join(x.tobytes() for x in ins)
+    out = ex.outputs()
+    assert out[0].tobytes() == want and out[P - 1].tobytes() == want, "reference executor result wrong"
+    t = sum(times) / len(times)
+    per_rank = busbytes("allgather", P, m) / t / 1e9
+    value = per_rank * (1 if args.gpus == 1 else P)
     sample = (f"oracle executor loop (SPEC.md:418-426 restated in C, {threads} threads) on {P} ranks x {m} B per "
-              f"rank of the same schedule ({sname}); bus bytes = P*(P-1)*m per step")
-    line = {"metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True,
+              f"rank, schedule file {name}.json; every step is one whole execution of the workload")
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * t, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded PRNG bytes)",
             "impl": "reference",
-            # the GPU arm's workload (same schedule, ranks and bytes per rank); each
-            # step runs the CPU executor on a bounded sample of it (sample_bytes_per_rank)
-            "config": {"workload": (f"{sname}; {P} ranks loopback on 1 B200 (all rank buffers in one HBM)"
-                                    if args.gpus == 1 else
-                                    f"{sname}; one rank per GPU, CUDA IPC peers over NVLink"),
-                       "ranks": P, "bytes_per_rank": args.bytes, "schedule": sname,
-                       "sample_bytes_per_rank": m, "executor": "CPU reference (oracle port)",
+            "config": {"workload": _workload_text(args.gpus, P, name), "ranks": P, "bytes_per_rank": m,
+                       "schedule": sched_label(name), "schedule_file": f"tests/golden/schedules/bench/{name}.json",
+                       "same_config": m == args.bytes, "executor": "CPU reference (oracle port)",
                        "parallelism": f"{threads} host threads"},
-            "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "aggregate_GBps": round(per_rank * P, 3),
+            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                              "sample": sample},
-            "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _workload_text(gpus: int, P: int, name: str) -> str:
+    if gpus == 1:
+        return f"{sched_label(name)}; {P} ranks loopback on 1 B200 (all rank buffers in one HBM)"
+    return f"{sched_label(name)}; one rank per GPU on {P} B200s, CUDA IPC peers over NVLink/NVSwitch"
+
+
+# --------------------------------------------------------------------------- GPU helpers
+def graph_time_us(plan, send, recv, stream, iters):
+    """Device time per launch: `iters` launches captured in one CUDA graph
+    (host launch cost excluded), replayed twice, the second replay timed."""
+    import torch
+    for _ in range(3):
+        plan.launch(send, recv, stream)
+    stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(iters):
+            plan.launch(send, recv, stream)
+    with torch.cuda.stream(stream):  # replay() launches on the current stream
+        g.replay()
+        stream.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+    stream.synchronize()
+    plan.check()
+    return a.elapsed_time(b) * 1e3 / iters
+
+
+def oracle_check_loopback(sccl, name, nbytes, dtype, seed=5):
+    """Bit-exact check of every rank's output against the CPU oracle on the
+    same schedule file (small size); returns {rank: digest_equal}."""
+    import numpy as np
+    import torch
+    O = _oracle()
+    js = load_schedule(name)
+    d = json.loads(js)
+    P = d["P"]
+    ins = O.seeded_inputs(d["collective"], P, nbytes, dtype, seed)
+    ref = O.execute(d, ins, nbytes, dtype)
+    plan = sccl.LoopbackPlan(js, nbytes, dtype, device=0)
+    send = [torch.from_numpy(x).cuda() for x in ins]
+    recv = [torch.zeros(r.size, dtype=torch.uint8, device="cuda") for r in ref]
+    plan.launch(send, recv)
+    torch.cuda.synchronize()
+    plan.check()
+    plan.close()
+    return all(O.digest([a.cpu().numpy()]) == O.digest([b]) for a, b in zip(recv, ref))
 
 
 # --------------------------------------------------------------------------- GPU, N = 1
@@ -181,7 +255,8 @@ def run_loopback(args):
     P = 8
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
-    js, sname = schedule_for(P, args.schedule)
+    name = workload_schedule(P, args.schedule)
+    js = load_schedule(name)
     m = args.bytes
     plan = sccl.LoopbackPlan(js, m, sccl.U8, device=0, nchannels=args.nchannels, tile_bytes=args.tile)
     info = plan.info()
@@ -193,16 +268,15 @@ def run_loopback(args):
         for _ in range(args.warmup):
             plan.launch(send, recv, stream)
     stream.synchronize()
-    # correctness of what is timed: every rank holds the concatenation
-    want = torch.cat(send)
+    want = torch.cat(send)  # every rank holds the concatenation
     assert all(torch.equal(r, want) for r in recv), "bench: allgather result wrong"
+    oracle_ok = oracle_check_loopback(sccl, name, 1 << 20, sccl.U8)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_all = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
-        # untimed soak under the sampler so the clock record sees this load
-        t_soak = time.perf_counter()
+        t_soak = time.perf_counter()  # untimed soak so the clock record sees this load
         while time.perf_counter() - t_soak < 0.6:
             for _ in range(8):
                 plan.launch(send, recv, stream)
@@ -217,137 +291,72 @@ def run_loopback(args):
         torch.cuda.synchronize()
     launches = plan.launch_count - n0
     plan.check()
-    total_ms = t_all[0].elapsed_time(t_all[1])
-    per = [a.elapsed_time(b) for a, b in ev]
-    ms = total_ms / args.steps
-    kern_ms = sum(per) / len(per)
-    bus = P * (P - 1) * m
-    value = bus / (ms * 1e-3) / 1e9
+    ms = t_all[0].elapsed_time(t_all[1]) / args.steps
+    kern_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    per_rank = busbytes("allgather", P, m) / (ms * 1e-3) / 1e9
     peaks, src = _peaks()
-    hbm = hbm_bytes_per_launch(plan)
-    achieved = hbm / (kern_ms * 1e-3) / 1e9
+    sched_bytes = hbm_bytes_per_launch(plan)
     min_b = P * m + P * P * m  # inputs read once + outputs written once
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(f"{args.schedule}:{m}")
-        except Exception:
-            traffic = None
+    traffic, traffic_src = _profile_traffic(f"{name}:{m}")
 
-    def time_us(p2, s2, r2, iters):
-        """device time per launch: `iters` launches captured in one CUDA
-        graph (no host launch overhead in the measurement), replayed twice,
-        the second replay timed with events"""
-        for _ in range(3):
-            p2.launch(s2, r2, stream)
-        stream.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for _ in range(iters):
-                p2.launch(s2, r2, stream)
-        with torch.cuda.stream(stream):  # replay() launches on the current stream
-            g.replay()
-            stream.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            g.replay()
-            b.record(stream)
-        stream.synchronize()
-        p2.check()
-        return a.elapsed_time(b) * 1e3 / iters
+    extra = {} if args.no_sweep else loopback_extras(args, sccl, plan, send, recv, stream, peaks)
+    e2e = loopback_e2e(args, plan, send, recv)
 
-    # latency sweep: the (7,7,7) schedule and the one-shot (1,1,1) per size
-    from paper_2008_08708_b200 import schedules as S
-    sweep = []
-    if not args.no_sweep:
-        one = S.to_json(S.one_shot_allgather(P))
-        for sz in (1 << 10, 8 << 10, 64 << 10, 1 << 20, 16 << 20):
-            row = {"bytes_per_rank": sz}
-            for tag, sj in (("777", js), ("oneshot", one)):
-                p2 = sccl.LoopbackPlan(sj, sz, sccl.U8, device=0)
-                us = time_us(p2, [x[:sz] for x in send], [x[:P * sz] for x in recv], 50 if sz < (1 << 20) else 10)
-                row[f"{tag}_us"] = round(us, 2)
-                row[f"{tag}_busbw_per_rank_GBps"] = round((P - 1) * sz / (us * 1e-6) / 1e9, 2)
-                row[f"{tag}_protocol"] = p2.info()["protocol"]
-                p2.close()
-            sweep.append(row)
+    cpu_m = min(m, args.cpu_bytes)
+    cpu_val, cpu_s, cpu_n = cpu_reference_run(P, js, cpu_m, args.cpu_seconds, 1)
+    line = {
+        "metric": METRIC, "value": round(per_rank, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
+        "config": {"workload": _workload_text(1, P, name), "ranks": P, "bytes_per_rank": m,
+                   "schedule": sched_label(name), "schedule_file": f"tests/golden/schedules/bench/{name}.json",
+                   "nchannels": info["nchannels"], "tile_bytes": info["tile_bytes"], "grid": info["grid"],
+                   "threads": info["threads"],
+                   "l2": f"no flush: inputs {P * m >> 20} MiB + outputs {P * P * m >> 20} MiB per step >> 126 MB L2",
+                   "parallelism": "loopback8",
+                   "value_convention": "per-rank bus GB/s (nccl-tests busBW, (P-1)*m/t); one GPU"},
+        "aggregate_GBps": round(per_rank * P, 2),
+        "oracle_check": {"bytes_per_rank": 1 << 20, "all_ranks_bit_exact": oracle_ok},
+        # algorithmic bytes = what any executor must move in one HBM: every
+        # rank's input read once, every rank's output written once.  The
+        # lowered (7,7,7) schedule also re-reads each relayed receipt to
+        # forward it (schedule_bytes); window-major execution serves most of
+        # those from L2, so ncu DRAM bytes land near the algorithmic bytes.
+        "roofline": {"bound": "hbm", "achieved": round(min_b / (kern_ms * 1e-3) / 1e9, 1), "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(min_b / (kern_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": src,
+                     "algorithmic_bytes_per_launch": min_b, "kernel_ms": round(kern_ms, 4),
+                     "schedule_bytes_per_launch": sched_bytes,
+                     "frac_schedule_bytes": round(sched_bytes / (kern_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)},
+        "cpu_baseline": {"value": round(cpu_val / P, 3), "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": f"oracle executor, same schedule file, {P} ranks x {cpu_m} B, {cpu_n} runs in "
+                                   f"{cpu_s:.1f} s, 1 thread (SPEC.md:447); per-rank bus GB/s"},
+        "e2e": e2e,
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    line.update(extra)
+    print(json.dumps(line), flush=True)
 
-    # BASELINE configs 3 and 4 on the same device (loopback, 64 MiB per rank)
-    extra = {}
-    if not args.no_sweep:
-        M = 64 << 20
-        xs = [x[:M] for x in send]
-        ys = [x[:M] for x in recv]
-        ag = S.hamiltonian_allgather(P)
-        for tag, sj, dt in (("allreduce_56_14_14_bf16", S.allreduce_from(ag), sccl.BF16),
-                            ("allreduce_8_2_2_bf16", S.allreduce_from(S.one_shot_allgather(P)), sccl.BF16),
-                            ("alltoall_8_1_1_u8", S.to_json(S.direct_alltoall(P)), sccl.U8)):
-            p2 = sccl.LoopbackPlan(sj, M, dt, device=0)
-            us = time_us(p2, xs, ys, 10)
-            busb = (2 * (P - 1) * M // P) if tag.startswith("allreduce") else ((P - 1) * M // P)
-            extra[tag] = {"bytes_per_rank": M, "us": round(us, 1),
-                          "busbw_per_rank_GBps": round(busb / (us * 1e-6) / 1e9, 1),
-                          "hbm_GBps": round(hbm_bytes_per_launch(p2) / (us * 1e-6) / 1e9, 1),
-                          "hbm_frac": round(hbm_bytes_per_launch(p2) / (us * 1e-6) / 1e9 / _peaks()[0]["hbm_gbs"], 3),
-                          # inputs read once + outputs written once
-                          "frac_of_min": round(2 * P * M / (us * 1e-6) / 1e9 / _peaks()[0]["hbm_gbs"], 3)}
-            # ncu dram__bytes_read+write of the same launch (profiles/traffic.json):
-            # receipt/relay slots consumed right after they land are served
-            # from L2, so the algorithmic count can exceed what reaches HBM
-            try:
-                dram = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(f"{tag}:{M}")
-            except Exception:
-                dram = None
-            if dram:
-                extra[tag]["dram_traffic"] = dram
-                extra[tag]["dram_frac"] = round(dram / (us * 1e-6) / 1e9 / _peaks()[0]["hbm_gbs"], 3)
-            p2.close()
 
-    # comparison point on the same device: the same lowered program run as
-    # per-op cudaMemcpyAsync device-to-device copies in step order on one
-    # stream (the paper's per-step copy lowering, PAPER.md:718) -- what a
-    # library-copy executor of the schedule achieves without the kernel
-    copy_engine = None
-    if not args.no_sweep and not info["protocol"] == "ll":
-        for r in recv:
-            r.zero_()
-        torch.cuda.synchronize()  # the zeroing ran on the default stream
-        plan.launch_copy_engine(send, recv, stream)
-        stream.synchronize()
-        assert all(torch.equal(r, want) for r in recv), "bench: copy-engine result wrong"
-        ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ca.record(stream)
-        for _ in range(3):
-            plan.launch_copy_engine(send, recv, stream)
-        cb.record(stream)
-        stream.synchronize()
-        ce_ms = ca.elapsed_time(cb) / 3
-        copy_engine = {"ms": round(ce_ms, 3), "value": round(bus / (ce_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
-                       "kernel_speedup": round(ce_ms / ms, 2),
-                       "note": "same lowered program, one cudaMemcpyAsync D2D per op output, step order, one stream"}
-
-    # e2e: through the public API with host buffers, every step:
-    #   H2D of all P ranks' inputs (pinned host -> device),
-    #   the collective,
-    #   D2H of the step's result: the gathered buffer (P*m bytes; every rank
-    #   holds the same one -- on an N-GPU box each GPU reads its own back over
-    #   its own PCIe link in parallel, so one copy is the per-GPU cost).
-    # Two buffer sets and three streams pipeline step i+1's H2D with step
-    # i's D2H; the timed region covers all steps end to end.
+def loopback_e2e(args, plan, send, recv):
+    """Through the public API with host buffers, every step: H2D of all P
+    ranks' inputs from pinned memory, the collective, D2H of ALL P ranks'
+    outputs (P*P*m bytes).  Two device buffer sets and three streams overlap
+    step i+1's H2D with step i's D2H; the timed region covers every step."""
+    import torch
+    P, m = len(send), send[0].numel()
     hsend = [[torch.empty(m, dtype=torch.uint8, pin_memory=True) for _ in range(P)] for _ in range(2)]
     for k in range(2):
         for h, x in zip(hsend[k], send):
             h.copy_(x.cpu())
-    hres = [torch.empty(P * m, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    hres = torch.empty(P * P * m, dtype=torch.uint8, pin_memory=True)  # every rank's output
     dsend = [send, [torch.empty_like(x) for x in send]]
     drecv = [recv, [torch.empty_like(x) for x in recv]]
     s_h2d, s_k, s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    # enough steps that the pipeline fill (one H2D before the first D2H) is
-    # a small part of the timed region
-    e2e_steps = max(8, min(2 * args.steps, 32))
+    steps = max(4, min(args.steps, 8))
 
-    def e2e_run(nsteps):
+    def run(nsteps):
         ev_in = [torch.cuda.Event() for _ in range(nsteps)]
         ev_k = [torch.cuda.Event() for _ in range(nsteps)]
         ev_out = [torch.cuda.Event() for _ in range(nsteps)]
@@ -366,96 +375,273 @@ def run_loopback(args):
             ev_k[i].record(s_k)
             s_d2h.wait_event(ev_k[i])
             with torch.cuda.stream(s_d2h):
-                hres[k].copy_(drecv[k][i % P], non_blocking=True)
+                for r in range(P):
+                    hres[r * P * m:(r + 1) * P * m].copy_(drecv[k][r], non_blocking=True)
                 ev_out[i].record(s_d2h)
         return ev_out[-1]
 
-    e2e_run(2)
+    run(2)
     torch.cuda.synchronize()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(s_h2d)
     s_k.wait_event(a)
     s_d2h.wait_event(a)
-    last = e2e_run(e2e_steps)
+    last = run(steps)
     s_h2d.wait_event(last)
     b.record(s_h2d)
     torch.cuda.synchronize()
-    e2e_ms = a.elapsed_time(b) / e2e_steps
-    assert torch.equal(hres[(e2e_steps - 1) % 2], want.cpu()), "e2e result wrong"
-    e2e_val = bus / (e2e_ms * 1e-3) / 1e9
+    e2e_ms = a.elapsed_time(b) / steps
+    wc = torch.cat(hsend[0])  # both host input sets hold the same bytes
+    assert all(torch.equal(hres[r * P * m:(r + 1) * P * m], wc) for r in range(P)), "e2e result wrong"
+    return {"value": round(busbytes("allgather", P, m) / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": P * m, "d2h_bytes_per_step": P * P * m, "ms_per_step": round(e2e_ms, 3),
+            "note": "per-rank bus GB/s through LoopbackPlan.launch with host buffers: H2D of all ranks' inputs + "
+                    "collective + D2H of all ranks' outputs (8 GiB) every step, over one PCIe link; "
+                    "pipelined over 2 device buffer sets / 3 streams"}
 
-    # CPU baseline (oracle, 1 thread as the reference executor is specified)
-    cpu_m = min(m, args.cpu_bytes)
-    cpu_val, cpu_s, cpu_n = cpu_reference_run(P, js, cpu_m, args.cpu_seconds, 1)
 
-    line = {
-        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
-        "config": {"workload": f"{sname}; {P} ranks loopback on 1 B200 (all rank buffers in one HBM)",
-                   "ranks": P, "bytes_per_rank": m, "schedule": sname, "nchannels": info["nchannels"],
-                   "tile_bytes": info["tile_bytes"], "grid": info["grid"], "threads": info["threads"],
-                   "l2": f"no flush: inputs {P * m >> 20} MiB + outputs {P * P * m >> 20} MiB per step >> 126 MB L2",
-                   "parallelism": "loopback8"},
-        "busbw_per_rank_GBps": round((P - 1) * m / (ms * 1e-3) / 1e9, 2),
-        # algorithmic bytes = what any executor must move in one HBM: every
-        # rank's input read once, every rank's output written once.  The
-        # lowered (7,7,7) schedule also re-reads each relayed receipt to
-        # forward it (schedule_bytes); window-major execution serves most of
-        # those re-reads from L2, so `traffic` (ncu DRAM bytes) lands near
-        # the algorithmic bytes rather than the schedule's.
-        "roofline": {"bound": "hbm", "achieved": round(min_b / (kern_ms * 1e-3) / 1e9, 1), "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(min_b / (kern_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
-                     "traffic": traffic, "peak_source": src, "algorithmic_bytes_per_launch": min_b,
-                     "kernel_ms": round(kern_ms, 4), "schedule_bytes_per_launch": hbm,
-                     "frac_schedule_bytes": round(achieved / peaks["hbm_gbs"], 4),
-                     "note": "algorithmic = inputs read once + outputs written once (P*m + P*P*m); "
-                             "schedule_bytes adds the relay re-reads the lowered schedule prescribes, which "
-                             "window-major execution mostly serves from L2 (traffic = ncu DRAM bytes)"},
-        "cpu_baseline": {"value": round(cpu_val, 3), "unit": "GB/s", "cores": 1, "kind": "port",
-                         "sample": f"oracle executor, same schedule, {P} ranks x {cpu_m} B, {cpu_n} runs in "
-                                   f"{cpu_s:.1f} s, 1 thread (SPEC.md:447)"},
-        "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": P * m,
-                "d2h_bytes_per_step": P * m, "ms_per_step": round(e2e_ms, 3),
-                "note": "H2D of all ranks' inputs + collective + D2H of the gathered result buffer, "
-                        "pipelined over 2 buffer sets / 3 streams"},
-        "clocks": clk.summary(),
-        "gpu_launches": launches,
-        "latency_sweep": sweep,
-        "other_collectives": extra,
-        "copy_engine_baseline": copy_engine,
-    }
-    print(json.dumps(line), flush=True)
+def loopback_extras(args, sccl, plan, send, recv, stream, peaks):
+    """BASELINE configs 1, 3, 4 and the latency sweep on the same device."""
+    import torch
+    P = 8
+    out = {}
+    pk = peaks["hbm_gbs"]
+    # latency sweep (CUDA-graph timed): allgathers, allreduces, alltoall
+    sweep = []
+    for sz in (1 << 10, 8 << 10, 64 << 10, 1 << 20, 16 << 20):
+        row = {"bytes_per_rank": sz}
+        for tag, nm, dt in (("ag777", "ag_ham_full8", sccl.U8), ("ag111", "ag_oneshot_full8", sccl.U8),
+                            ("ar822_bf16", "ar_oneshot_full8", sccl.BF16), ("ar56_bf16", "ar_ham_full8", sccl.BF16),
+                            ("a2a881", "a2a_direct_full8", sccl.U8)):
+            p2 = sccl.LoopbackPlan(load_schedule(nm), sz, dt, device=0)
+            coll = json.loads(load_schedule(nm))["collective"]
+            us = graph_time_us(p2, [x[:p2.send_bytes] for x in send], [x[:p2.recv_bytes] for x in recv], stream,
+                               50 if sz < (1 << 20) else 10)
+            row[f"{tag}_us"] = round(us, 2)
+            row[f"{tag}_busbw_per_rank_GBps"] = round(busbytes(coll, P, sz) / (us * 1e-6) / 1e9, 2)
+            row[f"{tag}_protocol"] = p2.info()["protocol"]
+            p2.close()
+        sweep.append(row)
+    out["latency_sweep"] = sweep
+
+    # configs 3 and 4 at 64 MiB per rank (HBM floor = inputs once + outputs once)
+    M = 64 << 20
+    xs, ys = [x[:M] for x in send], [x[:M] for x in recv]
+    oc = {}
+    for tag, nm, dt in (("allreduce_56_14_14_bf16", "ar_ham_full8", sccl.BF16),
+                        ("allreduce_56_14_14_f32", "ar_ham_full8", sccl.F32),
+                        ("allreduce_8_2_2_bf16", "ar_oneshot_full8", sccl.BF16),
+                        ("allreduce_8_2_2_f32", "ar_oneshot_full8", sccl.F32),
+                        ("allreduce_ring_8_14_14_bf16", "ar_ring_ring8", sccl.BF16),
+                        ("alltoall_8_1_1_u8", "a2a_direct_full8", sccl.U8)):
+        p2 = sccl.LoopbackPlan(load_schedule(nm), M, dt, device=0)
+        coll = json.loads(load_schedule(nm))["collective"]
+        us = graph_time_us(p2, xs, ys, stream, 10)
+        floor = 2 * P * M
+        oc[tag] = {"bytes_per_rank": M, "us": round(us, 1),
+                   "busbw_per_rank_GBps": round(busbytes(coll, P, M) / (us * 1e-6) / 1e9, 1),
+                   "frac_of_hbm_floor": round(floor / (us * 1e-6) / 1e9 / pk, 3),
+                   "schedule_bytes_GBps": round(hbm_bytes_per_launch(p2) / (us * 1e-6) / 1e9, 1),
+                   "pull": p2.info()["pull"], "grid": p2.info()["grid"]}
+        dram, dsrc = _profile_traffic(f"{nm}:{dt}:{M}")
+        if dram:
+            oc[tag]["dram_traffic"] = dram
+            oc[tag]["dram_traffic_source"] = dsrc
+        p2.close()
+    out["other_collectives"] = oc
+    out["allreduce_e2e"] = allreduce_e2e(sccl, xs, ys, stream)
+
+    # config 1: ring(8) latency-optimal allgathers at 1 MiB per rank, the CPU
+    # reference executor (1 thread and all threads) beside the GPU executor,
+    # with the host memcpy roofline of the CPU side
+    O = _oracle()
+    c1 = {}
+    m1 = 1 << 20
+    threads = os.cpu_count() or 1
+    memcpy_gbs = O.lib().oracle_memcpy_bw(64 << 20, threads, 5) / 1e9
+    for nm in ("ag_bidir_ring8", "ag_ring8_2_4_7"):
+        js = load_schedule(nm)
+        d = json.loads(js)
+        p2 = sccl.LoopbackPlan(js, m1, sccl.U8, device=0)
+        us = graph_time_us(p2, [x[:m1] for x in send], [x[:P * m1] for x in recv], stream, 50)
+        p2.close()
+        ins = O.seeded_inputs("allgather", P, m1, O.U8, 0)
+        ex = O.Execution(d, ins, m1, O.U8, check=True)
+        row = {"gpu_us": round(us, 2)}
+        for th in (1, threads):
+            ex.run(th)
+            ts = []
+            for _ in range(20):
+                t0 = time.perf_counter()
+                ex.run(th)
+                ts.append(time.perf_counter() - t0)
+            row[f"cpu_{th}t_us_median"] = round(1e6 * statistics.median(ts), 1)
+            row[f"cpu_{th}t_us_min"] = round(1e6 * min(ts), 1)
+        # host bytes the CPU executor moves: every receipt read + written, plus the local slots
+        host_bytes = 2 * (len(d["sends"]) * m1 // (d["G"] // P))
+        row["cpu_host_bytes"] = host_bytes
+        row["cpu_memcpy_roofline_us"] = round(host_bytes / (memcpy_gbs * 1e9) * 1e6, 1)
+        c1[f"{nm} ({d['C']},{d['S']},{d['R']})"] = row
+    c1["host_memcpy_GBps"] = round(memcpy_gbs, 1)
+    c1["host_threads"] = threads
+    out["config1_cpu_vs_gpu_1MiB"] = c1
+
+    # the same lowered program as per-op cudaMemcpyAsync copies (the paper's
+    # per-step copy lowering, PAPER.md:718): a library-copy executor's speed
+    if plan.info()["protocol"] != "ll":
+        for r in recv:
+            r.zero_()
+        torch.cuda.synchronize()
+        plan.launch_copy_engine(send, recv, stream)
+        stream.synchronize()
+        want = torch.cat(send)
+        assert all(torch.equal(r, want) for r in recv), "bench: copy-engine result wrong"
+        ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ca.record(stream)
+        for _ in range(3):
+            plan.launch_copy_engine(send, recv, stream)
+        cb.record(stream)
+        stream.synchronize()
+        ce_ms = ca.elapsed_time(cb) / 3
+        m = send[0].numel()
+        out["copy_engine_baseline"] = {
+            "ms": round(ce_ms, 3), "busbw_per_rank_GBps": round(busbytes("allgather", P, m) / (ce_ms * 1e-3) / 1e9, 2),
+            "note": "same lowered program, one cudaMemcpyAsync D2D per op output, step order, one stream"}
+        plan.launch(send, recv, stream)  # leave the plan's buffers in the kernel's state
+        stream.synchronize()
+    return out
+
+
+def allreduce_e2e(sccl, xs, ys, stream):
+    """BASELINE config 3 end to end: allreduce (8,2,2) bf16 at 64 MiB per
+    rank through the public API with host buffers (H2D every rank's input,
+    D2H every rank's output, per step), with the CPU reference executor on a
+    bounded sample beside it."""
+    import torch
+    P, M = len(xs), xs[0].numel()
+    nm = "ar_oneshot_full8"
+    plan = sccl.LoopbackPlan(load_schedule(nm), M, sccl.BF16, device=0)
+    hin = [torch.randint(-16, 17, (M // 2,), dtype=torch.int16).to(torch.bfloat16).view(torch.uint8).pin_memory()
+           for _ in range(P)]
+    hout = torch.empty(P * M, dtype=torch.uint8, pin_memory=True)
+    steps = 5
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for i in range(steps + 1):
+            if i == 1:
+                a.record(stream)
+            for h, x in zip(hin, xs):
+                x.copy_(h, non_blocking=True)
+            plan.launch(xs, ys, stream)
+            for r in range(P):
+                hout[r * M:(r + 1) * M].copy_(ys[r], non_blocking=True)
+        b.record(stream)
+    stream.synchronize()
+    plan.check()
+    plan.close()
+    ms = a.elapsed_time(b) / steps
+    want = torch.stack([h.view(torch.bfloat16).double() for h in hin]).sum(0).to(torch.bfloat16).view(torch.uint8)
+    assert all(torch.equal(hout[r * M:(r + 1) * M], want) for r in range(P)), "allreduce e2e wrong"
+    # CPU reference on a bounded sample (4 MiB per rank, 1 thread and all threads)
+    O = _oracle()
+    d = json.loads(load_schedule(nm))
+    ms_cpu = {}
+    for th in (1, os.cpu_count() or 1):
+        ins = O.seeded_inputs("allreduce", P, 4 << 20, O.BF16, 0)
+        ex = O.Execution(d, ins, 4 << 20, O.BF16, check=True)
+        ex.run(th)
+        t0 = time.perf_counter()
+        for _ in range(5):
+            ex.run(th)
+        ms_cpu[th] = (time.perf_counter() - t0) / 5 * 1e3
+    bb = busbytes("allreduce", P, M)
+    return {"workload": "allreduce (8,2,2) bf16, 64 MiB per rank, 8 loopback ranks",
+            "e2e": {"value": round(bb / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": P * M,
+                    "d2h_bytes_per_step": P * M, "ms_per_step": round(ms, 3)},
+            "cpu_baseline": [{"value": round(busbytes("allreduce", P, 4 << 20) / (t * 1e-3) / 1e9, 3), "unit": "GB/s",
+                              "cores": th, "kind": "port",
+                              "sample": "oracle executor, ar_oneshot_full8, 8 ranks x 4 MiB bf16, per-rank bus GB/s"}
+                             for th, t in ms_cpu.items()]}
+
+
+# --------------------------------------------------------------------------- CPU reference (bounded)
+def cpu_reference_run(P: int, js: str, m: int, seconds: float, threads: int):
+    """Time the oracle executor loop on the same schedule; returns
+    (aggregate bus GB/s over the P ranks, seconds, runs)."""
+    O = _oracle()
+    d = json.loads(js)
+    ins = O.seeded_inputs(d["collective"], P, m, O.U8, 0)
+    ex = O.Execution(d, ins, m, O.U8, check=True)
+    ex.run(threads)  # warm-up
+    n, t0 = 0, time.perf_counter()
+    while True:
+        ex.run(threads)
+        n += 1
+        dt = time.perf_counter() - t0
+        if dt >= seconds:
+            break
+    return P * busbytes("allgather", P, m) * n / dt / 1e9, dt, n
 
 
 # --------------------------------------------------------------------------- GPU, N > 1
+def nvlink_counters(index: int):
+    """NVML NVLink 5 byte counters of GPU `index`, summed over its links:
+    (tx bytes, rx bytes, field source) or None.  Fields 202 / 204
+    (NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / _RCV_BYTES) per link; fallback
+    138 / 139 (THROUGHPUT_DATA_TX / RX, KiB)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        for tx_id, rx_id, scale in ((202, 204, 1), (138, 139, 1024)):
+            try:
+                reqs = [(tx_id, l) for l in range(18)] + [(rx_id, l) for l in range(18)]
+                vals = pynvml.nvmlDeviceGetFieldValues(h, reqs)
+                tx = rx = 0
+                ok = 0
+                for req, v in zip(reqs, vals):
+                    if v.nvmlReturn != 0:
+                        continue
+                    ok += 1
+                    x = int(v.value.ullVal) * scale
+                    if req[0] == tx_id:
+                        tx += x
+                    else:
+                        rx += x
+                if ok:
+                    return tx, rx, f"NVML field {tx_id}/{rx_id} over {ok // 2} links"
+            except Exception:
+                continue
+    except Exception:
+        return None
+    return None
+
+
 def run_multi(args):
     import torch
     import torch.distributed as dist
     from paper_2008_08708_b200 import sccl
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    # SCCL_BENCH_SHARE_GPU=1: every rank on cuda:0 (validates this multi-process
-    # path on a 1-GPU box: IPC peers, sys-scope flags, the JSON line).  The
-    # ranks time-slice one GPU, so its numbers are not performance; NCCL
-    # refuses duplicate GPUs, so the process group is gloo and the NCCL
-    # comparison is skipped.
+    # SCCL_BENCH_SHARE_GPU=1: every rank on cuda:0 (validates this path on a
+    # one-GPU box; the ranks time-slice one GPU, so its numbers are not
+    # performance).  NCCL refuses duplicate GPUs: gloo, no NCCL baselines.
     shared = os.environ.get("SCCL_BENCH_SHARE_GPU") == "1"
-    if shared:
-        local = 0
-    torch.cuda.set_device(local)
+    dev_index = 0 if shared else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if shared:
         dist.init_process_group("gloo")
     else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
     P = world
-    js, sname = schedule_for(P, args.schedule)
+    name = workload_schedule(P, args.schedule)
+    js = load_schedule(name)
     m = args.bytes
-    plan = sccl.Plan(js, rank, P, m, sccl.U8, device=local, nchannels=args.nchannels, tile_bytes=args.tile,
+    plan = sccl.Plan(js, rank, P, m, sccl.U8, device=dev_index, nchannels=args.nchannels, tile_bytes=args.tile,
                      mem_handles=args.mem)
     plan.bind_with()
-    dev = torch.device("cuda", local)
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
     send = torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev, generator=g)
@@ -464,16 +650,10 @@ def run_multi(args):
     for _ in range(args.warmup):
         plan.launch(send, recv, stream)
     torch.cuda.synchronize()
-    if shared:
-        parts = [torch.empty(m, dtype=torch.uint8) for _ in range(P)]
-        dist.all_gather(parts, send.cpu())
-        ref = torch.cat(parts).to(dev)
-    else:
-        ref = torch.empty(P * m, dtype=torch.uint8, device=dev)
-        dist.all_gather_into_tensor(ref, send)
-    torch.cuda.synchronize()
+    ref = gather_ref(dist, send, P, shared, dev)
     assert torch.equal(ref, recv), f"rank {rank}: allgather differs from the gathered inputs"
     regptr, _ = plan.recv_buffer()
+    oracle_ok = multi_oracle_check(dist, sccl, rank, P, dev_index, args.mem)
 
     def timed(fn, steps):
         dist.barrier()
@@ -489,15 +669,23 @@ def run_multi(args):
         return float(t)
 
     n0 = plan.launch_count
-    with ClockSampler(local) as clk:
+    nv0 = nvlink_counters(dev_index)
+    with ClockSampler(dev_index) as clk:
         ms = timed(lambda: plan.launch(send, regptr, stream), args.steps)
+    nv1 = nvlink_counters(dev_index)
     launches = plan.launch_count - n0
-    ms_nccl = None if shared else timed(lambda: dist.all_gather_into_tensor(ref, send), args.steps)
     plan.check()
-    bus = P * (P - 1) * m
-    value = bus / (ms * 1e-3) / 1e9
-    per_gpu = (P - 1) * m / (ms * 1e-3) / 1e9
-    # e2e through the public API with pinned host buffers
+    per_rank = busbytes("allgather", P, m) / (ms * 1e-3) / 1e9
+    traffic = None
+    traffic_src = None
+    if nv0 and nv1 and not shared:
+        traffic = (nv1[0] - nv0[0]) / args.steps  # TX bytes per launch of this GPU
+        traffic_src = f"{nv1[2]}, TX bytes per launch around the timed region (rank {rank})"
+    traffic_all = [None] * P
+    dist.all_gather_object(traffic_all, traffic)
+
+    # e2e through the public API with pinned host buffers: this rank's input
+    # H2D, the collective, this rank's whole output D2H, every step
     hs = torch.empty(m, dtype=torch.uint8, pin_memory=True)
     hs.copy_(send.cpu())
     hr = torch.empty(P * m, dtype=torch.uint8, pin_memory=True)
@@ -507,27 +695,178 @@ def run_multi(args):
         plan.launch(send, recv, stream)
         hr.copy_(recv, non_blocking=True)
     e2e_ms = timed(e2e_step, max(3, min(args.steps, 10)))
+    baselines = {} if (shared or args.no_sweep) else nccl_baselines(args, dist, sccl, rank, P, dev, dev_index,
+                                                                     send, ref, ms, timed)
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": P, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
-            "config": {"workload": f"{sname}; one rank per GPU, CUDA IPC peers over NVLink", "ranks": P,
-                       "bytes_per_rank": m, "parallelism": f"ranks{P}", "nchannels": plan.info()["nchannels"],
-                       "l2": "no flush: buffers >> L2",
-                       "shared_gpu": shared, "mem_handles": args.mem},
-            "busbw_per_rank_GBps": round(per_gpu, 2),
-            "nccl": None if shared else {"ms": round(ms_nccl, 4),
-                                         "busbw_per_rank_GBps": round((P - 1) * m / (ms_nccl * 1e-3) / 1e9, 2)},
-            "roofline": {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": 900.0, "unit": "GB/s",
-                         "frac": round(per_gpu / 900.0, 4), "traffic": None,
+            "metric": METRIC, "value": round(per_rank * P, 2), "unit": "GB/s", "n_gpus": 1 if shared else P,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
+            "config": {"workload": (f"{sched_label(name)}; {P} ranks as {P} processes time-sliced on ONE GPU "
+                                    "(multi-process path validation, not performance)") if shared
+                       else _workload_text(P, P, name),
+                       "ranks": P, "bytes_per_rank": m, "schedule_file": f"tests/golden/schedules/bench/{name}.json",
+                       "parallelism": f"ranks{P}", "nchannels": plan.info()["nchannels"],
+                       "l2": "no flush: buffers >> L2", "shared_gpu": shared, "mem_handles": args.mem,
+                       "value_convention": "sum over GPUs of per-rank bus GB/s (nccl-tests busBW)"},
+            "busbw_per_rank_GBps": round(per_rank, 2),
+            "oracle_check": {"bytes_per_rank": 65536, "ranks_bit_exact": oracle_ok},
+            "roofline": {"bound": "nvlink", "achieved": round(per_rank, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
+                         "frac": round(per_rank / NVLINK_PEAK, 4), "traffic": traffic_all[0],
+                         "traffic_per_rank": traffic_all, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": busbytes("allgather", P, m),
                          "peak_source": "nominal NVLink 5 per direction per GPU"},
-            "e2e": {"value": round(bus / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": P * m,
-                    "d2h_bytes_per_step": P * P * m},
+            "e2e": {"value": round(busbytes("allgather", P, m) * P / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": P * m, "d2h_bytes_per_step": P * P * m,
+                    "note": "every rank: H2D of its input + collective + D2H of its whole output, per step; "
+                            "sum over GPUs"},
             "clocks": clk.summary(), "gpu_launches": launches,
         }
+        line.update(baselines)
         print(json.dumps(line), flush=True)
+    plan.close()
     dist.destroy_process_group()
+
+
+def gather_ref(dist, send, P, shared, dev):
+    import torch
+    m = send.numel()
+    if shared:
+        parts = [torch.empty(m, dtype=torch.uint8) for _ in range(P)]
+        dist.all_gather(parts, send.cpu())
+        return torch.cat(parts).to(dev)
+    ref = torch.empty(P * m, dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(ref, send)
+    torch.cuda.synchronize()
+    return ref
+
+
+def multi_oracle_check(dist, sccl, rank, P, dev_index, mem):
+    """Every rank's output of the workload schedule at 64 KiB per rank against
+    the CPU oracle's (digest); returns the per-rank results (rank 0)."""
+    import torch
+    O = _oracle()
+    name = workload_schedule(P, "auto")
+    js = load_schedule(name)
+    d = json.loads(js)
+    nb = 65536
+    ins = O.seeded_inputs(d["collective"], P, nb, O.U8, 9)
+    want = O.execute(d, ins, nb, O.U8)[rank]
+    plan = sccl.Plan(js, rank, P, nb, sccl.U8, device=dev_index, mem_handles=mem)
+    plan.bind_with()
+    recv = torch.zeros(want.size, dtype=torch.uint8, device=f"cuda:{dev_index}")
+    plan.launch(torch.from_numpy(ins[rank]).to(recv.device), recv)
+    torch.cuda.synchronize()
+    plan.check()
+    ok = O.digest([recv.cpu().numpy()]) == O.digest([want])
+    plan.close()
+    res = [None] * P
+    dist.all_gather_object(res, ok)
+    return res
+
+
+def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours, timed):
+    """Same-box NCCL (NCCL_PROTO=Simple; alltoall
+    as grouped send/recv) beside the executor, each timed
+    the same way (max over ranks).  Every NCCL configuration gets its own
+    communicator, created while its NCCL_* variables are set."""
+    import torch
+    m = send.numel()
+
+    def group_with(env):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            grp = dist.new_group(backend="nccl")
+            t = torch.zeros(1, device=dev)
+            dist.all_reduce(t, group=grp)  # the communicator is created now, with env in force
+            torch.cuda.synchronize()
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        return grp
+
+    out = {}
+    g_simple = group_with({"NCCL_PROTO": "Simple"})
+    g_ring = group_with({"NCCL_ALGO": "Ring"})
+    g_tree = group_with({"NCCL_ALGO": "Tree"})
+    bw = lambda coll, nbytes, t: round(busbytes(coll, P, nbytes) / (t * 1e-3) / 1e9, 2)
+
+    # allgather at the workload size
+    ag = {"ours_ms": round(ms_ours, 4), "ours_busbw": bw("allgather", m, ms_ours)}
+    for tag, grp in (("nccl_default", None), ("nccl_simple", g_simple)):
+        t = timed(lambda: dist.all_gather_into_tensor(ref, send, group=grp), args.steps)
+        ag[f"{tag}_ms"], ag[f"{tag}_busbw"] = round(t, 4), bw("allgather", m, t)
+    out["nccl_allgather"] = ag
+
+    # allreduce bf16 at 64 MiB: our one-shot (and Hamiltonian at P=8) vs NCCL Ring / Tree / default
+    M = 64 << 20
+    x = torch.randint(-16, 17, (M // 2,), device=dev).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    ar = {"bytes_per_rank": M}
+    for nm in ([f"ar_oneshot_full{P}"] + ([f"ar_ham_full{P}"] if P in (2, 8) else [])):
+        p2 = sccl.Plan(load_schedule(nm), rank, P, M, sccl.BF16, device=dev_index, mem_handles=args.mem)
+        p2.bind_with()
+        reg, _ = p2.recv_buffer()
+        p2.launch(x.view(torch.uint8), reg)
+        t = timed(lambda: p2.launch(x.view(torch.uint8), reg), args.steps)
+        p2.launch(x.view(torch.uint8), y.view(torch.uint8))
+        torch.cuda.synchronize()
+        z = x.clone()
+        dist.all_reduce(z)
+        torch.cuda.synchronize()
+        assert torch.equal(y, z), f"rank {rank}: {nm} differs from NCCL all_reduce"
+        ar[f"ours_{nm}_ms"], ar[f"ours_{nm}_busbw"] = round(t, 4), bw("allreduce", M, t)
+        p2.close()
+    for tag, grp in (("nccl_default", None), ("nccl_ring", g_ring), ("nccl_tree", g_tree), ("nccl_simple", g_simple)):
+        z = x.clone()
+        t = timed(lambda: dist.all_reduce(z, group=grp), args.steps)
+        ar[f"{tag}_ms"], ar[f"{tag}_busbw"] = round(t, 4), bw("allreduce", M, t)
+    out["nccl_allreduce_bf16"] = ar
+
+    # alltoall at 64 MiB: direct (P,1,1) vs NCCL grouped send/recv
+    a_in = torch.randint(0, 256, (M,), dtype=torch.uint8, device=dev)
+    a_out = torch.empty_like(a_in)
+    p3 = sccl.Plan(load_schedule(f"a2a_direct_full{P}"), rank, P, M, sccl.U8, device=dev_index, mem_handles=args.mem)
+    p3.bind_with()
+    reg3, _ = p3.recv_buffer()
+    t = timed(lambda: p3.launch(a_in, reg3), args.steps)
+    p3.launch(a_in, a_out)
+    chk = torch.empty_like(a_in)
+    dist.all_to_all_single(chk, a_in)
+    torch.cuda.synchronize()
+    assert torch.equal(chk, a_out), f"rank {rank}: alltoall differs from NCCL"
+    tn = timed(lambda: dist.all_to_all_single(chk, a_in), args.steps)
+    out["nccl_alltoall"] = {"bytes_per_rank": M, "ours_ms": round(t, 4), "ours_busbw": bw("alltoall", M, t),
+                            "nccl_ms": round(tn, 4), "nccl_busbw": bw("alltoall", M, tn)}
+    p3.close()
+
+    # latency sweep (<= 64 KB) and bandwidth points (>= 64 MB): allgather with
+    # the cost model's per-size choice among this P's schedule files
+    cands = [n for n in (f"ag_oneshot_full{P}", f"ag_ring_ring{P}", f"ag_ham_full{P}")
+             if os.path.exists(os.path.join(SCHED_DIR, n + ".json"))]
+    texts = [load_schedule(n) for n in cands]
+    sweep = []
+    for sz in (1 << 10, 4 << 10, 16 << 10, 64 << 10, 1 << 20, 64 << 20, 256 << 20):
+        i, proto, _ = sccl.select(texts, sz, sccl.U8, multiprocess=True)
+        p4 = sccl.Plan(texts[i], rank, P, sz, sccl.U8, device=dev_index, protocol=proto, mem_handles=args.mem)
+        p4.bind_with()
+        reg4, _ = p4.recv_buffer()
+        s4 = send[:sz]
+        r4 = ref[:P * sz]
+        iters = 200 if sz <= (64 << 10) else 20
+        t = timed(lambda: p4.launch(s4, reg4), iters)
+        tn = timed(lambda: dist.all_gather_into_tensor(r4, s4), iters)
+        tns = timed(lambda: dist.all_gather_into_tensor(r4, s4, group=g_simple), iters)
+        sweep.append({"bytes_per_rank": sz, "schedule": cands[i], "protocol": proto, "ours_us": round(t * 1e3, 2),
+                      "nccl_us": round(tn * 1e3, 2), "nccl_simple_us": round(tns * 1e3, 2),
+                      "ours_busbw": bw("allgather", sz, t), "nccl_busbw": bw("allgather", sz, tn)})
+        p4.close()
+    out["allgather_sweep_vs_nccl"] = sweep
+    return out
 
 
 def main():
@@ -537,20 +876,19 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--bytes", type=int, default=128 << 20, help="per-rank allgather input")
-    ap.add_argument("--schedule", default="auto", choices=["auto", "777", "oneshot", "ring"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "ham", "oneshot", "ring"])
     ap.add_argument("--nchannels", type=int, default=0)
     ap.add_argument("--mem", default="ipc", choices=["ipc", "vmm"],
                     help="N>1: share plan regions through CUDA IPC handles or VMM (cuMem) fds")
     ap.add_argument("--tile", type=int, default=0)
-    ap.add_argument("--ref-bytes", type=int, default=16 << 20)
+    ap.add_argument("--ref-bytes", type=int, default=0,
+                    help="--impl reference: bytes per rank (0 = the GPU arm's --bytes)")
     ap.add_argument("--cpu-bytes", type=int, default=16 << 20)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.gpus == 1 and args.schedule == "auto":
-        args.schedule = "777"
     if args.impl == "reference":
         run_reference(args)
     elif args.gpus == 1 and "WORLD_SIZE" not in os.environ or os.environ.get("WORLD_SIZE") == "1":

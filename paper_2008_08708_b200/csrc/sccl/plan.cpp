@@ -14,6 +14,7 @@
 #include "../../../include/sccl_exec.h"
 #include "error.hpp"
 #include "layout.hpp"
+#include "policy.hpp"
 
 namespace sccl {
 cudaError_t launch_exec(const KParams& p, int dtype, bool sys, cudaStream_t st);
@@ -71,26 +72,28 @@ int esize_of(int dtype) {
   throw sccl::invalid_argument_error("unknown dtype");
 }
 
-// predicted time (us) of a lowered program, see plan_build_host.  sys:
-// system-scope signalling (multi-process mode), whose release fences make
-// every bulk-protocol step ~3.6 us dearer (fit with SCCL_LOOPBACK_SYS=1).
-double predict_us(const sccl::Program& pg, int steps, bool ll, bool sys = false) {
-  double mb = 0;
-  for (auto& rp : pg.ranks)
-    for (auto& op : rp.ops)
-      if (op.kind != sccl::OP_WAIT) mb += double(op.len) * double(op.ins.size() + op.outs.size());
-  mb /= 1e6;
-  // tools/fit_protocol.py over tools/gpu_runs/proto_refit_round1w.sh
-  if (ll) return sys ? 4.79 + 0.520 * steps + 0.353 * mb : 4.80 + 0.522 * steps + 0.353 * mb;
-  return sys ? 5.00 + 6.33 * steps + 0.163 * mb : 4.50 + 2.72 * steps + 0.126 * mb;
-}
-
 bool loopback_sys() {  // SCCL_LOOPBACK_SYS=1: loopback launches use system scope (measurement only)
   static const bool v = [] {
     const char* e = std::getenv("SCCL_LOOPBACK_SYS");
     return e && std::atoi(e) != 0;
   }();
   return v;
+}
+
+// The policy table whose protocol constants price a plan: system-scope
+// signalling (multi-process, or loopback under SCCL_LOOPBACK_SYS) makes every
+// bulk-protocol step dearer.
+const sccl::ModePolicy& signal_policy(bool loopback) { return sccl::mode_policy(loopback && !loopback_sys()); }
+
+// predicted time (us) of a lowered program, see plan_build_host
+double predict_us(const sccl::Program& pg, int steps, bool ll, const sccl::ModePolicy& pol) {
+  double mb = 0;
+  for (auto& rp : pg.ranks)
+    for (auto& op : rp.ops)
+      if (op.kind != sccl::OP_WAIT) mb += double(op.len) * double(op.ins.size() + op.outs.size());
+  mb /= 1e6;
+  if (ll) return pol.ll_c + pol.ll_alpha * steps + pol.ll_beta * mb;
+  return pol.simple_c + pol.simple_alpha * steps + pol.simple_beta * mb;
 }
 
 // Driver-API VMM entry points, resolved at run time through the runtime
@@ -203,10 +206,10 @@ ProgramStats program_stats(const Schedule& sched, const Program& pg, bool loopba
   return st;
 }
 
-// A launch streams when its program moves > 1 GB: past the 126 MB L2, the
-// window-major order, L2 hints, receipt discards and the stage choice for
-// streaming reductions pay; below it the data stays L2-resident.
-constexpr double kStreamBytes = 1e9;
+// A launch streams when its program moves > ModePolicy::stream_bytes (1 GB):
+// past the 126 MB L2, the window-major order, L2 hints, receipt discards and
+// the stage choice for streaming reductions pay; below it the data stays
+// L2-resident.
 
 // Protocol (auto): lower both ways and take the smaller predicted time
 // t = c + alpha*S + beta*MB (S = schedule steps, MB = bytes the lowered
@@ -223,8 +226,8 @@ bool choose_ll(sccl_plan& p, int64_t bytes, int es, int protocol, bool loopback,
   int steps = 0;
   for (auto* ph : p.sched.flat()) steps += ph->S;
   Program a = lower(p.sched, bytes, es, true, pull), b = lower(p.sched, bytes, es, false, pull);
-  const bool sys = !loopback || loopback_sys();
-  const bool ll = predict_us(a, steps, true, sys) < predict_us(b, steps, false, sys);
+  const ModePolicy& pol = signal_policy(loopback);
+  const bool ll = predict_us(a, steps, true, pol) < predict_us(b, steps, false, pol);
   p.pg = ll ? std::move(a) : std::move(b);
   return ll;
 }
@@ -238,8 +241,9 @@ bool choose_ll(sccl_plan& p, int64_t bytes, int es, int protocol, bool loopback,
 // Small chunks: the smallest power of two that holds one.  Stages come in
 // multiples of the storer-warp count (each storer warp owns the stages s
 // with s % kStorerWarps == its index): 3 or 6.
-void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const ChannelRequest& req) {
-  const bool wide = st.max_fanin >= 4 && !(st.bytes > kStreamBytes && !p.ll);
+void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const ChannelRequest& req,
+                   const ModePolicy& pol) {
+  const bool wide = st.max_fanin >= 4 && !(st.bytes > pol.stream_bytes && !p.ll);
   int tile = req.tile;
   if (tile <= 0) {
     // wide reductions with small chunks: 16 KiB tiles (6 stages, 2 CTAs/SM)
@@ -275,7 +279,8 @@ void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const C
 // step and a relayed receipt is forwarded sooner after it lands: (7,7,7)
 // at 128 MiB/rank 1979 -> 1869 us (64 MiB 993 -> 975, 512 MiB 8048 -> 7595;
 // 16 MiB 254 -> 289, hence its 4 GB floor); combining schedules lost.
-void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const ChannelRequest& req, bool loopback) {
+void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const ChannelRequest& req, bool loopback,
+                     const ModePolicy& pol) {
   const int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, p.ll ? 0 : p.tile, p.nstage)
                   : p.ll ? 2048 / kLLThreads
                          : std::max(1, std::min(2, int((227 << 10) / (p.nstage * p.tile + kSmemHdr))));
@@ -286,8 +291,9 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
   // 192: 199, 296: 190, 96: 232; 256 MiB: 714 / 769 / -- / 893 us;
   // tools/gpu_runs/r02/abort_reg.sh)
   const bool pull_stream = loopback && !p.ll && p.pg.pull && st.reduces && !st.rereads && st.max_fanin >= 4 &&
-                           st.bytes >= kStreamBytes / 8;  // (small launches are latency-bound: more CTAs)
-  const int cap = loopback ? std::max(1, (pull_stream ? req.sms : resident) / p.sched.P) : 32;
+                           st.bytes >= pol.stream_bytes / 8;  // (small launches are latency-bound: more CTAs)
+  const int cap = pol.max_ctas_per_rank > 0 ? pol.max_ctas_per_rank
+                                            : std::max(1, (pull_stream ? req.sms : resident) / p.sched.P);
   const int64_t part = p.ll ? kLLPart : p.tile;
   int kb, kc;
   if (req.nchannels > 0) {
@@ -296,7 +302,8 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
   } else {
     kb = int(std::max<int64_t>(1, std::min<int64_t>(cap, (maxlen + part - 1) / part)));
     kc = req.chunk_groups > 0 ? req.chunk_groups : std::max(1, std::min(p.pg.G, cap / kb));
-    if (req.chunk_groups <= 0 && kc == 1 && kb >= 4 && !p.ll && st.bytes > 4 * kStreamBytes && st.rereads &&
+    if (req.chunk_groups <= 0 && kc == 1 && kb >= 4 && !p.ll && pol.group_split && st.bytes > 4 * pol.stream_bytes &&
+        st.rereads &&
         !st.reduces && double(st.nops_rank0) >= 4.0 * st.steps) {
       kc = 2;
       kb /= 2;
@@ -412,6 +419,7 @@ int group_of(const sccl_plan& p, int chunk) {
 // makes the fence on the store path ~3x dearer, so only very short plans
 // self-publish there (<= 4 tiles; tools/gpu_runs/sys_pub_round1n.sh).
 void choose_release(sccl_plan& p, bool loopback) {
+  const ModePolicy& pol = signal_policy(loopback);
   int64_t max_tiles = 0;
   for (auto& rp : p.pg.ranks)
     for (int g = 0; g < p.kc; ++g) {
@@ -424,7 +432,7 @@ void choose_release(sccl_plan& p, bool loopback) {
       }
       max_tiles = std::max(max_tiles, n);
     }
-  p.selfpub = max_tiles <= ((!loopback || loopback_sys()) ? 4 : 16);
+  p.selfpub = max_tiles <= pol.selfpub_max_tiles;
   if (const char* env = std::getenv("SCCL_SELFPUB")) p.selfpub = std::atoi(env) != 0;
 }
 
@@ -519,7 +527,7 @@ void encode_program(sccl_plan& p) {
   }
 }
 
-// Streaming policies (launches over kStreamBytes):
+// Streaming policies (launches over ModePolicy::stream_bytes; loopback table only):
 //  * window-major (simple protocol, every op 16-byte aligned, some op
 //    re-reads a receipt): a CTA moves one byte window of each op, in
 //    program order, before the next window, so relayed and reduced receipts
@@ -528,7 +536,7 @@ void encode_program(sccl_plan& p) {
 //    tiles when it has one (a ring) (tools/gpu_runs/window_round1r.sh,
 //    window2_round1s.sh).  Schedules that never re-read a receipt (one-shot,
 //    direct alltoall) stay op-major: the per-window descriptor reloads
-//    would only cost.  Below kStreamBytes: AR at 16 MiB/rank was 3-5 %
+//    would only cost.  Below stream_bytes: AR at 16 MiB/rank was 3-5 %
 //    slower with windows and hints.
 //  * L2 hints: single-use loads and stores evict-first
 //    (tools/gpu_runs/l2hint_round1t.sh).  Receipts a later op re-reads are
@@ -542,29 +550,33 @@ void encode_program(sccl_plan& p) {
 //    writes landed (off the compute path) still cost 1-3 % on (56,14,14)
 //    and ring AR, and 5 % on (8,2,2) against the compute warps
 //    (tools/gpu_runs/discard3_round1w.sh).
-//  * discards: wide reductions (fan-in >= 4) drop consumed scratch receipts
-//    from L2 (discard.global.L2: no write-back of dead bytes): (8,2,2) at
-//    64/128 MiB 321 -> 296 / 614 -> 560 us; chains of 2-input reduces lost
-//    10-20 % to the discard instructions and keep the write-back.
+//  * discards: streaming reductions drop consumed scratch receipts from L2
+//    (discard.global.L2: no write-back of dead bytes): push-lowered (8,2,2)
+//    at 64/128 MiB 321 -> 296 / 614 -> 560 us; chains of 2-input reduces
+//    lost 10-20 % to the discard instructions in round 1 but gain 4-6 % with
+//    the round-2 pipeline (numbers below).
 // SCCL_WINDOW=<bytes> (0 = op-major), SCCL_L2HINT and SCCL_DISCARD override.
-void choose_streaming(sccl_plan& p, const ProgramStats& st, bool loopback) {
-  const bool streams = !p.ll && st.bytes > kStreamBytes;
+void choose_streaming(sccl_plan& p, const ProgramStats& st, bool loopback, const ModePolicy& pol) {
+  const bool streams = !p.ll && st.bytes > pol.stream_bytes;
   bool all_vec = true;
   for (auto& d : p.ops) all_vec &= d.kind == OP_WAIT || d.vec;
   const double ops_per_step = double(st.nops_rank0) / double(std::max(1, p.kc * st.steps));
   const int m = std::max(1, std::min(4, int(std::ceil(4.0 / std::max(ops_per_step, 1e-9)))));
-  p.window = (streams && all_vec && st.rereads) ? uint32_t(p.tile) * uint32_t(m) : 0u;
+  p.window = (streams && pol.window_major && all_vec && st.rereads) ? uint32_t(p.tile) * uint32_t(m) : 0u;
   if (const char* env = std::getenv("SCCL_WINDOW")) {
     const long w = std::atol(env);
     p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
   }
-  p.l2hint = streams ? 1 : 0;
+  p.l2hint = streams && pol.l2_hints ? 1 : 0;
   const char* hint_env = std::getenv("SCCL_L2HINT");  // 0, 1, or 3 (| kL2RelayPlain)
   if (hint_env) p.l2hint = std::atoi(hint_env) & 3;
   if (p.l2hint == kL2RelayPlain) p.l2hint = 0;
   bool any_dead = false;  // scratch receipts with one reader (pull plans of one-shot reductions have none)
   for (auto& x : p.ins) any_dead |= x.dead_after != 0;
-  p.discard = p.l2hint && st.max_fanin >= 4 && any_dead;
+  // (round 2: with pull and the current pipeline, chains gain too: AR
+  // (56,14,14) 64 / 256 MiB 260 -> 245 / 1040 -> 977 us, ring AR -3.5 %,
+  // DRAM 1.49 -> 1.29 GB per 64 MiB launch; tools/gpu_runs/r02/chain_discard.sh)
+  p.discard = p.l2hint && pol.discard && any_dead;
   if (const char* env = std::getenv("SCCL_DISCARD")) p.discard = std::atoi(env) != 0 && !p.ll;
   if (p.l2hint && !p.discard && !hint_env) p.l2hint |= kL2RelayPlain;
   p.dcache_min_ops = 4;  // SCCL_DCACHE=<n> overrides (0 = off)
@@ -637,12 +649,14 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   p.timeout_ns = timeout_ms < 0 ? 0 : (timeout_ms == 0 ? def_ms : timeout_ms) * 1000000LL;
 
   const ProgramStats st = program_stats(p.sched, p.pg, loopback);
-  choose_stages(p, st, maxlen, req);
-  choose_channels(p, st, maxlen, req, loopback);
+  const ModePolicy& pol = mode_policy(loopback);
+  p.policy = pol.version;
+  choose_stages(p, st, maxlen, req, pol);
+  choose_channels(p, st, maxlen, req, loopback, pol);
   assign_groups(p);
   choose_release(p, loopback);
   encode_program(p);
-  choose_streaming(p, st, loopback);
+  choose_streaming(p, st, loopback, pol);
   layout_memory(p, loopback);
 }
 
@@ -833,7 +847,7 @@ int sccl_schedule_select(const char* const* jsons, int n, size_t bytes, int dtyp
       for (auto* ph : s.flat()) steps += ph->S;
       for (int ll = 0; ll < 2; ++ll) {  // lower() verifies and throws on invalid input
         const bool mp = multiprocess != 0;
-        const double t = predict_us(lower(s, int64_t(bytes), es, ll != 0, !mp), steps, ll != 0, mp || loopback_sys());
+        const double t = predict_us(lower(s, int64_t(bytes), es, ll != 0, !mp), steps, ll != 0, signal_policy(!mp));
         if (bi < 0 || t < best) {
           best = t;
           bi = i;
@@ -1223,7 +1237,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"groups_balanced\":" << (p->groups_balanced ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"pull\":" << (p->pg.pull ? 1 : 0) << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"groups_balanced\":" << (p->groups_balanced ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"pull\":" << (p->pg.pull ? 1 : 0) << ",\"policy\":\"" << p->policy << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

@@ -22,6 +22,7 @@ struct sccl_plan {
   bool ll = false;       // low-latency protocol
   bool selfpub = false;  // simple protocol: storer warps release their own counters (latency-bound plans)
   long long timeout_ns = 0;
+  std::string policy;    // version of the policy table the plan was built under
 
   // host copy of the device program (also used by the CPU interpreter)
   std::vector<sccl::DevOp> ops;

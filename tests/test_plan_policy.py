@@ -69,7 +69,7 @@ def test_l2_hints_above_one_gigabyte():
 
 def test_relays_evict_last_only_when_discarded():
     assert info("ag777", 128 << 20, protocol="simple")["relay_evict_last"] == 0
-    assert info("ar56", 128 << 20, protocol="simple")["relay_evict_last"] == 0
+    assert info("ar56", 128 << 20, protocol="simple")["relay_evict_last"] == 1  # its receipts are discarded
     assert info("ar822", 128 << 20, protocol="simple", pull="off")["relay_evict_last"] == 1  # discarded after use
     assert info("ar822", 16 << 20, protocol="simple")["relay_evict_last"] == 0   # no hints at all
 
@@ -77,7 +77,7 @@ def test_relays_evict_last_only_when_discarded():
 def test_discard_only_for_wide_streaming_reductions():
     assert info("ar822", 128 << 20, protocol="simple", pull="off")["discard"] == 1   # fan-in 8
     assert info("ar822", 128 << 20, protocol="simple")["discard"] == 0   # pull: no receipts
-    assert info("ar56", 128 << 20, protocol="simple")["discard"] == 0    # 2-input reduce chain
+    assert info("ar56", 128 << 20, protocol="simple")["discard"] == 1    # 2-input reduce chain (round 2)
     assert info("ar822", 16 << 20, protocol="simple")["discard"] == 0    # fits L2
     assert info("ag777", 128 << 20, protocol="simple")["discard"] == 0   # no reduction
 
@@ -138,3 +138,43 @@ def test_ll_splits_chunks_when_groups_run_out():
     # one-shot allreduce: 8 chunk groups only; 64 KiB -> 8 KiB chunks in 2 KiB parts
     i = info("ar822", 64 << 10, protocol="ll")
     assert (i["chunk_groups"], i["byte_parts"]) == (8, 4)
+
+
+def test_multiprocess_plans_do_not_inherit_loopback_hbm_policies():
+    """One rank per GPU: NVLink, not the shared HBM, is the bound, so the
+    loopback-tuned streaming policies stay off (policy.hpp): no window-major
+    order, no L2 hints, no receipt discards, no chunk-group split, at most 32
+    CTAs per rank; the plan reports its table's version."""
+    for name, nb in (("ag777", 128 << 20), ("ar822", 512 << 20), ("ar56", 512 << 20), ("ring", 1 << 30)):
+        js, dt = SCHED[name]
+        mp = sccl.Plan(js, 0, P, nb, dt, device=-1, protocol="simple").info()
+        assert mp["policy"].startswith("multiprocess"), mp["policy"]
+        assert (mp["window"], mp["l2hint"], mp["discard"]) == (0, 0, 0), (name, mp)
+        assert mp["chunk_groups"] * mp["byte_parts"] <= 32 and mp["chunk_groups"] == 1, (name, mp)
+        lb = info(name, nb, protocol="simple")
+        assert lb["policy"].startswith("loopback")
+    assert info("ag777", 128 << 20, protocol="simple")["window"] > 0  # the loopback table keeps them
+
+
+def test_policy_table_override(tmp_path):
+    """SCCL_POLICY replaces a table at run time (tools/tune.py --multi writes
+    one from an N>1 sweep); read once per process."""
+    import json
+    import subprocess
+    import sys
+    t = tmp_path / "policy.json"
+    t.write_text(json.dumps({"multiprocess": {"version": "multiprocess-test", "window_major": True,
+                                              "l2_hints": True, "max_ctas_per_rank": 8,
+                                              "simple_alpha": 100.0}}))
+    code = ("import sys, json; sys.path.insert(0, %r)\n"
+            "from paper_2008_08708_b200 import sccl, schedules as S\n"
+            "js = S.to_json(S.hamiltonian_allgather(8))\n"
+            "i = sccl.Plan(js, 0, 8, 128 << 20, sccl.U8, device=-1, protocol='simple').info()\n"
+            "j = sccl.Plan(js, 0, 8, 1 << 20, sccl.U8, device=-1).info()\n"
+            "print(json.dumps([i['policy'], i['window'] > 0, i['l2hint'], i['nchannels'], j['protocol']]))"
+            % str(sccl._HERE.rsplit("/", 1)[0]))
+    out = subprocess.run([sys.executable, "-c", code], env={**__import__("os").environ, "SCCL_POLICY": str(t)},
+                         capture_output=True, text=True, check=True).stdout
+    pol, window, l2, nch, proto = json.loads(out)
+    assert pol == "multiprocess-test" and window and l2 == 1 and nch <= 8
+    assert proto == "ll"  # a 100 us bulk step makes LL win at 1 MiB

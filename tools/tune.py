@@ -112,5 +112,92 @@ def main():
         plan.close()
 
 
+def main_multi(grid):
+    """--multi: the N>1 refit (run under torchrun, one rank per GPU).  Times
+    every (schedule, size, protocol, nchannels) of the grid with one rank
+    per GPU (CUDA events, max over ranks), refits the protocol model
+    c + alpha * steps + beta * MB (this rank's program bytes) per protocol by
+    relative-error least squares, picks the CTAs-per-rank cap that wins most
+    often, and writes a policy table for SCCL_POLICY (the "multiprocess"
+    section of policy.hpp's ModePolicy) to grid["out"]."""
+    import time
+    import numpy as np
+    import torch.distributed as dist
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    shared = os.environ.get("SCCL_BENCH_SHARE_GPU") == "1"
+    dev = 0 if shared else int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(dev)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    bench_dir = os.path.join(ROOT, "tests", "golden", "schedules", "bench")
+    names = grid.get("scheds", [f"ag_oneshot_full{P}", f"ag_ring_ring{P}", f"ar_oneshot_full{P}",
+                                f"ar_ring_ring{P}", f"a2a_direct_full{P}"])
+    sizes = grid.get("sizes", [1 << k for k in range(10, 27, 2)])
+    chans = grid.get("nchannels", [0])
+    maxb = max(sizes)
+    send = torch.randint(0, 256, (maxb,), dtype=torch.uint8, device="cuda")
+    rows = []
+    for name in names:
+        js = open(os.path.join(bench_dir, name + ".json")).read()
+        d = json.loads(js)
+        steps = sum(ph["S"] for ph in d.get("phases", [d]))
+        dt = sccl.BF16 if d["collective"] == "allreduce" else sccl.U8
+        for sz, proto, nch in itertools.product(sizes, ("ll", "simple"), chans):
+            if d["collective"] == "alltoall" and sz % (P * 2):
+                continue
+            plan = sccl.Plan(js, rank, P, sz, dt, device=dev, protocol=proto, nchannels=nch)
+            plan.bind_with()
+            reg, _ = plan.recv_buffer()
+            s = send[:plan.send_bytes]
+            iters = 50 if sz <= (1 << 20) else 10
+            for _ in range(3):
+                plan.launch(s, reg)
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(iters):
+                plan.launch(s, reg)
+            b.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) * 1e3 / iters], device="cpu" if shared else "cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            info = plan.info()
+            mb = sum(op["len"] * (len(op["ins"]) + len(op["outs"])) for op in info["program"]["ranks"][rank]["ops"]
+                     if op["kind"] != "wait") / 1e6
+            r = {"sched": name, "steps": steps, "bytes": sz, "protocol": proto, "nchannels": info["nchannels"],
+                 "us": round(float(t), 2), "mb": mb}
+            rows.append(r)
+            if rank == 0:
+                print(json.dumps(r), flush=True)
+            plan.close()
+    if rank == 0:
+        co = {}
+        for proto in ("ll", "simple"):
+            pts = [r for r in rows if r["protocol"] == proto]
+            A = np.array([[1.0 / r["us"], r["steps"] / r["us"], r["mb"] / r["us"]] for r in pts])
+            sol, *_ = np.linalg.lstsq(A, np.ones(len(pts)), rcond=None)
+            co[proto] = [round(float(x), 4) for x in sol]
+        wins = {}
+        for key in {(r["sched"], r["bytes"]) for r in rows}:
+            best = min((r for r in rows if (r["sched"], r["bytes"]) == key), key=lambda r: r["us"])
+            wins[best["nchannels"]] = wins.get(best["nchannels"], 0) + 1
+        table = {"multiprocess": {
+            "version": f"multiprocess-nvlink-P{P}-{time.strftime('%Y%m%d')}",
+            "ll_c": co["ll"][0], "ll_alpha": co["ll"][1], "ll_beta": co["ll"][2],
+            "simple_c": co["simple"][0], "simple_alpha": co["simple"][1], "simple_beta": co["simple"][2],
+            "max_ctas_per_rank": max(wins, key=wins.get) if len(chans) > 1 else 32}}
+        out = grid.get("out", os.path.join(ROOT, "gpurun_out", f"policy_multiprocess_P{P}.json"))
+        with open(out, "w") as f:
+            json.dump(table, f, indent=1)
+        print(json.dumps({"policy_table": out, **table}), flush=True)
+    dist.destroy_process_group()
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--multi":
+        main_multi(json.loads(sys.argv[2]) if len(sys.argv) > 2 else {})
+    else:
+        main()
