@@ -821,6 +821,18 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
         assert torch.equal(y, z), f"rank {rank}: {nm} differs from NCCL all_reduce"
         ar[f"ours_{nm}_ms"], ar[f"ours_{nm}_busbw"] = round(t, 4), bw("allreduce", M, t)
         p2.close()
+    if sccl.nvls_supported(dev_index, P):  # the switch-offloaded comparison backend
+        nv = sccl.NvlsAllreduce(rank, P, M, sccl.BF16, device=dev_index)
+        nv.launch(x, y)
+        torch.cuda.synchronize()
+        nv.check()
+        z = x.clone()
+        dist.all_reduce(z)
+        torch.cuda.synchronize()
+        ar["nvls_matches_nccl"] = bool(torch.equal(y, z))
+        t = timed(lambda: nv.launch(), args.steps)  # in its multicast-bound buffer (zero-copy)
+        ar["ours_nvls_ms"], ar["ours_nvls_busbw"] = round(t, 4), bw("allreduce", M, t)
+        nv.close()
     for tag, grp in (("nccl_default", None), ("nccl_ring", g_ring), ("nccl_tree", g_tree), ("nccl_simple", g_simple)):
         z = x.clone()
         t = timed(lambda: dist.all_reduce(z, group=grp), args.steps)

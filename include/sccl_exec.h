@@ -164,6 +164,31 @@ int64_t sccl_plan_launch_count(sccl_plan* plan);
 
 int sccl_plan_destroy(sccl_plan* plan);
 
+/* ---- NVLS allreduce (comparison backend) ----------------
+ * Not schedule-driven: every rank's buffer is bound to one CUDA multicast
+ * object and rank r reduces slice r inside the NVSwitch (multimem.ld_reduce,
+ * multimem.st) -- the switch-offloaded allreduce NCCL calls NVLS.  f32 /
+ * bf16 / f16 sums (the switch accumulates 16-bit types in f32, in its own
+ * order: exact for integer-valued data, within the stated float tolerance
+ * otherwise).  Setup is collective: rank 0 creates and exports the
+ * multicast object (POSIX fd), every rank joins (adds its device), and
+ * after a barrier every rank binds.  bytes: multiple of 16 and of
+ * nranks * element size.  One rank per GPU; needs multicast support
+ * (an NVSwitch system whose fabric manager provides multicast). */
+typedef struct sccl_nvls sccl_nvls;
+/* supported = 1 when the device can form a multicast team of nranks GPUs
+ * (attribute CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED and a trial object) */
+int sccl_nvls_supported(int device, int nranks, int* supported);
+int sccl_nvls_create(int rank, int nranks, size_t bytes, int dtype, int device, sccl_nvls** out);
+int sccl_nvls_export_fd(sccl_nvls* nvls, int* fd);
+int sccl_nvls_join(sccl_nvls* nvls, int fd);
+int sccl_nvls_bind(sccl_nvls* nvls);
+/* the multicast-bound buffer: launching from / into it is zero-copy */
+int sccl_nvls_buffer(sccl_nvls* nvls, void** ptr, size_t* bytes);
+int sccl_nvls_launch(sccl_nvls* nvls, const void* sendbuf, void* recvbuf, void* stream);
+int sccl_nvls_check(sccl_nvls* nvls);
+int sccl_nvls_destroy(sccl_nvls* nvls);
+
 /* thread-local message of the last failing call */
 const char* sccl_last_error(void);
 

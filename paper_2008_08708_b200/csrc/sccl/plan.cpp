@@ -14,6 +14,8 @@
 #include "../../../include/sccl_exec.h"
 #include "error.hpp"
 #include "layout.hpp"
+#include "abi.hpp"
+#include "driver.hpp"
 #include "policy.hpp"
 
 namespace sccl {
@@ -22,33 +24,16 @@ cudaError_t exec_occupancy(int dtype, bool sys, int tile, int nstage, int* block
 int exec_threads();
 }  // namespace sccl
 
+using sccl::cu_check;
+using sccl::Vmm;
+using sccl::vmm_api;
+using sccl::vmm_map;
+
+using sccl::cuda_check;
+using sccl::g_err;
+using sccl::guarded;
+
 namespace {
-
-thread_local std::string g_err;
-
-void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw sccl::cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-template <class F>
-int guarded(F&& f) {
-  try {
-    f();
-    return SCCL_OK;
-  } catch (const sccl::invalid_argument_error& e) {
-    g_err = e.what();
-    return SCCL_INVALID_ARGUMENT;
-  } catch (const sccl::cuda_error& e) {
-    g_err = e.what();
-    return SCCL_CUDA_ERROR;
-  } catch (const sccl::timeout_error& e) {
-    g_err = e.what();
-    return SCCL_PEER_TIMEOUT;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return SCCL_INTERNAL;
-  }
-}
 
 void put_string(const std::string& s, char* out, size_t* len) {
   if (!len) throw sccl::invalid_argument_error("len must not be NULL");
@@ -94,64 +79,6 @@ double predict_us(const sccl::Program& pg, int steps, bool ll, const sccl::ModeP
   mb /= 1e6;
   if (ll) return pol.ll_c + pol.ll_alpha * steps + pol.ll_beta * mb;
   return pol.simple_c + pol.simple_alpha * steps + pol.simple_beta * mb;
-}
-
-// Driver-API VMM entry points, resolved at run time through the runtime
-// (no link-time dependency on libcuda: the library must load on GPU-less
-// build hosts).
-struct Vmm {
-  decltype(&cuMemCreate) create = nullptr;
-  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
-  decltype(&cuMemAddressReserve) reserve = nullptr;
-  decltype(&cuMemAddressFree) addr_free = nullptr;
-  decltype(&cuMemMap) map = nullptr;
-  decltype(&cuMemUnmap) unmap = nullptr;
-  decltype(&cuMemSetAccess) set_access = nullptr;
-  decltype(&cuMemRelease) release = nullptr;
-  decltype(&cuMemExportToShareableHandle) export_handle = nullptr;
-  decltype(&cuMemImportFromShareableHandle) import_handle = nullptr;
-  decltype(&cuMemGetAddressRange) address_range = nullptr;
-};
-const Vmm& vmm_api() {
-  static Vmm v;
-  static bool done = false;
-  if (!done) {
-    auto get = [](const char* name, auto& fn) {
-      void* f = nullptr;
-      cudaDriverEntryPointQueryResult q{};
-      if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || !f)
-        throw sccl::cuda_error(std::string("driver entry point ") + name + " unavailable");
-      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(f);
-    };
-    get("cuMemCreate", v.create);
-    get("cuMemGetAllocationGranularity", v.granularity);
-    get("cuMemAddressReserve", v.reserve);
-    get("cuMemAddressFree", v.addr_free);
-    get("cuMemMap", v.map);
-    get("cuMemUnmap", v.unmap);
-    get("cuMemSetAccess", v.set_access);
-    get("cuMemRelease", v.release);
-    get("cuMemExportToShareableHandle", v.export_handle);
-    get("cuMemImportFromShareableHandle", v.import_handle);
-    get("cuMemGetAddressRange", v.address_range);
-    done = true;
-  }
-  return v;
-}
-void cu_check(CUresult r, const char* what) {
-  if (r != CUDA_SUCCESS) throw sccl::cuda_error(std::string(what) + " failed (CUresult " + std::to_string(int(r)) + ")");
-}
-// map `handle` (size bytes) at a fresh VA range readable and writable by `device`
-char* vmm_map(const Vmm& v, CUmemGenericAllocationHandle handle, size_t size, int device) {
-  CUdeviceptr va = 0;
-  cu_check(v.reserve(&va, size, 0, 0, 0), "cuMemAddressReserve");
-  cu_check(v.map(va, size, 0, handle, 0), "cuMemMap");
-  CUmemAccessDesc acc{};
-  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  acc.location.id = device;
-  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  cu_check(v.set_access(va, size, &acc, 1), "cuMemSetAccess");
-  return reinterpret_cast<char*>(va);
 }
 
 struct IpcBlob {

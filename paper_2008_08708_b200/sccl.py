@@ -76,6 +76,16 @@ def lib():
         L.sccl_plan_register_export.argtypes = [c_p, c_p, c_sz, c_p, ctypes.POINTER(c_sz)]
         L.sccl_plan_register_bind.argtypes = [c_p, c_p, ctypes.POINTER(c_p), c_sz]
         L.sccl_plan_deregister.argtypes = [c_p, c_p]
+        L.sccl_nvls_supported.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.sccl_nvls_create.argtypes = [ctypes.c_int, ctypes.c_int, c_sz, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(c_p)]
+        L.sccl_nvls_export_fd.argtypes = [c_p, ctypes.POINTER(ctypes.c_int)]
+        L.sccl_nvls_join.argtypes = [c_p, ctypes.c_int]
+        L.sccl_nvls_bind.argtypes = [c_p]
+        L.sccl_nvls_buffer.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_sz)]
+        L.sccl_nvls_launch.argtypes = [c_p, c_p, c_p, c_p]
+        L.sccl_nvls_check.argtypes = [c_p]
+        L.sccl_nvls_destroy.argtypes = [c_p]
         L.sccl_launch.argtypes = [c_p, c_p, c_p, c_p]
         L.sccl_launch_loopback.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
         L.sccl_launch_loopback_copy_engine.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
@@ -419,6 +429,18 @@ class AutoLoopbackPlan:
         self.schedules = [_text(s).decode() for s in schedules]
         self.dtype, self.device, self.max_plans = dtype, device, max_plans
         self._plans = {}  # bytes_per_rank -> (schedule index, protocol, LoopbackPlan)
+        self.discovery = None
+
+    @classmethod
+    def from_machine(cls, collective: str = "allgather", P: int = 8, dtype: int = U8, device: int = 0,
+                     max_plans: int = 16):
+        """Candidates from topology discovery (frontier.for_this_machine):
+        on one GPU, every committed Pareto frontier for P ranks."""
+        from . import frontier
+        info, scheds = frontier.for_this_machine(collective, P)
+        self = cls(scheds, dtype, device, max_plans)
+        self.discovery = info
+        return self
 
     def plan_for(self, bytes_per_rank: int):
         if bytes_per_rank not in self._plans:
@@ -443,3 +465,154 @@ class AutoLoopbackPlan:
         for _, _, plan in self._plans.values():
             plan.close()
         self._plans.clear()
+
+
+class AutoPlan:
+    """One rank of a one-process-per-GPU execution with per-size algorithm
+    switching: each new per-rank byte count picks its
+    schedule and protocol with `select(..., multiprocess=True)` (the
+    system-scope cost model), creates that rank's Plan and binds it to the
+    peers (collective: every rank must launch the same sizes in the same
+    order, as SPMD code does)."""
+
+    def __init__(self, schedules: Sequence, rank: int, nranks: int, dtype: int = U8, device: int = 0,
+                 group=None, mem_handles: str = "ipc", max_plans: int = 16):
+        self.schedules = [_text(s).decode() for s in schedules]
+        self.rank, self.nranks, self.dtype, self.device = rank, nranks, dtype, device
+        self.group, self.mem_handles, self.max_plans = group, mem_handles, max_plans
+        self._plans = {}
+        self.discovery = None
+
+    @classmethod
+    def from_machine(cls, collective: str, rank: int, nranks: int, dtype: int = U8, device: int = 0,
+                     group=None, mem_handles: str = "ipc"):
+        """Candidates for the discovered target (switch:N on an NVSwitch
+        box: the switch(N) and full(N) frontiers)."""
+        from . import frontier
+        from . import topology
+        info = topology.discover()
+        target = info["target"] if info["target"].split(":")[0] in ("switch", "full") else f"full:{nranks}"
+        self = cls(frontier.candidates(collective, target, nranks), rank, nranks, dtype, device, group, mem_handles)
+        self.discovery = dict(info, used_target=target)
+        return self
+
+    def plan_for(self, bytes_per_rank: int):
+        if bytes_per_rank not in self._plans:
+            if len(self._plans) >= self.max_plans:
+                self._plans.pop(next(iter(self._plans)))[2].close()
+            i, proto, _ = select(self.schedules, bytes_per_rank, self.dtype, multiprocess=True)
+            plan = Plan(self.schedules[i], self.rank, self.nranks, bytes_per_rank, self.dtype, device=self.device,
+                        protocol=proto, mem_handles=self.mem_handles)
+            plan.bind_with(self.group)
+            self._plans[bytes_per_rank] = (i, proto, plan)
+        return self._plans[bytes_per_rank]
+
+    def launch(self, sendbuf, recvbuf, bytes_per_rank: int, stream=None):
+        i, proto, plan = self.plan_for(bytes_per_rank)
+        plan.launch(sendbuf, recvbuf, stream)
+        return i, proto
+
+    def check(self):
+        for _, _, plan in self._plans.values():
+            plan.check()
+
+    def close(self):
+        for _, _, plan in self._plans.values():
+            plan.close()
+        self._plans.clear()
+
+
+def nvls_supported(device: int = 0, nranks: int = 1) -> bool:
+    """The device can form a multicast team of nranks GPUs (the attribute
+    plus a trial cuMulticastCreate)."""
+    v = ctypes.c_int(0)
+    _raise(lib().sccl_nvls_supported(device, nranks, ctypes.byref(v)))
+    return bool(v.value)
+
+
+def _share_fd_from_root(rank: int, nranks: int, fd: int, group=None) -> int:
+    """Rank 0's file descriptor to every other rank (SCM_RIGHTS over Linux
+    abstract Unix sockets; the socket names travel through torch.distributed).
+    Returns the local fd (rank 0: -1, and its fd is closed)."""
+    import socket
+    import uuid
+    import torch.distributed as dist
+    name = f"\0sccl-nvls-{uuid.uuid4().hex}-{rank}"
+    srv = None
+    if rank != 0:
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(name)
+        srv.listen(1)
+    names: List[Optional[str]] = [None] * nranks
+    dist.all_gather_object(names, name, group=group)
+    got = -1
+    if rank == 0:
+        for r in range(1, nranks):
+            c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            c.connect(names[r])
+            socket.send_fds(c, [b"fd"], [fd])
+            c.close()
+        os.close(fd)
+    else:
+        conn, _ = srv.accept()
+        _, fds, _, _ = socket.recv_fds(conn, 2, 1)
+        got = fds[0]
+        conn.close()
+        srv.close()
+    dist.barrier(group=group)
+    return got
+
+
+class NvlsAllreduce:
+    """NVLS allreduce (SURVEY.md 8(f) f4 comparison backend): every rank's
+    buffer bound to one CUDA multicast object, rank r reduces slice r inside
+    the NVSwitch (multimem.ld_reduce / multimem.st).  One rank per GPU;
+    nranks = 1 needs no process group (a one-device multicast team)."""
+
+    def __init__(self, rank: int, nranks: int, nbytes: int, dtype: int = BF16, device: int = 0, group=None):
+        self._h = ctypes.c_void_p(0)
+        self.rank, self.nranks, self.nbytes = rank, nranks, nbytes
+        _raise(lib().sccl_nvls_create(rank, nranks, nbytes, dtype, device, ctypes.byref(self._h)))
+        fd = -1
+        if nranks > 1:
+            import torch.distributed as dist
+            if rank == 0:
+                f = ctypes.c_int(-1)
+                _raise(lib().sccl_nvls_export_fd(self._h, ctypes.byref(f)))
+                fd = f.value
+            fd = _share_fd_from_root(rank, nranks, fd, group)
+        try:
+            _raise(lib().sccl_nvls_join(self._h, fd))
+        finally:
+            if fd >= 0:
+                os.close(fd)
+        if nranks > 1:
+            import torch.distributed as dist
+            dist.barrier(group=group)  # every device is in the team before anyone binds
+        _raise(lib().sccl_nvls_bind(self._h))
+        if nranks > 1:
+            import torch.distributed as dist
+            dist.barrier(group=group)
+
+    def buffer(self):
+        p, n = ctypes.c_void_p(0), ctypes.c_size_t(0)
+        _raise(lib().sccl_nvls_buffer(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    def launch(self, sendbuf=None, recvbuf=None, stream=None):
+        _raise(lib().sccl_nvls_launch(self._h, ctypes.c_void_p(_ptr(sendbuf)), ctypes.c_void_p(_ptr(recvbuf)),
+                                      ctypes.c_void_p(_stream_ptr(stream))))
+
+    def check(self):
+        _raise(lib().sccl_nvls_check(self._h))
+
+    def close(self):
+        if self._h:
+            lib().sccl_nvls_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -116,6 +116,124 @@ def encode(kind: str, topo: str, C: int, S: int, R: int, root: int = 0) -> Tuple
     return "\n".join(L) + "\n", meta
 
 
+def automorphisms(topo: str) -> List[Tuple[int, ...]]:
+    """Node permutations that preserve every constraint of the topology
+    (edge sets with their bounds)."""
+    import itertools
+    P, groups = topology_edges(topo)
+    cons = {(frozenset(es), b) for es, b in groups}
+    out = []
+    for g in itertools.permutations(range(P)):
+        if all((frozenset((g[a], g[d]) for a, d in es), b) in cons for es, b in cons):
+            out.append(g)
+    return out
+
+
+def encode_symmetric(kind: str, topo: str, C: int, S: int, R: int, group: List[Tuple[int, ...]],
+                     root: int = 0) -> Tuple[str, dict]:
+    """C1-C6 restricted to schedules invariant under a node-permutation
+    group acting freely on the nodes (an automorphism group of the
+    topology): chunk (i, n) -- index i of node n -- is sent along the image
+    under g of the route of chunk (i, g^-1(n)).  Variables exist only for
+    the chunks of one node per orbit; the bandwidth constraint C5 counts the
+    images of every base send.  A |G|-fold smaller problem; a solution is a
+    valid schedule (decode_symmetric expands and the C++ verifier checks
+    it), but symmetry may exclude every solution (then: unsat here, not
+    necessarily for the instance)."""
+    if kind not in ("allgather", "alltoall"):
+        raise ValueError("symmetric encoding: per-node chunk ownership (allgather, alltoall) only")
+    P, groups = topology_edges(topo)
+    if any(g[n] == n for g in group[1:] for n in range(P)) or group[0] != tuple(range(P)):
+        raise ValueError("the group must start with the identity and act freely on the nodes")
+    G = P * C
+    pre, post = _relations(kind, G, P, root)
+    E = sorted({e for es, b in groups for e in es if all(bb > 0 for ees, bb in groups if e in ees)})
+    reps, seen = [], set()
+    for n in range(P):
+        if n not in seen:
+            reps.append(n)
+            seen |= {g[n] for g in group}
+    inv = [tuple(sorted(range(P), key=lambda x: g[x])) for g in group]  # g^-1
+    base = [i * P + n for n in reps for i in range(C)]
+    L = ["(set-logic QF_LIA)"]
+    st = lambda c, n: f"st_{c}_{n}"
+    snd = lambda n, c, m: f"snd_{n}_{c}_{m}"
+    for c in base:
+        for n in range(P):
+            L.append(f"(declare-fun {st(c, n)} () Int)")
+            L.append(f"(assert (and (>= {st(c, n)} 0) (<= {st(c, n)} {S + 1})))")
+        for (n, m) in E:
+            L.append(f"(declare-fun {snd(n, c, m)} () Bool)")
+    for s_ in range(1, S + 1):
+        L.append(f"(declare-fun r_{s_} () Int)")
+        L.append(f"(assert (>= r_{s_} 1))")
+    for c in base:
+        for n in range(P):
+            if (c, n) in pre:
+                L.append(f"(assert (= {st(c, n)} 0))")
+            if (c, n) in post:
+                L.append(f"(assert (<= {st(c, n)} {S}))")
+            if (c, n) not in pre:
+                ins = [snd(a, c, n) for (a, b) in E if b == n]
+                tot = "(+ " + " ".join(f"(ite {x} 1 0)" for x in ins) + " 0)" if ins else "0"
+                L.append(f"(assert (=> (<= {st(c, n)} {S}) (= {tot} 1)))")
+                L.append(f"(assert (=> (= {st(c, n)} {S + 1}) (= {tot} 0)))")
+        for (n, m) in E:
+            L.append(f"(assert (=> {snd(n, c, m)} (< {st(c, n)} {st(c, m)})))")
+    for s_ in range(1, S + 1):
+        for es, b in groups:
+            terms = []
+            for gi in inv:  # send (n,m) of image chunk g(c) <=> send (g^-1 n, g^-1 m) of base chunk c
+                for (n, m) in es:
+                    a_, d_ = gi[n], gi[m]
+                    if (a_, d_) in E:
+                        terms += [f"(ite (and {snd(a_, c, d_)} (= {st(c, d_)} {s_})) 1 0)" for c in base]
+            if terms:
+                L.append(f"(assert (<= (+ {' '.join(terms)}) (* {b} r_{s_})))")
+    L.append(f"(assert (= (+ {' '.join(f'r_{s_}' for s_ in range(1, S + 1))}) {R}))")
+    L.append("(check-sat)")
+    L.append("(get-model)")
+    meta = {"kind": kind, "topo": topo, "P": P, "G": G, "C": C, "S": S, "R": R, "root": root, "E": E,
+            "base": base, "group": group}
+    return "\n".join(L) + "\n", meta
+
+
+def decode_symmetric(model: Dict[str, str], meta: dict) -> dict:
+    """Expand the base chunks' sends by the group (chunk (i, n) -> (i, g(n)))."""
+    P, S = meta["P"], meta["S"]
+    sends = set()
+    for c in meta["base"]:
+        i, n0 = divmod(c, P)
+        for (a, b) in meta["E"]:
+            if model.get(f"snd_{a}_{c}_{b}") == "true":
+                t = int(model[f"st_{c}_{b}"]) - 1
+                if 0 <= t < S:
+                    for g in meta["group"]:
+                        sends.add((i * P + g[n0], g[a], g[b], t))
+    d = {"collective": meta["kind"], "version": 1, "topology": {"name": meta["topo"]}, "P": P, "G": meta["G"],
+         "C": meta["C"], "S": S, "R": meta["R"], "rounds": [int(model[f"r_{s_}"]) for s_ in range(1, S + 1)]}
+    d["sends"] = sorted([list(x) for x in sends], key=lambda x: (x[3], x[0], x[1], x[2]))
+    return d
+
+
+def synthesize_symmetric(kind: str, topo: str, C: int, S: int, R: int,
+                         timeout: float = 600.0) -> Tuple[str, Optional[str], float]:
+    """synthesize() under the topology's automorphism group (free part):
+    for the DGX-1 (order 4, two node orbits) a 4x smaller problem -- the
+    (6,3,7) allgather of Table 4, whose plain encoding the solver did not
+    finish in 1400 s here."""
+    group = [g for g in automorphisms(topo) if g == tuple(range(len(g))) or all(g[n] != n for n in range(len(g)))]
+    text, meta = encode_symmetric(kind, topo, C, S, R, group)
+    status, model, dt = solve(text, timeout)
+    if status != "sat":
+        return status, None, dt
+    js = sccl.canonicalize(decode_symmetric(model, meta))
+    v = sccl.verify(js)
+    if v:
+        raise RuntimeError(f"decoded symmetric schedule failed verification: {v[:3]}")
+    return "sat", js, dt
+
+
 def solve(text: str, timeout: float = 600.0) -> Tuple[str, Dict[str, str], float]:
     """Run the SMT-LIB2 solver child process."""
     solver = os.environ.get("SCCL_SOLVER", "z3")
@@ -220,11 +338,15 @@ def bandwidth_lower_bound(kind: str, topo: str, root: int = 0) -> "Fraction":
         raise ValueError(f"no bandwidth bound for {kind}")
 
     def cap(n, inbound):
+        """chunks per round node n can receive (send): every link into (out
+        of) n carries at most the smallest bound of the constraints that
+        contain it, and a constraint made only of n's links caps their sum"""
         side = (lambda e: e[1] == n) if inbound else (lambda e: e[0] == n)
-        c = sum(b for es, b in groups for e in es if side(e) and len(es) == 1)
-        for es, b in groups:  # grouped ingress / egress constraints (switch model)
+        links = {e for es, _ in groups for e in es if side(e)}
+        c = sum(min(b for es, b in groups if e in es) for e in links)
+        for es, b in groups:
             if len(es) > 1 and all(side(e) for e in es):
-                c = b if c == 0 else min(c, b)
+                c = min(c, b)
         return c
 
     best = Fraction(0)

@@ -545,3 +545,61 @@ def test_float_reduction_within_stated_tolerance(name, dt, protocol):
             want, bnd = exact, bound
         err = np.abs(got - want)
         assert np.all(err <= bnd), (r, float(np.max(err - bnd)))
+
+
+@pytest.mark.parametrize("protocol", ["ll", "simple"])
+@pytest.mark.parametrize("dt", [O.I32, O.F32, O.BF16])
+def test_dgx1_48_6_14_direct_sum(protocol, dt):
+    """SPEC.md:426 / acceptance :641 on the GPU: the DGX-1 Allreduce
+    (48,6,14) (RS+AG of the synthesized (6,3,7)) over random integer
+    payloads leaves all 8 ranks with the direct sum, bit for bit (for the
+    float types: integer values in [-16, 16], exact in any order), and
+    equal to the oracle."""
+    js = open(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "schedules",
+                                         "ar_from_dgx1_6_3_7.json")).read().strip()
+    d = json.loads(js)
+    assert (d["C"], d["S"], d["R"]) == (48, 6, 14)
+    nbytes = 48 * 4096 if protocol == "simple" else 48 * 256
+    mode = "random" if dt == O.I32 else "smallint"
+    ins = O.seeded_inputs("allreduce", 8, nbytes, dt, 641, mode)
+    npdt = {O.I32: np.int32, O.F32: np.float32}.get(dt)
+    if dt == O.BF16:
+        vals = [(x.view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64) for x in ins]
+    else:
+        vals = [x.view(npdt).astype(np.float64 if dt != O.I32 else np.int64) for x in ins]
+    direct = np.sum(vals, axis=0)
+    ref = O.execute(d, ins, nbytes, dt)
+    run_gpu(js, nbytes, dt, seed=641, mode=mode, protocol=protocol)
+    for o in ref:
+        if dt == O.BF16:
+            got = (o.view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        elif dt == O.I32:
+            got = o.view(np.int32).astype(np.int64)
+            direct = direct.astype(np.int64).astype(np.int32).astype(np.int64)  # wrapping sum
+        else:
+            got = o.view(npdt).astype(np.float64)
+        assert np.array_equal(got, direct)
+
+
+def test_auto_plan_from_machine_gpu():
+    """Topology discovery on this box (one GPU: loopback) -> the committed
+    frontiers for P = 8 -> the cost model's per-size choice: allgather and
+    allreduce at several sizes, bit-exact with the oracle."""
+    for coll, dt in (("allgather", O.U8), ("allreduce", O.BF16)):
+        ap = sccl.AutoLoopbackPlan.from_machine(coll, 8, dt)
+        assert ap.discovery["target"] == "loopback:1"
+        chosen = set()
+        for nb in (1024, 64 << 10, 4 << 20):
+            i, proto, plan = ap.plan_for(nb)
+            chosen.add((i, proto))
+            d = json.loads(ap.schedules[i])
+            ins = O.seeded_inputs(coll, 8, nb, dt, 3)
+            ref = O.execute(d, ins, nb, dt)
+            send = [torch.from_numpy(x).to(DEV) for x in ins]
+            recv = [torch.zeros(r.size, dtype=torch.uint8, device=DEV) for r in ref]
+            ap.launch(send, recv, nb)
+            torch.cuda.synchronize()
+            ap.check()
+            assert all(np.array_equal(a.cpu().numpy(), b) for a, b in zip(recv, ref)), (coll, nb)
+        assert len(chosen) >= 2, chosen  # the choice changes with size
+        ap.close()

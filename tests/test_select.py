@@ -11,7 +11,7 @@ from paper_2008_08708_b200 import sccl
 from paper_2008_08708_b200 import schedules as S
 
 HERE = os.path.dirname(__file__)
-PARETO = os.path.join(HERE, "golden", "schedules", "pareto")
+PARETO = os.path.join(os.path.dirname(HERE), "paper_2008_08708_b200", "frontiers")
 
 
 def frontier_candidates():

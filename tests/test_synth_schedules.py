@@ -38,6 +38,24 @@ def test_table4_allreduce_tuples():
     b = json.loads(_load("ar_from_dgx1_2_2_3"))
     assert (a["C"], a["S"], a["R"]) == (8, 4, 4)
     assert (b["C"], b["S"], b["R"]) == (16, 4, 6)
+    c = json.loads(_load("ar_from_dgx1_6_3_7"))  # the SPEC's own row (acceptance :641)
+    assert (c["C"], c["S"], c["R"]) == (48, 6, 14)
+    g = json.loads(_load("ag_dgx1_6_3_7"))  # Table 4 (6,3,7): bandwidth-optimal, R/C = 7/6 = b_l
+    assert (g["C"], g["S"], g["R"]) == (6, 3, 7) and sum(g["rounds"]) == 7
+
+
+@pytest.mark.skipif(shutil.which(os.environ.get("SCCL_SOLVER", "z3")) is None, reason="no SMT solver")
+def test_symmetric_encoding_small():
+    """The symmetry-reduced encoding (DGX-1 automorphism group, order 4,
+    acting freely) finds verifier-clean schedules; images of the base
+    chunks' routes fill in the rest."""
+    from paper_2008_08708_b200 import synth
+    grp = synth.automorphisms("dgx1")
+    assert len(grp) == 4 and all(g[n] != n for g in grp[1:] for n in range(8))
+    st, js, _ = synth.synthesize_symmetric("allgather", "dgx1", 1, 2, 2, timeout=60)
+    assert st == "sat" and sccl.verify(js) == []
+    d = json.loads(js)
+    assert len(d["sends"]) == 56  # exactly once: 8 chunks x 7 receivers
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -74,13 +92,13 @@ def test_synth_small_instances():
     assert st == "sat" and sccl.verify(js) == []
 
 
-PARETO = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "schedules", "pareto", "ag_*.json")))
+PARETO = sorted(glob.glob(os.path.join(os.path.dirname(os.path.dirname(__file__)), "paper_2008_08708_b200", "frontiers", "ag_*.json")))
 
 
 def test_pareto_index_matches_paper():
     """Table 5 (PAPER.md:952-954): ring(8) k=0 frontier starts at (1,4,4);
     k=3 reaches (2,4,7), both latency- and bandwidth-optimal."""
-    idx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "schedules", "pareto", "index.json")))
+    idx = json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "paper_2008_08708_b200", "frontiers", "index.json")))
     r8 = {(e["k"], e["C"], e["S"], e["R"]) for e in idx if e["topology"] == "ring:8"}
     assert (0, 1, 4, 4) in r8 and (3, 2, 4, 7) in r8
     assert all(e["bandwidth_optimal"] for e in idx if e["topology"].startswith("full"))

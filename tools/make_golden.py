@@ -78,6 +78,12 @@ def main():
     fixtures.append(vec_case("ar_dgx1_8_4_4_int", S.allreduce_from(ag_dgx), 4096, O.I32, 641, "random",
                              "SPEC.md:426, acceptance SPEC.md:641 (the (8,4,4) Table 4 row); exact sums",
                              {"check_direct_sum": True}))
+    # the SPEC's own (48,6,14) row: RS+AG of the SMT-synthesized DGX-1 (6,3,7)
+    with open(os.path.join(OUT, "schedules", "ar_from_dgx1_6_3_7.json")) as f:
+        ar48 = f.read().strip()
+    fixtures.append(vec_case("ar_dgx1_48_6_14_int", ar48, 6144, O.I32, 641, "random",
+                             "SPEC.md:426, acceptance SPEC.md:641: DGX-1 Allreduce (48,6,14), random integer "
+                             "payloads, all 8 nodes hold the direct sum", {"check_direct_sum": True}))
     fixtures.append(vec_case("ag_fig2_u8", S.to_json(S.recursive_doubling_ring4()), 1000, O.U8, 1, "random",
                              "Fig. 2 (PAPER.md:309-312)"))
     fixtures.append(vec_case("ag_777_u8", S.to_json(S.hamiltonian_allgather(8)), 4096 + 48, O.U8, 2, "random",

@@ -1,8 +1,10 @@
 #!/usr/bin/env python3
 """BASELINE config 5: Pareto frontiers (Algorithm 1) of
-allgather on ring(P) for k = 0..3 and on full(P), P in {2, 4, 8}; each
+allgather on ring(P) for k = 0..3, on full(P), and on the NVSwitch model
+switch(P) (per-GPU egress / ingress groups) for k = 0 and
+k = P - 2, P in {2, 4, 8}; each
 frontier entry is committed as a canonical schedule file (models are not
-unique) under tests/golden/schedules/pareto/, with an index.
+unique) under paper_2008_08708_b200/frontiers/, with an index.
 Usage: python tools/make_pareto_schedules.py"""
 import json
 import os
@@ -12,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2008_08708_b200 import synth  # noqa: E402
 
-OUT = os.path.join(ROOT, "tests", "golden", "schedules", "pareto")
+OUT = os.path.join(ROOT, "paper_2008_08708_b200", "frontiers")
 
 
 def main():
@@ -20,6 +22,7 @@ def main():
     index = []
     for P in (2, 4, 8):
         runs = [(f"ring:{P}", k) for k in range(4)] + [(f"full:{P}", 0)]
+        runs += [(f"switch:{P}", k) for k in sorted({0, P - 2})]
         for topo, k in runs:
             fr = synth.pareto_synthesize("allgather", topo, k, max_steps=8, timeout=120)
             for e in fr:

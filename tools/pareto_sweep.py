@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """BASELINE config 5 on one GPU: every committed Pareto-frontier allgather
-(tests/golden/schedules/pareto/) and its allreduce (invert + compose) timed in
+(paper_2008_08708_b200/frontiers/) and its allreduce (invert + compose) timed in
 loopback across sizes (CUDA-graph timed), then an alpha-beta fit per P
 (costmodel.fit) and the per-size winner.  One JSON line per measurement,
 then one summary line per P."""
@@ -20,7 +20,7 @@ SIZES = [1 << 10, 1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24]
 
 
 def main():
-    d = os.path.join(ROOT, "tests", "golden", "schedules", "pareto")
+    d = os.path.join(ROOT, "paper_2008_08708_b200", "frontiers")
     index = json.load(open(os.path.join(d, "index.json")))
     seen = set()
     maxb = max(SIZES)

@@ -22,13 +22,18 @@ cases = [
     (S.allreduce_from(S.ring_allgather(4)), 1000, O.F32, "ll"),
     (S.to_json(S.direct_alltoall(4, 8)), 4096 + 32, O.U8, "simple"),
     (S.to_json(S.bidir_ring_allgather(8)), 1000, O.U8, "simple"),  # unaligned offsets
+    # round 2: pull-lowered reductions (peers' SEND read in place), push for comparison
+    (S.allreduce_from(S.hamiltonian_allgather(8)), 65536, O.BF16, "simple"),
+    (S.allreduce_from(S.one_shot_allgather(8)), 8192, O.F32, "ll"),
+    (S.allreduce_from(S.one_shot_allgather(8)), 40960, O.BF16, "simple", "off"),
 ]
 bad = 0
-for js, nb, dt, proto in cases:
+for js, nb, dt, proto, *pull in cases:
     d = json.loads(js)
     ins = O.seeded_inputs(d["collective"], d["P"], nb, dt, 1)
     ref = O.execute(d, ins, nb, dt)
-    plan = sccl.LoopbackPlan(js, nb, dt, device=0, protocol=proto, timeout_ms=120000)
+    plan = sccl.LoopbackPlan(js, nb, dt, device=0, protocol=proto, timeout_ms=120000,
+                             pull=pull[0] if pull else "auto")
     send = [torch.from_numpy(x).cuda() for x in ins]
     recv = [torch.zeros(r.size, dtype=torch.uint8, device="cuda") for r in ref]
     plan.launch(send, recv)
