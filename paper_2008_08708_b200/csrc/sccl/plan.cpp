@@ -141,7 +141,7 @@ ProgramStats program_stats(const Schedule& sched, const Program& pg, bool loopba
 // Protocol (auto): lower both ways and take the smaller predicted time
 // t = c + alpha*S + beta*MB (S = schedule steps, MB = bytes the lowered
 // program reads + writes).  Constants: a relative-error least-squares fit
-// to the B200 loopback crossover sweep (tools/gpu_runs/proto_round1i.sh:
+// to the B200 loopback crossover sweep (tools/gpu_runs/r01/proto_round1i.sh:
 // 7 schedules x 16 KiB-16 MiB x both protocols; mean regret vs the
 // per-point best 1.9 %); system scope uses its own fit.
 bool choose_ll(sccl_plan& p, int64_t bytes, int es, int protocol, bool loopback, bool pull) {
@@ -175,7 +175,7 @@ void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const C
   if (tile <= 0) {
     // wide reductions with small chunks: 16 KiB tiles (6 stages, 2 CTAs/SM)
     // put twice the CTAs on the chunks (AR (8,2,2) 512 KiB-2 MiB per rank:
-    // -13..-26 %, tools/gpu_runs/midtile2_round1w.sh)
+    // -13..-26 %, tools/gpu_runs/r01/midtile2_round1w.sh)
     tile = wide ? (maxlen <= (256 << 10) ? 16384 : kMaxTile) : 32768;
     // one-shot copies (one fan-out op per rank, nothing re-read) up to
     // 512 KiB: two 16 KiB tiles per CTA overlap the load of one with the
@@ -238,7 +238,7 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
     // LL: cap / kb rounding down can leave CTA slots idle (ring AG at
     // 256 KiB: 1 x 64 of 111 per rank); take the chunk-group count that
     // fills the most slots (fewest groups on ties) when that is 25 % more:
-    // ring / one-shot AG 256 KiB -22 / -9 % (tools/gpu_runs/llgrid4_round1w.sh)
+    // ring / one-shot AG 256 KiB -22 / -9 % (tools/gpu_runs/r01/llgrid4_round1w.sh)
     if (p.ll && req.chunk_groups <= 0 && 4 * kc * kb < 3 * cap) {
       int bc = kc, bb = kb;
       for (int c = kc + 1; c <= std::min(p.pg.G, cap); ++c) {
@@ -251,7 +251,7 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
     // to 40 KiB: one chunk per CTA (kc = G, kb = 1) instead of byte parts of
     // several chunks, so each CTA forwards one chunk down its chain without
     // queueing behind the others' hops: (7,7,7) 64-256 KiB -24..-31 %,
-    // (56,14,14) 256 KiB-2 MiB -6..-32 % (tools/gpu_runs/llgrid2_round1w.sh;
+    // (56,14,14) 256 KiB-2 MiB -6..-32 % (tools/gpu_runs/r01/llgrid2_round1w.sh;
     // at 75 KiB chunks the byte parts win again)
     if (p.ll && req.chunk_groups <= 0 && st.rereads && st.steps >= 4 && p.pg.G >= 32 && p.pg.G <= cap &&
         maxlen <= (40 << 10)) {
@@ -262,7 +262,7 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
     // idle: split the chunks further, down to 2 KiB per CTA, up to 64 CTAs
     // per rank (a larger LL grid lost: (7,7,7) 16 KiB with 896 CTAs +29 %).
     // AR (8,2,2) 64 / 128 KiB -28 / -26 %, one-shot AG 4-16 KiB -14..-16 %
-    // (tools/gpu_runs/llpart_round1w.sh, llgrow_round1w.sh).
+    // (tools/gpu_runs/r01/llpart_round1w.sh, llgrow_round1w.sh).
     if (p.ll && req.chunk_groups <= 0) {
       const int grid_cap = loopback ? std::min(cap, 512 / std::max(1, p.sched.P)) : cap;
       while (2 * kc * kb <= grid_cap && maxlen / (2 * kb) >= 2048) kb *= 2;
@@ -285,7 +285,7 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
 // mean and the greedy map is 3 % better: the (7,7,7) allgather at 128 MiB
 // (modulo 1.09x the mean, greedy 1.03x) ran 1.3 % slower greedy -- it is
 // HBM-bound, and the modulo order is the one its L2 reuse was tuned on
-// (tools/gpu_runs/groups_ab_round1w.sh, groups2_ab_round1w.sh).
+// (tools/gpu_runs/r01/groups_ab_round1w.sh, groups2_ab_round1w.sh).
 void assign_groups(sccl_plan& p) {
   const int P = int(p.pg.ranks.size());
   int maxc = 0;
@@ -342,9 +342,9 @@ int group_of(const sccl_plan& p, int chunk) {
 // Counter release: latency-bound plans (<= 16 tiles per CTA) let each
 // storer warp release its own tile's counters (no hand-off, ~0.3 us less
 // per hop); longer ones keep the fence off the store path in the signaler
-// warp, batched across ops (tools/gpu_runs/winsig_round1h.sh).  System scope
+// warp, batched across ops (tools/gpu_runs/r01/winsig_round1h.sh).  System scope
 // makes the fence on the store path ~3x dearer, so only very short plans
-// self-publish there (<= 4 tiles; tools/gpu_runs/sys_pub_round1n.sh).
+// self-publish there (<= 4 tiles; tools/gpu_runs/r01/sys_pub_round1n.sh).
 void choose_release(sccl_plan& p, bool loopback) {
   const ModePolicy& pol = signal_policy(loopback);
   int64_t max_tiles = 0;
@@ -460,23 +460,23 @@ void encode_program(sccl_plan& p) {
 //    program order, before the next window, so relayed and reduced receipts
 //    are read back while still in L2.  One tile when a CTA has several ops
 //    per step (the other ops of the step cover the hop latency), up to 4
-//    tiles when it has one (a ring) (tools/gpu_runs/window_round1r.sh,
+//    tiles when it has one (a ring) (tools/gpu_runs/r01/window_round1r.sh,
 //    window2_round1s.sh).  Schedules that never re-read a receipt (one-shot,
 //    direct alltoall) stay op-major: the per-window descriptor reloads
 //    would only cost.  Below stream_bytes: AR at 16 MiB/rank was 3-5 %
 //    slower with windows and hints.
 //  * L2 hints: single-use loads and stores evict-first
-//    (tools/gpu_runs/l2hint_round1t.sh).  Receipts a later op re-reads are
+//    (tools/gpu_runs/r01/l2hint_round1t.sh).  Receipts a later op re-reads are
 //    stored with the default policy: evict-last cost 1.5-3 % on relays and
 //    reduce chains (AG (7,7,7) 128 MiB 1945 -> 1888 us, AR (56,14,14)
-//    663 -> 654, ring AR 616 -> 600; tools/gpu_runs/l2mode2_round1w.sh).
+//    663 -> 654, ring AR 616 -> 600; tools/gpu_runs/r01/l2mode2_round1w.sh).
 //    Only plans that discard the receipts after use keep evict-last (one-shot
 //    AR: 572 vs 578 us).  Demoting a relay to evict_normal with
 //    applypriority after its last load cost 7-17 % (the instructions).
 //    Discarding chain receipts from the signaler warp once their tile's
 //    writes landed (off the compute path) still cost 1-3 % on (56,14,14)
 //    and ring AR, and 5 % on (8,2,2) against the compute warps
-//    (tools/gpu_runs/discard3_round1w.sh).
+//    (tools/gpu_runs/r01/discard3_round1w.sh).
 //  * discards: streaming reductions drop consumed scratch receipts from L2
 //    (discard.global.L2: no write-back of dead bytes): push-lowered (8,2,2)
 //    at 64/128 MiB 321 -> 296 / 614 -> 560 us; chains of 2-input reduces

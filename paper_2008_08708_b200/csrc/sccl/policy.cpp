@@ -17,7 +17,7 @@ namespace {
 //    (7 schedules x 16 KiB-16 MiB x both protocols), mean regret 0.9 %;
 //  * 1 GB streaming threshold, window-major, L2 hints, discards and the
 //    chunk-group split: profiles/r01/window, l2policy, discard;
-//  * self-publish up to 16 tiles per CTA (tools/gpu_runs/winsig_round1h.sh).
+//  * self-publish up to 16 tiles per CTA (tools/gpu_runs/r01/winsig_round1h.sh).
 ModePolicy loopback_default() {
   ModePolicy p;
   p.version = "loopback-b200-r02";

@@ -16,7 +16,7 @@ import torch  # noqa: E402
 from paper_2008_08708_b200 import costmodel, sccl  # noqa: E402
 from tune import time_plan  # noqa: E402
 
-SIZES = [1 << 10, 1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24]
+SIZES = [1 << k for k in range(10, 31, 2)]  # 1 KiB .. 1 GiB per rank (BASELINE config 5 uses config 2/3 sizes)
 
 
 def main():
