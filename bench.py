@@ -393,11 +393,47 @@ def loopback_e2e(args, plan, send, recv):
     e2e_ms = a.elapsed_time(b) / steps
     wc = torch.cat(hsend[0])  # both host input sets hold the same bytes
     assert all(torch.equal(hres[r * P * m:(r + 1) * P * m], wc) for r in range(P)), "e2e result wrong"
+
+    # context, not the headline: one rank's share of the host traffic (its
+    # input H2D, its output D2H) per step -- what each GPU of a one-rank-per-
+    # GPU box moves over its own PCIe link; here all 8 ranks share one link
+    def run_one(nsteps):
+        ev_k = [torch.cuda.Event() for _ in range(nsteps)]
+        for i in range(nsteps):
+            k = i % 2
+            with torch.cuda.stream(s_h2d):
+                if i >= 2:
+                    s_h2d.wait_event(ev_k[i - 2])
+                dsend[k][0].copy_(hsend[k][0], non_blocking=True)
+            s_k.wait_stream(s_h2d)
+            s_k.wait_stream(s_d2h)
+            plan.launch(dsend[k], drecv[k], s_k)
+            ev_k[i].record(s_k)
+            s_d2h.wait_event(ev_k[i])
+            with torch.cuda.stream(s_d2h):
+                hres[:P * m].copy_(drecv[k][0], non_blocking=True)
+        return s_d2h
+
+    run_one(2)
+    torch.cuda.synchronize()
+    a1, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a1.record(s_h2d)
+    s_k.wait_event(a1)
+    s_d2h.wait_event(a1)
+    run_one(steps)
+    b1.record(s_d2h)
+    torch.cuda.synchronize()
+    one_ms = a1.elapsed_time(b1) / steps
     return {"value": round(busbytes("allgather", P, m) / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": P * m, "d2h_bytes_per_step": P * P * m, "ms_per_step": round(e2e_ms, 3),
             "note": "per-rank bus GB/s through LoopbackPlan.launch with host buffers: H2D of all ranks' inputs + "
                     "collective + D2H of all ranks' outputs (8 GiB) every step, over one PCIe link; "
-                    "pipelined over 2 device buffer sets / 3 streams"}
+                    "pipelined over 2 device buffer sets / 3 streams",
+            "per_gpu_pcie_variant": {
+                "value": round(busbytes("allgather", P, m) / (one_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                "h2d_bytes_per_step": m, "d2h_bytes_per_step": P * m, "ms_per_step": round(one_ms, 3),
+                "note": "context only: one rank's H2D + D2H per step (what each GPU of an 8-GPU box moves over "
+                        "its own link); the headline e2e above copies every rank's data"}}
 
 
 def loopback_extras(args, sccl, plan, send, recv, stream, peaks):

@@ -1,0 +1,7 @@
+# round 2 evidence: ncu of the bench workload kernel (traffic), launch list, SASS excerpt, bench N=1 + reference arm
+set -x
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:exec_kernel -s 4 -c 1 -o gpurun_out/r02_prof_ag777 python bench.py --steps 2 --warmup 3 --no-sweep --cpu-seconds 0.1 --cpu-bytes 65536 > gpurun_out/r02_ncu_ag777.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv --log-file gpurun_out/r02_launches_bench.csv python bench.py --steps 3 --warmup 3 --no-sweep --cpu-seconds 0.2 --cpu-bytes 65536 > gpurun_out/r02_ncu_launch_bench.log 2>&1
+timeout 900 python bench.py --impl reference > gpurun_out/r02h_bench_ref.log 2>&1
+timeout 900 python bench.py > gpurun_out/r02h_bench.log 2>&1
