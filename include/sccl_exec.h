@@ -53,7 +53,8 @@ typedef struct {
                          <0 = disabled.  Expiry: the launch aborts cooperatively (publishes nothing
                          more, exits normally; the CUDA context stays usable), sccl_plan_check
                          returns SCCL_PEER_TIMEOUT and the plan refuses further launches.       */
-  int mem_handles;    /* multi-process region sharing: 0 = CUDA IPC handles, 1 = VMM (cuMem) POSIX FDs */
+  int mem_handles;    /* multi-process region sharing: 0 = CUDA IPC handles, 1 = VMM (cuMem) POSIX FDs,
+                         2 = caller-provided regions (sccl_plan_bind_peers_external)             */
   int pull;           /* combining sends of untouched inputs read in place by the receiver (no receipt
                          slot): 0 = auto (loopback plans: on), 1 = on (loopback only), -1 = off        */
 } sccl_plan_opts;
@@ -117,6 +118,17 @@ int sccl_plan_bind_peers(sccl_plan* plan, const void* const* peer_blobs, size_t 
  * maps peer r's region from fds[r] (fds[rank] is ignored). */
 int sccl_plan_export_fd(sccl_plan* plan, int* fd);
 int sccl_plan_bind_peers_fd(sccl_plan* plan, const void* const* peer_blobs, size_t blob_len, const int* fds);
+
+/* Caller-provided regions (opts.mem_handles = 2): the caller allocates
+ * every rank's region of sccl_plan_region_bytes bytes in memory all ranks
+ * have mapped -- e.g. torch symmetric memory (symm_mem.empty + rendezvous,
+ * whose buffer_ptrs are the peers' mappings) -- and binds with the
+ * pointers as mapped in this process (regions[rank] is this rank's own).
+ * Bind zeroes the own region; the caller must barrier after every rank has
+ * bound and before the first launch, and guarantee that every rank created
+ * the same plan (same schedule, size, dtype, options). */
+int sccl_plan_region_bytes(sccl_plan* plan, size_t* bytes);
+int sccl_plan_bind_peers_external(sccl_plan* plan, const void* const* regions);
 
 /* The plan's own registered (peer-writable) receive buffer.  Passing it, or
  * a buffer registered with sccl_plan_register_bind, as recvbuf to

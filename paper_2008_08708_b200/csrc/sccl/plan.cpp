@@ -611,7 +611,10 @@ void plan_device_setup(sccl_plan& p) {
   cuda_check(cudaMalloc(&p.d_epochs, ne * sizeof(uint64_t)), "cudaMalloc(epochs)");
   cuda_check(cudaMemset(p.d_epochs, 0, ne * sizeof(uint64_t)), "memset(epochs)");
   size_t total = p.region_bytes * size_t(nlaunch);
-  if (p.vmm) {  // shareable cuMem allocation (POSIX fd)
+  if (p.external) {
+    // the caller supplies every rank's region at bind time (e.g. torch
+    // symmetric memory, sccl_plan_bind_peers_external)
+  } else if (p.vmm) {  // shareable cuMem allocation (POSIX fd)
     const Vmm& v = vmm_api();
     CUmemAllocationProp prop{};
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
@@ -628,7 +631,7 @@ void plan_device_setup(sccl_plan& p) {
   } else {
     cuda_check(cudaMalloc(&p.d_region, total), "cudaMalloc(region)");
   }
-  cuda_check(cudaMemset(p.d_region, 0, total), "memset(region)");
+  if (!p.external) cuda_check(cudaMemset(p.d_region, 0, total), "memset(region)");
   cuda_check(cudaHostAlloc(&p.h_err, 64 * sizeof(int), cudaHostAllocMapped), "cudaHostAlloc(err)");
   std::memset(p.h_err, 0, 64 * sizeof(int));
   cuda_check(cudaHostGetDevicePointer(&p.d_err, p.h_err, 0), "cudaHostGetDevicePointer");
@@ -817,8 +820,11 @@ static int create_common(const char* json, int rank, int nranks, size_t bytes, i
       if (loopback && p->nch * p->nranks > p->resident_cap)
         throw invalid_argument_error("loopback needs P*nchannels <= resident CTAs (" +
                                      std::to_string(p->resident_cap) + ")");
-      if (o.mem_handles < 0 || o.mem_handles > 1) throw invalid_argument_error("mem_handles must be 0 (CUDA IPC) or 1 (VMM fd)");
+      if (o.mem_handles < 0 || o.mem_handles > 2)
+        throw invalid_argument_error("mem_handles must be 0 (CUDA IPC), 1 (VMM fd) or 2 (caller-provided regions)");
+      if (loopback && o.mem_handles == 2) throw invalid_argument_error("loopback plans own their memory");
       p->vmm = !loopback && o.mem_handles == 1;
+      p->external = !loopback && o.mem_handles == 2;
       if (!p->host_only) plan_device_setup(*p);
     } catch (...) {
       sccl_plan_destroy(p);
@@ -859,7 +865,7 @@ int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
     b.dtype = p->dtype;
     b.redop = p->redop;
     b.region_bytes = p->region_bytes;
-    if (!p->host_only && !p->vmm) {
+    if (!p->host_only && !p->vmm && !p->external) {
       cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
       cuda_check(cudaIpcGetMemHandle(&b.handle, p->d_region), "cudaIpcGetMemHandle");
     }
@@ -896,6 +902,7 @@ int sccl_plan_bind_peers(sccl_plan* p, const void* const* blobs, size_t blob_len
   return guarded([&] {
     const std::vector<IpcBlob> bs = check_blobs(p, blobs, blob_len);
     if (p->vmm) throw invalid_argument_error("VMM plan: bind with sccl_plan_bind_peers_fd");
+    if (p->external) throw invalid_argument_error("external-region plan: bind with sccl_plan_bind_peers_external");
     if (!p->host_only) {
       cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
       for (int r = 0; r < p->nranks; ++r) {
@@ -1032,6 +1039,37 @@ int sccl_plan_deregister(sccl_plan* p, void* buf) {
         return;  // peer mappings stay open until the plan is destroyed (other registrations may share them)
       }
     throw invalid_argument_error("buffer is not registered with this plan");
+  });
+}
+
+int sccl_plan_region_bytes(sccl_plan* p, size_t* bytes) {
+  return guarded([&] {
+    if (!p || !bytes) throw invalid_argument_error("NULL argument");
+    if (p->loopback) throw invalid_argument_error("loopback plans have no shared region");
+    *bytes = p->region_bytes;
+  });
+}
+
+int sccl_plan_bind_peers_external(sccl_plan* p, const void* const* regions) {
+  return guarded([&] {
+    if (!p || !regions) throw invalid_argument_error("NULL argument");
+    if (!p->external) throw invalid_argument_error("plan was not created with mem_handles = 2 (caller-provided regions)");
+    if (p->bound) throw invalid_argument_error("plan already bound");
+    for (int r = 0; r < p->nranks; ++r) {
+      if (!regions[r]) throw invalid_argument_error("missing region for rank " + std::to_string(r));
+      check_aligned(regions[r], "region");
+    }
+    if (!p->host_only) {
+      cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
+      p->d_region = static_cast<char*>(const_cast<void*>(regions[p->rank]));
+      // counters start at zero; peers may write into this region only after
+      // this rank's first launch (entry handshake), and the caller's barrier
+      // after every bind orders this memset before any peer's first launch
+      cuda_check(cudaMemset(p->d_region, 0, p->region_bytes), "memset(external region)");
+      cuda_check(cudaDeviceSynchronize(), "bind");
+      for (int r = 0; r < p->nranks; ++r) p->peer_region[r] = static_cast<char*>(const_cast<void*>(regions[r]));
+    }
+    p->bound = true;
   });
 }
 
@@ -1186,7 +1224,7 @@ int sccl_plan_destroy(sccl_plan* p) {
           v.addr_free(CUdeviceptr(p->peer_region[r]), p->vmm_size);
           if (r < p->peer_vmm.size() && p->peer_vmm[r]) v.release(CUmemGenericAllocationHandle(p->peer_vmm[r]));
         }
-    } else {
+    } else if (!p->external) {  // (caller-provided regions are the caller's to unmap)
       for (size_t r = 0; r < p->peer_region.size(); ++r)
         if (int(r) != p->rank && p->peer_region[r]) cudaIpcCloseMemHandle(p->peer_region[r]);
     }
@@ -1198,7 +1236,9 @@ int sccl_plan_destroy(sccl_plan* p) {
     cudaFree(p->d_dtab);
     cudaFree(p->d_nwin);
     cudaFree(p->d_epochs);
-    if (p->vmm) {
+    if (p->external) {
+      // caller-owned regions
+    } else if (p->vmm) {
       if (p->d_region) {
         const Vmm& v = vmm_api();
         v.unmap(CUdeviceptr(p->d_region), p->vmm_size);

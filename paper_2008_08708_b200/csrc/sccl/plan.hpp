@@ -54,6 +54,7 @@ struct sccl_plan {
   std::vector<char*> peer_region;  // multi-process: every rank's region (own included)
   // VMM mode (opts.mem_handles = 1): cuMem allocation handles (CUmemGenericAllocationHandle)
   bool vmm = false;
+  bool external = false;  // opts.mem_handles = 2: regions supplied by the caller (torch symmetric memory)
   uint64_t vmm_handle = 0;
   size_t vmm_size = 0;
   std::vector<uint64_t> peer_vmm;  // imported handles, 0 = none

@@ -73,6 +73,8 @@ def lib():
         L.sccl_plan_export_fd.argtypes = [c_p, ctypes.POINTER(ctypes.c_int)]
         L.sccl_plan_bind_peers_fd.argtypes = [c_p, ctypes.POINTER(c_p), c_sz, ctypes.POINTER(ctypes.c_int)]
         L.sccl_plan_recv_buffer.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_sz)]
+        L.sccl_plan_region_bytes.argtypes = [c_p, ctypes.POINTER(c_sz)]
+        L.sccl_plan_bind_peers_external.argtypes = [c_p, ctypes.POINTER(c_p)]
         L.sccl_plan_register_export.argtypes = [c_p, c_p, c_sz, c_p, ctypes.POINTER(c_sz)]
         L.sccl_plan_register_bind.argtypes = [c_p, c_p, ctypes.POINTER(c_p), c_sz]
         L.sccl_plan_deregister.argtypes = [c_p, c_p]
@@ -181,7 +183,7 @@ def version() -> str:
 PROTOCOLS = {"auto": 0, "simple": 1, "ll": 2}
 
 
-MEM_HANDLES = {"ipc": 0, "vmm": 1}
+MEM_HANDLES = {"ipc": 0, "vmm": 1, "external": 2}
 
 
 PULL = {"auto": 0, "on": 1, "off": -1}
@@ -293,7 +295,7 @@ class Plan(_PlanBase):
                  device: int = 0, nchannels: int = 0, tile_bytes: int = 0, timeout_ms: int = 0,
                  chunk_groups: int = 0, protocol: str = "auto", mem_handles: str = "ipc", pull: str = "auto"):
         super().__init__()
-        self.mem_handles = mem_handles
+        self.mem_handles, self.device = mem_handles, device
         o = _opts(device, nchannels, tile_bytes, timeout_ms, chunk_groups, protocol, mem_handles, pull)
         rc = lib().sccl_plan_create(_text(schedule), rank, nranks, bytes_per_rank, dtype, SUM,
                                     ctypes.byref(o), ctypes.byref(self._h))
@@ -364,6 +366,39 @@ class Plan(_PlanBase):
 
     def deregister(self, buf):
         _raise(lib().sccl_plan_deregister(self._h, ctypes.c_void_p(_ptr(buf))))
+
+    def region_bytes(self) -> int:
+        n = ctypes.c_size_t(0)
+        _raise(lib().sccl_plan_region_bytes(self._h, ctypes.byref(n)))
+        return n.value
+
+    def bind_external(self, regions: Sequence[int]):
+        """Bind to caller-provided regions (mem_handles="external"):
+        regions[r] = rank r's region as mapped in this process."""
+        arr = (ctypes.c_void_p * len(regions))(*regions)
+        _raise(lib().sccl_plan_bind_peers_external(self._h, arr))
+
+    def bind_symmetric_memory(self, group=None):
+        """mem_handles="external" through torch symmetric memory (SURVEY.md
+        8(f) f4, a production integration path): the plan region is a
+        symm_mem.empty tensor, rendezvous gives every peer's mapping of its
+        counterpart, and the plan runs on those (no IPC / fd exchange of our
+        own).  Collective; checks that every rank lowered the same plan."""
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        info = self.info()
+        key = (info["program"]["fingerprint"], info["nchannels"], info["tile_bytes"], info["protocol"],
+               self.region_bytes())
+        keys: List[Optional[tuple]] = [None] * self.nranks
+        dist.all_gather_object(keys, key, group=group)
+        if any(k != key for k in keys):
+            raise InvalidArgumentError(INVALID_ARGUMENT, f"ranks lowered different plans: {keys}")
+        t = symm_mem.empty(self.region_bytes(), dtype=torch.uint8, device=torch.device("cuda", self.device))
+        hdl = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
+        self.bind_external(list(hdl.buffer_ptrs))
+        dist.barrier(group=group)  # every region zeroed before any rank's first launch
+        self._symm = (t, hdl)
 
     def recv_buffer(self):
         p = ctypes.c_void_p(0)

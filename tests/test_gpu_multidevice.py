@@ -95,6 +95,25 @@ for name, js, dts in scheds:
                     dist.barrier()
                 plan.close()
                 n_ok += 1
+# torch symmetric memory as the plan region (one rank per GPU)
+if MEM == "ipc" and not SHARE:
+    for name, js, dts in scheds[:3]:
+        d = json.loads(js)
+        for proto in ("ll", "simple"):
+            nb = 1 << 20
+            plan = sccl.Plan(js, rank, W, nb, dts[0], device=dev, protocol=proto, timeout_ms=120000,
+                             mem_handles="external")
+            plan.bind_symmetric_memory()
+            ins = O.seeded_inputs(d["collective"], W, nb, dts[0], 77)
+            want = O.execute(d, ins, nb, dts[0])[rank]
+            recv = torch.full((plan.recv_bytes,), 0xEE, dtype=torch.uint8, device="cuda")
+            plan.launch(torch.from_numpy(ins[rank]).cuda(), recv)
+            torch.cuda.synchronize()
+            plan.check()
+            assert np.array_equal(recv.cpu().numpy(), want), ("symm_mem", name, proto, rank)
+            dist.barrier()
+            plan.close()
+            n_ok += 1
 print("OK", rank, n_ok, flush=True)
 dist.destroy_process_group()
 """

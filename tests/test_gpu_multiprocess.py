@@ -107,6 +107,63 @@ for proto in ("simple", "ll"):
     plan.deregister(target)
     plan.close()
     print("OK", rank, "registered", proto, flush=True)
+# caller-provided plan regions (mem_handles="external"): torch symmetric
+# memory refuses two ranks on one device ("detected allocations from
+# overlapping devices"), so here the regions are raw cudaMalloc allocations
+# shared with cudaIpcGetMemHandle / cudaIpcOpenMemHandle (the CUDA runtime
+# called directly through ctypes); test_gpu_multidevice.py binds torch
+# symmetric memory with one rank per GPU
+import ctypes, glob
+import nvidia.cuda_runtime as _crt
+rt = ctypes.CDLL(glob.glob(os.path.join(_crt.__path__[0], "lib", "libcudart.so*"))[0])
+class IpcHandle(ctypes.Structure):  # cudaIpcMemHandle_t, passed by value
+    _fields_ = [("reserved", ctypes.c_char * 64)]
+rt.cudaIpcGetMemHandle.argtypes = [ctypes.POINTER(IpcHandle), ctypes.c_void_p]
+rt.cudaIpcOpenMemHandle.argtypes = [ctypes.POINTER(ctypes.c_void_p), IpcHandle, ctypes.c_uint]
+js = S.allreduce_from(S.one_shot_allgather(W)) if W == 2 else S.to_json(S.ring_allgather(W))
+d = json.loads(js)
+nb = 1 << 18
+dt = O.BF16 if d["collective"] == "allreduce" else O.U8
+for proto in ("simple", "ll"):
+    plan = sccl.Plan(js, rank, W, nb, dt, device=0, protocol=proto, timeout_ms=120000, mem_handles="external")
+    how, opened, mine = "cuda_ipc", [], ctypes.c_void_p(0)
+    if True:  # (symmetric memory: test_gpu_multidevice.py, one rank per GPU)
+        assert rt.cudaMalloc(ctypes.byref(mine), ctypes.c_size_t(plan.region_bytes())) == 0
+        h = IpcHandle()
+        rc = rt.cudaIpcGetMemHandle(ctypes.byref(h), mine)
+        assert rc == 0, ("cudaIpcGetMemHandle", rc)
+        handles = [None] * W
+        dist.all_gather_object(handles, ctypes.string_at(ctypes.addressof(h), 64))  # (.reserved stops at a NUL)
+        ptrs = []
+        for r in range(W):
+            if r == rank:
+                ptrs.append(mine.value)
+                continue
+            q = ctypes.c_void_p(0)
+            hr = IpcHandle()
+            ctypes.memmove(ctypes.byref(hr), handles[r], 64)
+            rc = rt.cudaIpcOpenMemHandle(ctypes.byref(q), hr, 1)
+            assert rc == 0, ("cudaIpcOpenMemHandle", rc)
+            opened.append(q)
+            ptrs.append(q.value)
+        plan.bind_external(ptrs)
+        dist.barrier()
+    for it in range(2):
+        ins = O.seeded_inputs(d["collective"], W, nb, dt, 50 + it)
+        ref = O.execute(d, ins, nb, dt)
+        recv = torch.zeros(ref[rank].size, dtype=torch.uint8, device="cuda")
+        plan.launch(torch.from_numpy(ins[rank]).cuda(), recv)
+        torch.cuda.synchronize()
+        plan.check()
+        assert np.array_equal(recv.cpu().numpy(), ref[rank]), ("external", how, proto, it)
+        dist.barrier()
+    plan.close()
+    for q in opened:
+        rt.cudaIpcCloseMemHandle(q)
+    dist.barrier()
+    if mine.value:
+        rt.cudaFree(mine)
+    print("OK", rank, "external", how, proto, flush=True)
 dist.destroy_process_group()
 """
 
@@ -133,4 +190,6 @@ def test_processes_one_gpu(tmp_path, world, mem):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
     text = "".join(o for o, _ in outs)
-    assert text.count("OK") == (5 if world == 2 else 7) * world + 2 * world, text
+    if os.environ.get("SCCL_TEST_VERBOSE"):
+        print(text)
+    assert text.count("OK") == (5 if world == 2 else 7) * world + 4 * world, text
