@@ -60,6 +60,8 @@ def workload_schedule(P: int, which: str) -> str:
     """bench schedule file for the allgather workload at P ranks"""
     if which == "auto":
         which = "ham" if P in (2, 8) else "oneshot"
+    if P == 1:  # the multi-process path's one-GPU self-test (SCCL_BENCH_FORCE_MULTI=1)
+        which = "oneshot"
     return {"ham": f"ag_ham_full{P}", "oneshot": f"ag_oneshot_full{P}", "ring": f"ag_ring_ring{P}"}[which]
 
 
@@ -442,6 +444,8 @@ def loopback_extras(args, sccl, plan, send, recv, stream, peaks):
     P = 8
     out = {}
     pk = peaks["hbm_gbs"]
+    if send[0].numel() < (64 << 20):  # the sweeps below slice the workload's buffers
+        return {"extras_skipped": "the config 1/3/4 sweeps need --bytes >= 64 MiB"}
     # latency sweep (CUDA-graph timed): allgathers, allreduces, alltoall
     sweep = []
     for sz in (1 << 10, 8 << 10, 64 << 10, 1 << 20, 16 << 20):
@@ -898,13 +902,16 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
              if os.path.exists(os.path.join(SCHED_DIR, n + ".json"))]
     texts = [load_schedule(n) for n in cands]
     sweep = []
-    for sz in (1 << 10, 4 << 10, 16 << 10, 64 << 10, 1 << 20, 64 << 20, 256 << 20):
+    sizes = (1 << 10, 4 << 10, 16 << 10, 64 << 10, 1 << 20, 64 << 20, 256 << 20)
+    s_all = torch.randint(0, 256, (max(sizes),), dtype=torch.uint8, device=dev)  # (not the workload's m bytes)
+    r_all = torch.empty(P * max(sizes), dtype=torch.uint8, device=dev)
+    for sz in sizes:
         i, proto, _ = sccl.select(texts, sz, sccl.U8, multiprocess=True)
         p4 = sccl.Plan(texts[i], rank, P, sz, sccl.U8, device=dev_index, protocol=proto, mem_handles=args.mem)
         p4.bind_with()
         reg4, _ = p4.recv_buffer()
-        s4 = send[:sz]
-        r4 = ref[:P * sz]
+        s4 = s_all[:sz]
+        r4 = r_all[:P * sz]
         iters = 200 if sz <= (64 << 10) else 20
         t = timed(lambda: p4.launch(s4, reg4), iters)
         tn = timed(lambda: dist.all_gather_into_tensor(r4, s4), iters)
@@ -939,7 +946,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.gpus == 1 and "WORLD_SIZE" not in os.environ or os.environ.get("WORLD_SIZE") == "1":
+    elif (args.gpus == 1 and "WORLD_SIZE" not in os.environ or os.environ.get("WORLD_SIZE") == "1") and \
+            os.environ.get("SCCL_BENCH_FORCE_MULTI") != "1":
         run_loopback(args)
     else:
         run_multi(args)

@@ -19,6 +19,12 @@ OUT = os.path.join(ROOT, "tests", "golden", "schedules", "bench")
 def bench_schedules():
     """name -> canonical schedule JSON"""
     out = {}
+    # P = 1 (a local copy): bench.py's multi-process path self-test on one GPU
+    # (SCCL_BENCH_FORCE_MULTI=1 with one torchrun rank: a real NCCL communicator)
+    one1 = S.one_shot_allgather(1)
+    out["ag_oneshot_full1"] = sccl.canonicalize(S.to_json(one1))
+    out["ar_oneshot_full1"] = sccl.canonicalize(S.allreduce_from(one1))
+    out["a2a_direct_full1"] = sccl.canonicalize(S.to_json(S.direct_alltoall(1)))
     for P in (2, 4, 8):
         one = S.one_shot_allgather(P)
         out[f"ag_oneshot_full{P}"] = sccl.canonicalize(S.to_json(one))
