@@ -86,7 +86,8 @@ def _profile_traffic(key: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks, board power and throttle reasons sampled during the timed
+    region (NVML in-process; nvidia-smi if NVML is unavailable)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -98,7 +99,46 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_handle(self):
+        """In-process NVML (the device matched by PCI bus id), sampled every
+        50 ms: more samples than one nvidia-smi process per 0.2 s, plus the
+        board power.  (The two samplers time the bench workload alike:
+        tools/gpu_runs/r02/s2_sampler_ab.sh.)"""
+        if os.environ.get("SCCL_BENCH_SMI") == "1":  # A/B: the subprocess sampler
+            return None, None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            try:
+                return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return None, None
+
     def _run(self):
+        nv, h = self._nvml_handle()
+        self.kind = "nvml" if h is not None else "nvidia-smi"
+        if h is not None:
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            while not self._stop.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                    pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append([str(self.index), str(sm), str(mx), f"{pw:.1f}", hex(rs)] +
+                                     ["Active" if rs & b else "Not Active" for b in bits.values()])
+                except Exception:
+                    pass
+                self._stop.wait(0.05)
+            return
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -127,8 +167,10 @@ class ClockSampler:
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None,
+                "sampler": getattr(self, "kind", None)}
 
 
 def busbytes(coll: str, P: int, m: int) -> int:

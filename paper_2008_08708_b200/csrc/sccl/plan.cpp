@@ -200,12 +200,12 @@ void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const C
 // chunks are cut into byte parts so every SM streams (one stage per part:
 // fewer, longer parts lost more to idle SMs than they gained in
 // pipelining); small chunks are spread over chunk groups so independent
-// chunks travel in parallel instead of queueing in one CTA.  A streaming,
-// copy-only relay schedule with >= 4 ops per step (the (7,7,7) allgather:
-// 7) splits into two chunk groups, so a CTA's window holds fewer ops per
-// step and a relayed receipt is forwarded sooner after it lands: (7,7,7)
-// at 128 MiB/rank 1979 -> 1869 us (64 MiB 993 -> 975, 512 MiB 8048 -> 7595;
-// 16 MiB 254 -> 289, hence its 4 GB floor); combining schedules lost.
+// chunks travel in parallel instead of queueing in one CTA.  With
+// ModePolicy::group_split (off in both default tables since round 2.1) a
+// streaming, copy-only relay schedule with >= 4 ops per step splits into
+// two chunk groups, so a CTA's window holds fewer ops per step: round 1's
+// (7,7,7) at 128 MiB/rank went 1979 -> 1869 us with it; the round-2
+// pipeline runs one group faster (1752 -> 1730 us; policy.cpp).
 void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const ChannelRequest& req, bool loopback,
                      const ModePolicy& pol) {
   const int bps = req.blocks_per_sm ? req.blocks_per_sm(req.ctx, p.ll ? 0 : p.tile, p.nstage)

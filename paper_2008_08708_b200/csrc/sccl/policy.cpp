@@ -15,16 +15,22 @@ namespace {
 // Loopback (all ranks in one HBM): the round-1 B200 measurements.
 //  * protocol fit: tools/fit_protocol.py over the loopback crossover sweep
 //    (7 schedules x 16 KiB-16 MiB x both protocols), mean regret 0.9 %;
-//  * 1 GB streaming threshold, window-major, L2 hints, discards and the
-//    chunk-group split: profiles/r01/window, l2policy, discard;
+//  * 1 GB streaming threshold, window-major, L2 hints and discards:
+//    profiles/r01/window, l2policy, discard;
+//  * no chunk-group split: round 1 split the (7,7,7) allgather's chunks into
+//    two groups above 4 GB of traffic, but with the round-2 pipeline one
+//    group is faster at every size (64 / 128 / 256 / 512 MiB per rank:
+//    911 / 1752 / 3518 / 7044 -> 872 / 1730 / 3509 / 6903 us, medians of 3;
+//    tools/gpu_runs/r02/s2_ag_split_ab.sh, profiles/r02/s2_ag_split_ab.jsonl);
 //  * self-publish up to 16 tiles per CTA (tools/gpu_runs/r01/winsig_round1h.sh).
 ModePolicy loopback_default() {
   ModePolicy p;
-  p.version = "loopback-b200-r02";
+  p.version = "loopback-b200-r02.1";
   p.ll_c = 4.80, p.ll_alpha = 0.522, p.ll_beta = 0.353;
   p.simple_c = 4.50, p.simple_alpha = 2.72, p.simple_beta = 0.126;
   p.stream_bytes = 1e9;
-  p.window_major = p.l2_hints = p.discard = p.group_split = true;
+  p.window_major = p.l2_hints = p.discard = true;
+  p.group_split = false;
   p.max_ctas_per_rank = 0;
   p.selfpub_max_tiles = 16;
   return p;

@@ -53,11 +53,14 @@ def test_window_size_follows_ops_per_step():
     assert ar56["window"] == ar56["tile_bytes"]
 
 
-def test_chunk_group_split_for_big_copy_relays():
+def test_no_chunk_group_split_for_big_copy_relays():
+    # round 2: one chunk group beat the round-1 two-group split at 64-512 MiB
+    # (profiles/r02/s2_ag_split_ab.jsonl); the split stays as a policy-table
+    # flag (group_split) for SCCL_POLICY overrides
     big = info("ag777", 128 << 20, protocol="simple")
-    assert big["chunk_groups"] == 2 and big["window"] == 2 * big["tile_bytes"]
-    assert info("ag777", 16 << 20, protocol="simple")["chunk_groups"] == 1  # below 4 GB of traffic: no split
-    assert info("ar56", 128 << 20, protocol="simple")["chunk_groups"] == 1  # combining: no split
+    assert big["chunk_groups"] == 1 and big["window"] == big["tile_bytes"]
+    assert info("ag777", 16 << 20, protocol="simple")["chunk_groups"] == 1
+    assert info("ar56", 128 << 20, protocol="simple")["chunk_groups"] == 1
 
 
 def test_l2_hints_above_one_gigabyte():
@@ -165,16 +168,20 @@ def test_policy_table_override(tmp_path):
     t = tmp_path / "policy.json"
     t.write_text(json.dumps({"multiprocess": {"version": "multiprocess-test", "window_major": True,
                                               "l2_hints": True, "max_ctas_per_rank": 8,
-                                              "simple_alpha": 100.0}}))
+                                              "simple_alpha": 100.0},
+                             "loopback": {"version": "loopback-test", "group_split": True}}))
     code = ("import sys, json; sys.path.insert(0, %r)\n"
             "from paper_2008_08708_b200 import sccl, schedules as S\n"
             "js = S.to_json(S.hamiltonian_allgather(8))\n"
             "i = sccl.Plan(js, 0, 8, 128 << 20, sccl.U8, device=-1, protocol='simple').info()\n"
             "j = sccl.Plan(js, 0, 8, 1 << 20, sccl.U8, device=-1).info()\n"
-            "print(json.dumps([i['policy'], i['window'] > 0, i['l2hint'], i['nchannels'], j['protocol']]))"
+            "k = sccl.LoopbackPlan(js, 128 << 20, sccl.U8, device=-1, protocol='simple').info()\n"
+            "print(json.dumps([i['policy'], i['window'] > 0, i['l2hint'], i['nchannels'], j['protocol'],\n"
+            "                  k['policy'], k['chunk_groups']]))"
             % str(sccl._HERE.rsplit("/", 1)[0]))
     out = subprocess.run([sys.executable, "-c", code], env={**__import__("os").environ, "SCCL_POLICY": str(t)},
                          capture_output=True, text=True, check=True).stdout
-    pol, window, l2, nch, proto = json.loads(out)
+    pol, window, l2, nch, proto, lpol, kc = json.loads(out)
     assert pol == "multiprocess-test" and window and l2 == 1 and nch <= 8
     assert proto == "ll"  # a 100 us bulk step makes LL win at 1 MiB
+    assert lpol == "loopback-test" and kc == 2  # the round-1 chunk-group split, back on by table
