@@ -177,6 +177,14 @@ void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const C
     // put twice the CTAs on the chunks (AR (8,2,2) 512 KiB-2 MiB per rank:
     // -13..-26 %, tools/gpu_runs/r01/midtile2_round1w.sh)
     tile = wide ? (maxlen <= (256 << 10) ? 16384 : kMaxTile) : 32768;
+    // pull-lowered ones (the loopback one-shot allreduce: one fan-in-P op
+    // per rank, nothing re-read) keep 16 KiB tiles up to 512 KiB chunks and
+    // again from 250 MB of program traffic to the streaming threshold: AR
+    // (8,2,2) bf16 at 4 / 16 / 32 / 48 MiB per rank 19.7 / 54.0 / 101.5 /
+    // 148.5 -> 15.3 / 53.3 / 95.9 / 138.2 us; 8 and 12 MiB keep 64 KiB
+    // (27.0 vs 31.6, 41.0 vs 42.4 us) (tools/gpu_runs/r02/s2_ar822_tile.sh)
+    if (wide && p.pg.pull && st.reduces && !st.rereads && (maxlen <= (512 << 10) || st.bytes >= 250e6))
+      tile = 16384;
     // one-shot copies (one fan-out op per rank, nothing re-read) up to
     // 512 KiB: two 16 KiB tiles per CTA overlap the load of one with the
     // stores of the other (AG (1,1,1) 256 / 512 KiB: -27 / -16 %)
