@@ -502,7 +502,13 @@ void choose_streaming(sccl_plan& p, const ProgramStats& st, bool loopback, const
     const long w = std::atol(env);
     p.window = (w > 0 && all_vec && !p.ll) ? uint32_t(std::max<long>(16, w) / 16 * 16) : 0u;
   }
-  p.l2hint = streams && pol.l2_hints ? 1 : 0;
+  // pull-lowered reductions with no receipts (the loopback one-shot
+  // allreduce) run better without evict-first hints: AR (8,2,2) bf16 at
+  // 64 / 128 / 256 MiB per rank 182.7 / 358.5 / 713.1 -> 181.3 / 352.6 /
+  // 696.3 us (tools/gpu_runs/r02/s2_verify1.sh); copy-only one-shots keep
+  // them (A2A (8,1,1) +3.4 / +2.5 % without, profiles/r02/s2_rule_audit.jsonl)
+  const bool pulled_oneshot = p.pg.pull && st.reduces && !st.rereads;
+  p.l2hint = streams && pol.l2_hints && !pulled_oneshot ? 1 : 0;
   const char* hint_env = std::getenv("SCCL_L2HINT");  // 0, 1, or 3 (| kL2RelayPlain)
   if (hint_env) p.l2hint = std::atoi(hint_env) & 3;
   if (p.l2hint == kL2RelayPlain) p.l2hint = 0;

@@ -76,6 +76,8 @@ def test_pulled_one_shot_allreduce_tiles(mb, tile):
 def test_l2_hints_above_one_gigabyte():
     assert info("ag777", 128 << 20, protocol="simple")["l2hint"] == 1
     assert info("a2a", 128 << 20, protocol="simple")["l2hint"] == 1
+    assert info("ar822", 128 << 20, protocol="simple")["l2hint"] == 0  # pulled one-shot: faster without (round 2)
+    assert info("ar822", 128 << 20, protocol="simple", pull="off")["l2hint"] == 1
     assert info("ar822", 16 << 20, protocol="simple")["l2hint"] == 0
     assert info("ag777", 1 << 20, protocol="simple")["l2hint"] == 0
 
