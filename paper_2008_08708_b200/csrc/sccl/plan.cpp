@@ -113,11 +113,19 @@ struct ProgramStats {
   bool rereads = false;     // some op reads a receipt (a relay or a reduction)
   bool reduces = false;
   size_t nops_rank0 = 0;    // rank 0's non-WAIT ops
+  int work_chunks = 0;      // most distinct chunks any one rank has non-WAIT ops on
 };
 
 ProgramStats program_stats(const Schedule& sched, const Program& pg, bool loopback) {
   ProgramStats st;
   for (auto* ph : sched.flat()) st.steps += ph->S;
+  for (size_t r = 0; r < pg.ranks.size(); ++r) {
+    std::vector<int> chunks;
+    for (auto& op : pg.ranks[r].ops)
+      if (op.kind != OP_WAIT) chunks.push_back(op.chunk);
+    std::sort(chunks.begin(), chunks.end());
+    st.work_chunks = std::max(st.work_chunks, int(std::unique(chunks.begin(), chunks.end()) - chunks.begin()));
+  }
   for (size_t r = 0; r < pg.ranks.size(); ++r)
     for (auto& op : pg.ranks[r].ops) {
       if (op.kind == OP_WAIT) continue;
@@ -237,6 +245,16 @@ void choose_channels(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const
   } else {
     kb = int(std::max<int64_t>(1, std::min<int64_t>(cap, (maxlen + part - 1) / part)));
     kc = req.chunk_groups > 0 ? req.chunk_groups : std::max(1, std::min(p.pg.G, cap / kb));
+    // simple protocol: receipts land in place (only LL unpacks them in an op
+    // of the receiver), so a rank has work in as many chunk groups as it has
+    // chunks with data ops -- one for one-shot copies and pulled one-shot
+    // reductions.  Groups past that only wait; give their CTAs to byte parts
+    // instead, down to 8 KiB per CTA: AG (1,1,1) at 64 KiB per rank 9.9 ->
+    // 7.1 us (8 x 4 -> 1 x 8 CTAs per rank; tools/gpu_runs/r02/s2_ll_audit.sh)
+    if (!p.ll && req.chunk_groups <= 0 && st.work_chunks >= 1 && kc > st.work_chunks) {
+      kc = st.work_chunks;
+      while (2 * kc * kb <= cap && maxlen / (2 * kb) >= (8 << 10)) kb *= 2;
+    }
     if (req.chunk_groups <= 0 && kc == 1 && kb >= 4 && !p.ll && pol.group_split && st.bytes > 4 * pol.stream_bytes &&
         st.rereads &&
         !st.reduces && double(st.nops_rank0) >= 4.0 * st.steps) {

@@ -73,6 +73,18 @@ def test_pulled_one_shot_allreduce_tiles(mb, tile):
         assert info("ar822", mb << 20, protocol="simple", pull="off")["tile_bytes"] == 65536
 
 
+def test_simple_chunk_groups_follow_the_chunks_a_rank_works_on():
+    # round 2: one-shot copies / pulled one-shot reductions have one chunk of
+    # work per rank in the simple protocol; the CTAs go to byte parts
+    # (profiles/r02/s2_workchunks_ab.jsonl)
+    i = info("ag111", 64 << 10, protocol="simple")
+    assert (i["chunk_groups"], i["byte_parts"]) == (1, 8)
+    i = info("ar822", 1 << 20, protocol="simple")
+    assert (i["chunk_groups"], i["byte_parts"]) == (1, 16)
+    assert info("a2a", 256 << 10, protocol="simple")["chunk_groups"] == 8  # 8 chunks of work per rank
+    assert info("ag111", 1 << 10, protocol="ll")["chunk_groups"] == 8      # LL unpacks receipts in ops: unchanged
+
+
 def test_l2_hints_above_one_gigabyte():
     assert info("ag777", 128 << 20, protocol="simple")["l2hint"] == 1
     assert info("a2a", 128 << 20, protocol="simple")["l2hint"] == 1
