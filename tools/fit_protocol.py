@@ -4,7 +4,9 @@ protocol from a crossover sweep (tools/tune.py lines with "protocol": ll /
 simple forced), by relative-error least squares, and report the regret of
 the fitted choice against the best protocol per (schedule, size).
 
-usage: python tools/fit_protocol.py sweep.jsonl [...]"""
+usage: python tools/fit_protocol.py sweep.jsonl [...] [--eval llc,lla,llb,sc,sa,sb]
+(--eval: also report the regret of the given constants, e.g. the policy
+table's current ones)"""
 import collections
 import json
 import sys
@@ -42,8 +44,32 @@ def fit(pts, proto):
     return sol
 
 
+def regret(pts, co):
+    regrets = []
+    for (s, sz), d in sorted(pts.items()):
+        if len(d) < 2:
+            continue
+        pred = {p: co[p][0] + co[p][1] * STEPS[s] + co[p][2] * d[p][1] for p in d}
+        pick = min(pred, key=pred.get)
+        best = min(v[0] for v in d.values())
+        regrets.append((d[pick][0] / best - 1, s, sz, pick))
+    return regrets
+
+
 def main():
-    pts = load(sys.argv[1:])
+    args = [a for a in sys.argv[1:] if not a.startswith("--eval")]
+    ev = [a.split("=", 1)[1] if "=" in a else None for a in sys.argv[1:] if a.startswith("--eval")]
+    if "--eval" in sys.argv:
+        i = sys.argv.index("--eval")
+        ev = [sys.argv[i + 1]]
+        args = [a for j, a in enumerate(sys.argv[1:], 1) if j not in (i, i + 1)]
+    pts = load(args)
+    if ev and ev[0]:
+        v = [float(x) for x in ev[0].split(",")]
+        r = regret(pts, {"ll": v[:3], "simple": v[3:]})
+        a = np.array([x[0] for x in r])
+        print(f"given constants: points {len(a)}  mean regret {100 * a.mean():.1f} %  worst {100 * a.max():.1f} % "
+              f"({max(r)[1]} {max(r)[2]})")
     co = {p: fit(pts, p) for p in ("ll", "simple")}
     for p, (c, a, b) in co.items():
         print(f"{p:6s} c={c:.2f} us  a={a:.3f} us/step  b={b:.4f} us/MB")
