@@ -248,9 +248,11 @@ def _workload_text(gpus: int, P: int, name: str) -> str:
 
 
 # --------------------------------------------------------------------------- GPU helpers
-def graph_time_us(plan, send, recv, stream, iters):
+def graph_time_us(plan, send, recv, stream, iters, reps=3):
     """Device time per launch: `iters` launches captured in one CUDA graph
-    (host launch cost excluded), replayed twice, the second replay timed."""
+    (host launch cost excluded), replayed once untimed, then `reps` timed
+    replays; the median replay (a single short replay of microsecond
+    launches moved with the clock state the previous sweep point left)."""
     import torch
     for _ in range(3):
         plan.launch(send, recv, stream)
@@ -259,16 +261,19 @@ def graph_time_us(plan, send, recv, stream, iters):
     with torch.cuda.graph(g, stream=stream):
         for _ in range(iters):
             plan.launch(send, recv, stream)
+    ts = []
     with torch.cuda.stream(stream):  # replay() launches on the current stream
         g.replay()
         stream.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        g.replay()
-        b.record(stream)
-    stream.synchronize()
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            stream.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3 / iters)
     plan.check()
-    return a.elapsed_time(b) * 1e3 / iters
+    return statistics.median(ts)
 
 
 def oracle_check_loopback(sccl, name, nbytes, dtype, seed=5):
@@ -498,7 +503,7 @@ def loopback_extras(args, sccl, plan, send, recv, stream, peaks):
             p2 = sccl.LoopbackPlan(load_schedule(nm), sz, dt, device=0)
             coll = json.loads(load_schedule(nm))["collective"]
             us = graph_time_us(p2, [x[:p2.send_bytes] for x in send], [x[:p2.recv_bytes] for x in recv], stream,
-                               50 if sz < (1 << 20) else 10)
+                               200 if sz < (1 << 20) else 10)
             row[f"{tag}_us"] = round(us, 2)
             row[f"{tag}_busbw_per_rank_GBps"] = round(busbytes(coll, P, sz) / (us * 1e-6) / 1e9, 2)
             row[f"{tag}_protocol"] = p2.info()["protocol"]

@@ -26,6 +26,9 @@ cases = [
     (S.allreduce_from(S.hamiltonian_allgather(8)), 65536, O.BF16, "simple"),
     (S.allreduce_from(S.one_shot_allgather(8)), 8192, O.F32, "ll"),
     (S.allreduce_from(S.one_shot_allgather(8)), 40960, O.BF16, "simple", "off"),
+    # round 2 session 2: one chunk group, byte parts below a tile (one-shot copy / pulled one-shot reduce)
+    (S.to_json(S.one_shot_allgather(8)), 65536 + 48, O.U8, "simple"),
+    (S.allreduce_from(S.one_shot_allgather(8)), 1 << 20, O.BF16, "simple"),
 ]
 bad = 0
 for js, nb, dt, proto, *pull in cases:
