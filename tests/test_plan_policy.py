@@ -83,6 +83,13 @@ def test_simple_chunk_groups_follow_the_chunks_a_rank_works_on():
     assert (i["chunk_groups"], i["byte_parts"]) == (1, 16)
     assert info("a2a", 256 << 10, protocol="simple")["chunk_groups"] == 8  # 8 chunks of work per rank
     assert info("ag111", 1 << 10, protocol="ll")["chunk_groups"] == 8      # LL unpacks receipts in ops: unchanged
+    js, dt = SCHED["ag111"]  # one rank per GPU: the same cap (32 CTAs per rank, all on the rank's chunk)
+    mp = sccl.Plan(js, 0, P, 256 << 10, dt, device=-1, protocol="simple")
+    try:
+        i = mp.info()
+    finally:
+        mp.close()
+    assert (i["chunk_groups"], i["byte_parts"]) == (1, 32)
 
 
 def test_l2_hints_above_one_gigabyte():
