@@ -126,19 +126,13 @@ def _world():
     return min(n, 8)
 
 
-@pytest.mark.timeout(1800)
-@pytest.mark.parametrize("mem", ["ipc", "vmm"])
-def test_one_rank_per_gpu(tmp_path, mem):
-    W = _world()
-    if W < 2:
-        pytest.skip(f"one rank per GPU needs >= 2 CUDA devices, {W} visible (set SCCL_MULTIDEVICE_SHARE=1 "
-                    "to run the harness with every rank on cuda:0)")
+def _run(tmp_path, W, mem, share):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     script = tmp_path / "w.py"
     script.write_text(WORKER.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"), port=port))
-    procs = [subprocess.Popen([sys.executable, str(script), str(r), str(W), mem, "1" if SHARE else "0"],
+    procs = [subprocess.Popen([sys.executable, str(script), str(r), str(W), mem, "1" if share else "0"],
                               stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(W)]
     try:
         outs = [p.communicate(timeout=1700) for p in procs]
@@ -149,3 +143,25 @@ def test_one_rank_per_gpu(tmp_path, mem):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
     assert sum("OK" in o for o, _ in outs) == W
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("mem", ["ipc", "vmm"])
+def test_one_rank_per_gpu(tmp_path, mem):
+    W = _world()
+    if W < 2:
+        pytest.skip(f"one rank per GPU needs >= 2 CUDA devices, {W} visible (set SCCL_MULTIDEVICE_SHARE=1 "
+                    "to run the harness with every rank on cuda:0)")
+    _run(tmp_path, W, mem, SHARE)
+
+
+@pytest.mark.timeout(1800)
+def test_eight_rank_processes_time_sliced_on_one_gpu(tmp_path):
+    """The 8-rank multi-process configuration of the 8 x B200 box (every P=8
+    schedule the bench uses, (7,7,7) and (56,14,14) included) with eight
+    processes -- eight CUDA contexts, IPC-mapped regions, sys-scope
+    counters, entry handshakes -- all on cuda:0.  Correctness only (the
+    contexts time-slice); runs on any box with a GPU."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    _run(tmp_path, 8, "ipc", True)
