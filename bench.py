@@ -44,6 +44,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "collective bus GB/s and latency vs buffer size at 2/4/8 B200 vs NCCL and CPU ref"
 NVLINK_PEAK = 900.0  # GB/s per direction per GPU, NVLink 5 (nominal)
+# N > 1: peer-wait watchdog of every bench plan (the library default for one
+# rank per GPU is 600 s); every launch here takes milliseconds, so a peer that
+# has not signalled within a minute is a failure the line should report
+BENCH_TIMEOUT_MS = 60000
+# N > 1: the comparison sections (NCCL, NVLS, sweep) start only while the run
+# is younger than this; the line says which were skipped
+EXTRAS_BUDGET_S = float(os.environ.get("SCCL_BENCH_EXTRAS_S", "420"))
 
 
 def load_schedule(name: str) -> str:
@@ -709,6 +716,7 @@ def run_multi(args):
     import torch
     import torch.distributed as dist
     from paper_2008_08708_b200 import sccl
+    t_start = time.perf_counter()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     # SCCL_BENCH_SHARE_GPU=1: every rank on cuda:0 (validates this path on a
@@ -727,7 +735,7 @@ def run_multi(args):
     js = load_schedule(name)
     m = args.bytes
     plan = sccl.Plan(js, rank, P, m, sccl.U8, device=dev_index, nchannels=args.nchannels, tile_bytes=args.tile,
-                     mem_handles=args.mem)
+                     mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
     plan.bind_with()
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
@@ -738,7 +746,10 @@ def run_multi(args):
         plan.launch(send, recv, stream)
     torch.cuda.synchronize()
     ref = gather_ref(dist, send, P, shared, dev)
-    assert torch.equal(ref, recv), f"rank {rank}: allgather differs from the gathered inputs"
+    # recorded, not asserted: a rank that raised here would leave its peers
+    # waiting in the next collective; the line reports every rank's result
+    same = [None] * P
+    dist.all_gather_object(same, bool(torch.equal(ref, recv)))
     regptr, _ = plan.recv_buffer()
     oracle_ok = multi_oracle_check(dist, sccl, rank, P, dev_index, args.mem)
 
@@ -783,7 +794,7 @@ def run_multi(args):
         hr.copy_(recv, non_blocking=True)
     e2e_ms = timed(e2e_step, max(3, min(args.steps, 10)))
     baselines = {} if (shared or args.no_sweep) else nccl_baselines(args, dist, sccl, rank, P, dev, dev_index,
-                                                                     send, ref, ms, timed)
+                                                                     send, ref, ms, timed, t_start)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(per_rank * P, 2), "unit": "GB/s", "n_gpus": 1 if shared else P,
@@ -798,6 +809,8 @@ def run_multi(args):
                        "value_convention": "sum over GPUs of per-rank bus GB/s (nccl-tests busBW)"},
             "busbw_per_rank_GBps": round(per_rank, 2),
             "oracle_check": {"bytes_per_rank": 65536, "ranks_bit_exact": oracle_ok},
+            "workload_check": {"what": "every rank's output of the timed workload == torch.distributed all_gather "
+                                       "of the inputs", "ranks_equal": same},
             "roofline": {"bound": "nvlink", "achieved": round(per_rank, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
                          "frac": round(per_rank / NVLINK_PEAK, 4), "traffic": traffic_all[0],
                          "traffic_per_rank": traffic_all, "traffic_source": traffic_src,
@@ -839,7 +852,7 @@ def multi_oracle_check(dist, sccl, rank, P, dev_index, mem):
     nb = 65536
     ins = O.seeded_inputs(d["collective"], P, nb, O.U8, 9)
     want = O.execute(d, ins, nb, O.U8)[rank]
-    plan = sccl.Plan(js, rank, P, nb, sccl.U8, device=dev_index, mem_handles=mem)
+    plan = sccl.Plan(js, rank, P, nb, sccl.U8, device=dev_index, mem_handles=mem, timeout_ms=BENCH_TIMEOUT_MS)
     plan.bind_with()
     recv = torch.zeros(want.size, dtype=torch.uint8, device=f"cuda:{dev_index}")
     plan.launch(torch.from_numpy(ins[rank]).to(recv.device), recv)
@@ -852,13 +865,38 @@ def multi_oracle_check(dist, sccl, rank, P, dev_index, mem):
     return res
 
 
-def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours, timed):
+def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours, timed, t_start):
     """Same-box NCCL (NCCL_PROTO=Simple; alltoall
     as grouped send/recv) beside the executor, each timed
     the same way (max over ranks).  Every NCCL configuration gets its own
-    communicator, created while its NCCL_* variables are set."""
+    communicator, created while its NCCL_* variables are set.
+
+    Each comparison is a section: value checks are recorded (never asserted),
+    an exception is caught and reported under the section's key after every
+    rank has agreed on the outcome, and a section starts only while the run is
+    younger than EXTRAS_BUDGET_S (rank 0 decides for all) -- so one failed or
+    slow comparison costs its own key, not the bench line."""
     import torch
     m = send.numel()
+    out = {}
+
+    def section(key, fn):
+        go = [time.perf_counter() - t_start < EXTRAS_BUDGET_S]
+        dist.broadcast_object_list(go, src=0)
+        if not go[0]:
+            out[key] = {"skipped": f"bench extras budget ({EXTRAS_BUDGET_S:.0f} s) spent"}
+            return
+        err = None
+        try:
+            res = fn()
+        except Exception as e:  # noqa: BLE001 -- reported in the line
+            res, err = None, f"{type(e).__name__}: {e}"[:400]
+        errs = [None] * P
+        dist.all_gather_object(errs, err)
+        if any(errs):
+            out[key] = {"error": {r: e for r, e in enumerate(errs) if e}}
+        else:
+            out[key] = res
 
     def group_with(env):
         old = {k: os.environ.get(k) for k in env}
@@ -876,98 +914,130 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
                     os.environ[k] = v
         return grp
 
-    out = {}
     g_simple = group_with({"NCCL_PROTO": "Simple"})
     g_ring = group_with({"NCCL_ALGO": "Ring"})
     g_tree = group_with({"NCCL_ALGO": "Tree"})
     bw = lambda coll, nbytes, t: round(busbytes(coll, P, nbytes) / (t * 1e-3) / 1e9, 2)
+    agree = lambda ok: (lambda v: (dist.all_gather_object(v, bool(ok)), v)[1])([None] * P)
 
-    # allgather at the workload size
-    ag = {"ours_ms": round(ms_ours, 4), "ours_busbw": bw("allgather", m, ms_ours)}
-    for tag, grp in (("nccl_default", None), ("nccl_simple", g_simple)):
-        t = timed(lambda: dist.all_gather_into_tensor(ref, send, group=grp), args.steps)
-        ag[f"{tag}_ms"], ag[f"{tag}_busbw"] = round(t, 4), bw("allgather", m, t)
-    out["nccl_allgather"] = ag
+    def allgather():  # at the workload size
+        ag = {"ours_ms": round(ms_ours, 4), "ours_busbw": bw("allgather", m, ms_ours)}
+        for tag, grp in (("nccl_default", None), ("nccl_simple", g_simple)):
+            t = timed(lambda: dist.all_gather_into_tensor(ref, send, group=grp), args.steps)
+            ag[f"{tag}_ms"], ag[f"{tag}_busbw"] = round(t, 4), bw("allgather", m, t)
+        return ag
+    section("nccl_allgather", allgather)
 
-    # allreduce bf16 at 64 MiB: our one-shot (and Hamiltonian at P=8) vs NCCL Ring / Tree / default
+    # allreduce bf16 at 64 MiB: our one-shot (and Hamiltonian at P=2/8) vs NCCL Ring / Tree / default
     M = 64 << 20
     x = torch.randint(-16, 17, (M // 2,), device=dev).to(torch.bfloat16)
     y = torch.empty_like(x)
-    ar = {"bytes_per_rank": M}
-    for nm in ([f"ar_oneshot_full{P}"] + ([f"ar_ham_full{P}"] if P in (2, 8) else [])):
-        p2 = sccl.Plan(load_schedule(nm), rank, P, M, sccl.BF16, device=dev_index, mem_handles=args.mem)
-        p2.bind_with()
-        reg, _ = p2.recv_buffer()
-        p2.launch(x.view(torch.uint8), reg)
-        t = timed(lambda: p2.launch(x.view(torch.uint8), reg), args.steps)
-        p2.launch(x.view(torch.uint8), y.view(torch.uint8))
-        torch.cuda.synchronize()
-        z = x.clone()
-        dist.all_reduce(z)
-        torch.cuda.synchronize()
-        assert torch.equal(y, z), f"rank {rank}: {nm} differs from NCCL all_reduce"
-        ar[f"ours_{nm}_ms"], ar[f"ours_{nm}_busbw"] = round(t, 4), bw("allreduce", M, t)
-        p2.close()
-    if sccl.nvls_supported(dev_index, P):  # the switch-offloaded comparison backend
-        nv = sccl.NvlsAllreduce(rank, P, M, sccl.BF16, device=dev_index)
-        nv.launch(x, y)
-        torch.cuda.synchronize()
-        nv.check()
-        z = x.clone()
-        dist.all_reduce(z)
-        torch.cuda.synchronize()
-        ar["nvls_matches_nccl"] = bool(torch.equal(y, z))
-        t = timed(lambda: nv.launch(), args.steps)  # in its multicast-bound buffer (zero-copy)
-        ar["ours_nvls_ms"], ar["ours_nvls_busbw"] = round(t, 4), bw("allreduce", M, t)
-        nv.close()
-    for tag, grp in (("nccl_default", None), ("nccl_ring", g_ring), ("nccl_tree", g_tree), ("nccl_simple", g_simple)):
-        z = x.clone()
-        t = timed(lambda: dist.all_reduce(z, group=grp), args.steps)
-        ar[f"{tag}_ms"], ar[f"{tag}_busbw"] = round(t, 4), bw("allreduce", M, t)
-    out["nccl_allreduce_bf16"] = ar
-
-    # alltoall at 64 MiB: direct (P,1,1) vs NCCL grouped send/recv
-    a_in = torch.randint(0, 256, (M,), dtype=torch.uint8, device=dev)
-    a_out = torch.empty_like(a_in)
-    p3 = sccl.Plan(load_schedule(f"a2a_direct_full{P}"), rank, P, M, sccl.U8, device=dev_index, mem_handles=args.mem)
-    p3.bind_with()
-    reg3, _ = p3.recv_buffer()
-    t = timed(lambda: p3.launch(a_in, reg3), args.steps)
-    p3.launch(a_in, a_out)
-    chk = torch.empty_like(a_in)
-    dist.all_to_all_single(chk, a_in)
+    z_ref = x.clone()
+    dist.all_reduce(z_ref)
     torch.cuda.synchronize()
-    assert torch.equal(chk, a_out), f"rank {rank}: alltoall differs from NCCL"
-    tn = timed(lambda: dist.all_to_all_single(chk, a_in), args.steps)
-    out["nccl_alltoall"] = {"bytes_per_rank": M, "ours_ms": round(t, 4), "ours_busbw": bw("alltoall", M, t),
-                            "nccl_ms": round(tn, 4), "nccl_busbw": bw("alltoall", M, tn)}
-    p3.close()
+
+    def allreduce():
+        ar = {"bytes_per_rank": M}
+        for nm in ([f"ar_oneshot_full{P}"] + ([f"ar_ham_full{P}"] if P in (2, 8) else [])):
+            p2 = sccl.Plan(load_schedule(nm), rank, P, M, sccl.BF16, device=dev_index, mem_handles=args.mem,
+                           timeout_ms=BENCH_TIMEOUT_MS)
+            try:
+                p2.bind_with()
+                reg, _ = p2.recv_buffer()
+                p2.launch(x.view(torch.uint8), reg)
+                t = timed(lambda: p2.launch(x.view(torch.uint8), reg), args.steps)
+                p2.launch(x.view(torch.uint8), y.view(torch.uint8))
+                torch.cuda.synchronize()
+                p2.check()
+                ar[f"ours_{nm}_ms"], ar[f"ours_{nm}_busbw"] = round(t, 4), bw("allreduce", M, t)
+                # integer-valued bf16 inputs: the sum is exact in any order
+                ar[f"ours_{nm}_equals_nccl"] = agree(torch.equal(y, z_ref))
+            finally:
+                p2.close()
+        for tag, grp in (("nccl_default", None), ("nccl_ring", g_ring), ("nccl_tree", g_tree),
+                         ("nccl_simple", g_simple)):
+            z = x.clone()
+            t = timed(lambda: dist.all_reduce(z, group=grp), args.steps)
+            ar[f"{tag}_ms"], ar[f"{tag}_busbw"] = round(t, 4), bw("allreduce", M, t)
+        return ar
+    section("nccl_allreduce_bf16", allreduce)
+
+    # the switch-offloaded comparison backend, only when
+    # every rank's device can join a multicast team
+    sup = [None] * P
+    dist.all_gather_object(sup, bool(sccl.nvls_supported(dev_index, P)))
+
+    def nvls():
+        if not all(sup):
+            return {"skipped": f"no multicast team (nvls_supported per rank: {sup})"}
+        nv = sccl.NvlsAllreduce(rank, P, M, sccl.BF16, device=dev_index)
+        try:
+            nv.launch(x, y)
+            torch.cuda.synchronize()
+            nv.check()
+            r = {"bytes_per_rank": M, "equals_nccl": agree(torch.equal(y, z_ref))}
+            t = timed(lambda: nv.launch(), args.steps)  # in its multicast-bound buffer (zero-copy)
+            nv.check()
+            r["ours_nvls_ms"], r["ours_nvls_busbw"] = round(t, 4), bw("allreduce", M, t)
+            return r
+        finally:
+            nv.close()
+    section("nvls_allreduce_bf16", nvls)
+
+    def alltoall():  # at 64 MiB: direct (P,1,1) vs NCCL grouped send/recv
+        a_in = torch.randint(0, 256, (M,), dtype=torch.uint8, device=dev)
+        a_out = torch.empty_like(a_in)
+        p3 = sccl.Plan(load_schedule(f"a2a_direct_full{P}"), rank, P, M, sccl.U8, device=dev_index,
+                       mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
+        try:
+            p3.bind_with()
+            reg3, _ = p3.recv_buffer()
+            t = timed(lambda: p3.launch(a_in, reg3), args.steps)
+            p3.launch(a_in, a_out)
+            chk = torch.empty_like(a_in)
+            dist.all_to_all_single(chk, a_in)
+            torch.cuda.synchronize()
+            p3.check()
+            same = agree(torch.equal(chk, a_out))
+            tn = timed(lambda: dist.all_to_all_single(chk, a_in), args.steps)
+            return {"bytes_per_rank": M, "ours_ms": round(t, 4), "ours_busbw": bw("alltoall", M, t),
+                    "nccl_ms": round(tn, 4), "nccl_busbw": bw("alltoall", M, tn), "equals_nccl": same}
+        finally:
+            p3.close()
+    section("nccl_alltoall", alltoall)
 
     # latency sweep (<= 64 KB) and bandwidth points (>= 64 MB): allgather with
     # the cost model's per-size choice among this P's schedule files
-    cands = [n for n in (f"ag_oneshot_full{P}", f"ag_ring_ring{P}", f"ag_ham_full{P}")
-             if os.path.exists(os.path.join(SCHED_DIR, n + ".json"))]
-    texts = [load_schedule(n) for n in cands]
-    sweep = []
-    sizes = (1 << 10, 4 << 10, 16 << 10, 64 << 10, 1 << 20, 64 << 20, 256 << 20)
-    s_all = torch.randint(0, 256, (max(sizes),), dtype=torch.uint8, device=dev)  # (not the workload's m bytes)
-    r_all = torch.empty(P * max(sizes), dtype=torch.uint8, device=dev)
-    for sz in sizes:
-        i, proto, _ = sccl.select(texts, sz, sccl.U8, multiprocess=True)
-        p4 = sccl.Plan(texts[i], rank, P, sz, sccl.U8, device=dev_index, protocol=proto, mem_handles=args.mem)
-        p4.bind_with()
-        reg4, _ = p4.recv_buffer()
-        s4 = s_all[:sz]
-        r4 = r_all[:P * sz]
-        iters = 200 if sz <= (64 << 10) else 20
-        t = timed(lambda: p4.launch(s4, reg4), iters)
-        tn = timed(lambda: dist.all_gather_into_tensor(r4, s4), iters)
-        tns = timed(lambda: dist.all_gather_into_tensor(r4, s4, group=g_simple), iters)
-        sweep.append({"bytes_per_rank": sz, "schedule": cands[i], "protocol": proto, "ours_us": round(t * 1e3, 2),
-                      "nccl_us": round(tn * 1e3, 2), "nccl_simple_us": round(tns * 1e3, 2),
-                      "ours_busbw": bw("allgather", sz, t), "nccl_busbw": bw("allgather", sz, tn)})
-        p4.close()
-    out["allgather_sweep_vs_nccl"] = sweep
+    def sweep():
+        cands = [n for n in (f"ag_oneshot_full{P}", f"ag_ring_ring{P}", f"ag_ham_full{P}")
+                 if os.path.exists(os.path.join(SCHED_DIR, n + ".json"))]
+        texts = [load_schedule(n) for n in cands]
+        pts = []
+        sizes = (1 << 10, 4 << 10, 16 << 10, 64 << 10, 1 << 20, 64 << 20, 256 << 20)
+        s_all = torch.randint(0, 256, (max(sizes),), dtype=torch.uint8, device=dev)  # (not the workload's m bytes)
+        r_all = torch.empty(P * max(sizes), dtype=torch.uint8, device=dev)
+        for sz in sizes:
+            i, proto, _ = sccl.select(texts, sz, sccl.U8, multiprocess=True)
+            p4 = sccl.Plan(texts[i], rank, P, sz, sccl.U8, device=dev_index, protocol=proto, mem_handles=args.mem,
+                           timeout_ms=BENCH_TIMEOUT_MS)
+            try:
+                p4.bind_with()
+                reg4, _ = p4.recv_buffer()
+                s4 = s_all[:sz]
+                r4 = r_all[:P * sz]
+                iters = 200 if sz <= (64 << 10) else 20
+                t = timed(lambda: p4.launch(s4, reg4), iters)
+                p4.check()
+                tn = timed(lambda: dist.all_gather_into_tensor(r4, s4), iters)
+                tns = timed(lambda: dist.all_gather_into_tensor(r4, s4, group=g_simple), iters)
+                pts.append({"bytes_per_rank": sz, "schedule": cands[i], "protocol": proto,
+                            "ours_us": round(t * 1e3, 2), "nccl_us": round(tn * 1e3, 2),
+                            "nccl_simple_us": round(tns * 1e3, 2), "ours_busbw": bw("allgather", sz, t),
+                            "nccl_busbw": bw("allgather", sz, tn)})
+            finally:
+                p4.close()
+        return pts
+    section("allgather_sweep_vs_nccl", sweep)
     return out
 
 

@@ -331,38 +331,48 @@ class Plan(_PlanBase):
 
     def bind_with(self, group=None):
         """Exchange handles through torch.distributed (all_gather_object);
-        VMM plans also pass their region fds over Unix sockets (SCM_RIGHTS)."""
+        VMM plans also pass their region fds over Unix sockets (SCM_RIGHTS).
+        Collective, and it fails collectively: a step that raises on one rank
+        raises on every rank (_collective_step), so no peer is left to time
+        out in its first launch against a rank that never bound."""
         import torch.distributed as dist
+        mine = _collective_step(self.export_handles, group)
         blobs: List[Optional[bytes]] = [None] * self.nranks
-        dist.all_gather_object(blobs, self.export_handles(), group=group)
+        dist.all_gather_object(blobs, mine, group=group)
         if self.mem_handles != "vmm":
-            self.bind_peers(blobs)
+            _collective_step(lambda: self.bind_peers(blobs), group)
             return
-        fds = _exchange_fds(self.rank, self.nranks, self.export_fd(), group)
+        fd = _collective_step(self.export_fd, group, cleanup=os.close)
+        fds = _exchange_fds(self.rank, self.nranks, fd, group)
         try:
-            self.bind_peers_fd(blobs, fds)
+            _collective_step(lambda: self.bind_peers_fd(blobs, fds), group)
         finally:
-            for r, fd in enumerate(fds):
-                if r != self.rank and fd >= 0:
-                    os.close(fd)
+            for r, f in enumerate(fds):
+                if r != self.rank and f >= 0:
+                    os.close(f)
 
     def register(self, buf, group=None, nbytes: Optional[int] = None):
         """Register a caller device buffer (torch tensor or pointer) as a
         zero-copy receive target: collective over torch.distributed; every
         rank registers its own buffer.  Launches with recvbuf=buf then have
-        the peers write it directly."""
+        the peers write it directly.  Fails on every rank if it fails on one."""
         import torch.distributed as dist
         ptr = _ptr(buf)
         nb = nbytes if nbytes is not None else buf.numel() * buf.element_size()
-        n = ctypes.c_size_t(0)
-        lib().sccl_plan_register_export(self._h, ctypes.c_void_p(ptr), nb, None, ctypes.byref(n))
-        mine = ctypes.create_string_buffer(n.value)
-        _raise(lib().sccl_plan_register_export(self._h, ctypes.c_void_p(ptr), nb, mine, ctypes.byref(n)))
+
+        def export():
+            n = ctypes.c_size_t(0)
+            lib().sccl_plan_register_export(self._h, ctypes.c_void_p(ptr), nb, None, ctypes.byref(n))
+            mine = ctypes.create_string_buffer(n.value)
+            _raise(lib().sccl_plan_register_export(self._h, ctypes.c_void_p(ptr), nb, mine, ctypes.byref(n)))
+            return mine.raw[:n.value]
+        mine = _collective_step(export, group)
         blobs: List[Optional[bytes]] = [None] * self.nranks
-        dist.all_gather_object(blobs, mine.raw[:n.value], group=group)
+        dist.all_gather_object(blobs, mine, group=group)
         bufs = [ctypes.create_string_buffer(b, len(b)) for b in blobs]
         arr = (ctypes.c_void_p * len(bufs))(*[ctypes.addressof(b) for b in bufs])
-        _raise(lib().sccl_plan_register_bind(self._h, ctypes.c_void_p(ptr), arr, len(blobs[0])))
+        _collective_step(lambda: _raise(lib().sccl_plan_register_bind(self._h, ctypes.c_void_p(ptr), arr,
+                                                                       len(blobs[0]))), group)
 
     def deregister(self, buf):
         _raise(lib().sccl_plan_deregister(self._h, ctypes.c_void_p(_ptr(buf))))
@@ -396,7 +406,7 @@ class Plan(_PlanBase):
             raise InvalidArgumentError(INVALID_ARGUMENT, f"ranks lowered different plans: {keys}")
         t = symm_mem.empty(self.region_bytes(), dtype=torch.uint8, device=torch.device("cuda", self.device))
         hdl = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
-        self.bind_external(list(hdl.buffer_ptrs))
+        _collective_step(lambda: self.bind_external(list(hdl.buffer_ptrs)), group)
         dist.barrier(group=group)  # every region zeroed before any rank's first launch
         self._symm = (t, hdl)
 
@@ -409,6 +419,32 @@ class Plan(_PlanBase):
     def launch(self, sendbuf, recvbuf=None, stream=None):
         _raise(lib().sccl_launch(self._h, ctypes.c_void_p(_ptr(sendbuf)), ctypes.c_void_p(_ptr(recvbuf)),
                                  ctypes.c_void_p(_stream_ptr(stream))))
+
+
+def _collective_step(fn, group=None, cleanup=None):
+    """One local step of a collective setup (export, bind, join ...), run on
+    every rank, then agreed: if it raised on any rank, it raises on every rank
+    -- the first failing rank's status, every failing rank's message -- so no
+    rank goes on into a later collective (a barrier, a fd exchange, a launch
+    whose peers wait for its entry flag) that a failed peer never reaches.
+    cleanup(result) releases this rank's result when another rank failed."""
+    import torch.distributed as dist
+    res, err = None, None
+    try:
+        res = fn()
+    except SCCLError as e:
+        err = (e.code, str(e))
+    except Exception as e:  # noqa: BLE001 -- reported on every rank below
+        err = (INTERNAL, f"{type(e).__name__}: {e}")
+    errs: List[Optional[tuple]] = [None] * dist.get_world_size(group)
+    dist.all_gather_object(errs, err, group=group)
+    bad = [(r, e) for r, e in enumerate(errs) if e is not None]
+    if bad:
+        if err is None and cleanup is not None and res is not None:
+            cleanup(res)
+        _raise(bad[0][1][0], f"collective step failed on rank(s) {[r for r, _ in bad]}: " +
+               "; ".join(f"rank {r}: {e[1]}" for r, e in bad))
+    return res
 
 
 def _exchange_fds(rank: int, nranks: int, my_fd: int, group=None) -> List[int]:
@@ -605,28 +641,39 @@ class NvlsAllreduce:
     nranks = 1 needs no process group (a one-device multicast team)."""
 
     def __init__(self, rank: int, nranks: int, nbytes: int, dtype: int = BF16, device: int = 0, group=None):
+        """Collective for nranks > 1, and it fails collectively: every step
+        (create, rank 0's export, join, bind) is agreed across the ranks
+        (_collective_step), so a multicast team that cannot form raises on
+        every rank instead of leaving peers in a barrier."""
         self._h = ctypes.c_void_p(0)
         self.rank, self.nranks, self.nbytes = rank, nranks, nbytes
-        _raise(lib().sccl_nvls_create(rank, nranks, nbytes, dtype, device, ctypes.byref(self._h)))
+        multi = nranks > 1
+        step = (lambda fn, **kw: _collective_step(fn, group, **kw)) if multi else (lambda fn, **kw: fn())
+        step(lambda: _raise(lib().sccl_nvls_create(rank, nranks, nbytes, dtype, device, ctypes.byref(self._h))))
         fd = -1
-        if nranks > 1:
+        if multi:
             import torch.distributed as dist
-            if rank == 0:
+
+            def export():
+                if rank != 0:
+                    return -1
                 f = ctypes.c_int(-1)
                 _raise(lib().sccl_nvls_export_fd(self._h, ctypes.byref(f)))
-                fd = f.value
+                return f.value
+            fd = step(export, cleanup=lambda f: os.close(f) if f >= 0 else None)
             fd = _share_fd_from_root(rank, nranks, fd, group)
-        try:
-            _raise(lib().sccl_nvls_join(self._h, fd))
-        finally:
-            if fd >= 0:
-                os.close(fd)
-        if nranks > 1:
-            import torch.distributed as dist
+
+        def join():
+            try:
+                _raise(lib().sccl_nvls_join(self._h, fd))
+            finally:
+                if fd >= 0:
+                    os.close(fd)
+        step(join)
+        if multi:
             dist.barrier(group=group)  # every device is in the team before anyone binds
-        _raise(lib().sccl_nvls_bind(self._h))
-        if nranks > 1:
-            import torch.distributed as dist
+        step(lambda: _raise(lib().sccl_nvls_bind(self._h)))
+        if multi:
             dist.barrier(group=group)
 
     def buffer(self):

@@ -132,6 +132,51 @@ def test_gloo_two_process_handle_exchange(tmp_path, mode):
         assert text.count("MISMATCH") == 2
 
 
+_FAIL_WORKER = r"""
+import sys
+sys.path.insert(0, {root!r})
+import torch.distributed as dist
+from paper_2008_08708_b200 import sccl, schedules as S
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=int(sys.argv[1]), world_size=2)
+r = dist.get_rank()
+p = sccl.Plan(S.to_json(S.one_shot_allgather(2)), r, 2, 4096, sccl.U8, device=-1)
+if r == 1:  # only rank 1's local bind fails (e.g. a peer mapping the driver refuses)
+    def bad(blobs):
+        raise sccl.SCCLError(sccl.CUDA_ERROR, "injected cudaIpcOpenMemHandle failure")
+    p.bind_peers = bad
+try:
+    p.bind_with()
+    print("BOUND", r, flush=True)
+except sccl.SCCLError as e:
+    print("FAILED", r, e.code, "rank 1: [sccl status 4] injected" in str(e), flush=True)
+dist.barrier()  # both ranks reach the next collective: nobody was left waiting
+print("NEXT", r, flush=True)
+dist.destroy_process_group()
+"""
+
+
+def test_bind_fails_on_every_rank_when_one_rank_fails(tmp_path):
+    """bind_with is collective and fails collectively (_collective_step):
+    one rank's failed local bind raises on both ranks of a world-size-2 gloo
+    job, with the failing rank's status and message, and both go on to the
+    next collective instead of one of them waiting on a peer that gave up."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = tmp_path / "fail.py"
+    script.write_text(_FAIL_WORKER.format(root=ROOT, port=port))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    procs = [subprocess.Popen(["python", str(script), str(r)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                              text=True, env=env) for r in range(2)]
+    outs = [p.communicate(timeout=120) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e
+    text = "".join(o for o, _ in outs)
+    assert "FAILED 0 4 True" in text and "FAILED 1 4 True" in text, text
+    assert text.count("NEXT") == 2 and "BOUND" not in text
+
+
 _FD_WORKER = r"""
 import os, sys
 sys.path.insert(0, {root!r})
