@@ -248,8 +248,8 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _workload_text(gpus: int, P: int, name: str) -> str:
-    if gpus == 1:
+def _workload_text(gpus: int, P: int, name: str, multi: bool = False) -> str:
+    if gpus == 1 and not multi:
         return f"{sched_label(name)}; {P} ranks loopback on 1 B200 (all rank buffers in one HBM)"
     return f"{sched_label(name)}; one rank per GPU on {P} B200s, CUDA IPC peers over NVLink/NVSwitch"
 
@@ -802,7 +802,7 @@ def run_multi(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
             "config": {"workload": (f"{sched_label(name)}; {P} ranks as {P} processes time-sliced on ONE GPU "
                                     "(multi-process path validation, not performance)") if shared
-                       else _workload_text(P, P, name),
+                       else _workload_text(P, P, name, multi=True),
                        "ranks": P, "bytes_per_rank": m, "schedule_file": f"tests/golden/schedules/bench/{name}.json",
                        "parallelism": f"ranks{P}", "nchannels": plan.info()["nchannels"],
                        "l2": "no flush: buffers >> L2", "shared_gpu": shared, "mem_handles": args.mem,
