@@ -1097,7 +1097,13 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
   if (tid == 0) trace_ev(p, &s_trace_n, TR_FLAG, 0, 0);  // epoch known
   const uint64_t e = s_e;
   const uint32_t ef = uint32_t(e);
-  if (p.multiprocess)
+  // epoch-parity slot sets (one rank per GPU, plan.cpp ll_parity_safe):
+  // launch e reads and writes scratch set e & 1 and skips the entry
+  // handshake -- no flag stores at entry, no waits before the first store
+  const uint64_t spar = (e & 1) * p.ll_parity;
+  auto sc = [&](int space) -> uint64_t { return space == SP_SCRATCH_IDX ? spar : 0; };
+  const bool handshake = p.multiprocess && !p.ll_parity;
+  if (handshake)
     for (int t = tid; t < p.P; t += LL_NT)
       if (t != rank) {
         fence_rel<SYS>();
@@ -1114,7 +1120,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
         const DevIn in = p.ins[op.in_begin + i];
         if (int(in.chunk % uint32_t(p.kc)) != cg) continue;
         const DPart q = dsplit16m(int64_t(in.len), p.kb, p.kb_magic, cb);
-        const char* slot = p.base[in.rank][in.space] + in.off + 2 * q.off;
+        const char* slot = p.base[in.rank][in.space] + sc(in.space) + in.off + 2 * q.off;
         const int64_t npair = (q.len + 7) / 8;
         for (int64_t k = tid; k < npair; k += LL_NT)
           ll_read<SYS>(slot, k, q.len - 8 * k > 4, ef, p, rank, ch, int(oi - ob));
@@ -1127,14 +1133,14 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
     if (tid < op.nin) {
       const DevIn in = p.ins[op.in_begin + tid];
       s_inll[tid] = in.flag >= 0;
-      s_inp[tid] = p.base[in.rank][in.space] + in.off + (in.flag >= 0 ? 2 * q.off : q.off);
+      s_inp[tid] = p.base[in.rank][in.space] + sc(in.space) + in.off + (in.flag >= 0 ? 2 * q.off : q.off);
     }
     if (tid >= 32 && tid < 32 + op.nout) {  // outputs on warp 1: loaded in parallel with the inputs
       const int o = tid - 32;
       const DevOut d = p.outs[op.out_begin + o];
       s_outll[o] = d.flag >= 0;
-      s_outp[o] = p.base[d.rank][d.space] + d.off + (d.flag >= 0 ? 2 * q.off : q.off);
-      if (p.multiprocess && d.rank != rank && !(atomicOr(&s_entry_mask, 0u) & (1u << d.rank))) {
+      s_outp[o] = p.base[d.rank][d.space] + sc(d.space) + d.off + (d.flag >= 0 ? 2 * q.off : q.off);
+      if (handshake && d.rank != rank && !(atomicOr(&s_entry_mask, 0u) & (1u << d.rank))) {
         wait_ge<SYS>(reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]) + p.entry_base + d.rank * p.nch + ch, e,
                      p, rank, ch, int(oi - ob), -2);
         atomicOr(&s_entry_mask, 1u << d.rank);

@@ -11,6 +11,7 @@ constexpr int kMaxRanks = 16;   // pointer table width (kernel parameter space)
 constexpr int kMaxOpIn = 32;    // inputs of one copy/reduce op (staged in smem)
 constexpr int kMaxOpOut = 32;   // destinations of one op
 constexpr int SP_FLAGS_IDX = 3; // FLAGS space index in KParams::base
+constexpr int SP_SCRATCH_IDX = 2;  // SCRATCH space index in KParams::base
 constexpr int kMaxTile = 65536; // one TMA pipeline stage (bytes)
 constexpr int kMaxStages = 8;   // pipeline depth limit (mbarrier sets)
 constexpr int kL2RelayPlain = 2;  // KParams::l2hint: re-read receipts stored with the default L2 policy
@@ -79,6 +80,8 @@ struct KParams {
   const uint32_t* nwin;  // [launched CTAs] windows of each CTA's program
   int l2hint;            // bit 0: L2 eviction hints on bulk copies (launch traffic >> L2); | kL2RelayPlain
   int discard;           // 1: drop consumed scratch receipts of reduce tiles from L2 (no write-back)
+  uint64_t ll_parity;    // LL, one rank per GPU: scratch holds two slot sets of this many bytes and
+                         // launch e uses set e & 1, with no entry handshake (0 = one set + handshake)
 };
 
 // debug trace events of the simple-protocol kernel (record = {globaltimer ns,

@@ -86,6 +86,7 @@ struct IpcBlob {
   char fingerprint[24];
   int32_t rank, nranks, nch, kc, kb, tile;
   int32_t dtype, redop;  // the program fingerprint covers the element size, not the format
+  int32_t ll_parity, pad;  // LL slot sets by launch parity (no entry handshake): every rank or none
   uint64_t region_bytes;
   cudaIpcMemHandle_t handle;
 };
@@ -165,6 +166,47 @@ bool choose_ll(sccl_plan& p, int64_t bytes, int es, int protocol, bool loopback,
   const bool ll = predict_us(a, steps, true, pol) < predict_us(b, steps, false, pol);
   p.pg = ll ? std::move(a) : std::move(b);
   return ll;
+}
+
+// Epoch-parity LL slots (one rank per GPU).  The entry handshake exists so
+// that a sender in launch e never overwrites a receiver's slot before the
+// receiver has read that slot's launch e-1 word.  With two slot sets, launch
+// e writing set e & 1, the hazard moves to set reuse two launches apart:
+// sender S in launch e needs receiver R past launch e-2.  S starting launch
+// e means S finished e-1, i.e. every receipt of its launch e-1 landed; if
+// one of those receipts had to wait for R's own launch e-1 to run (R's data
+// reached S through a chain of sends, each reading the value its sender
+// held at that step), then R had entered e-1 and so finished e-2 (launches
+// of a plan are stream-ordered on every rank).  The condition, checked for
+// every cross-rank send S -> R of the flattened schedule: R is in S's
+// completion set.  Holds for allgather, alltoall, reduce-scatter and
+// allreduce (every output depends on every rank); fails for rooted kinds
+// (a broadcast root depends on nobody), which keep the handshake.  Only LL:
+// its receipts are scratch slots the receiver unpacks itself, while the
+// simple protocol stores final values into the peer's receive buffer, whose
+// previous contents the peer's stream may still be reading.
+bool ll_parity_safe(const Schedule& s) {
+  const int P = s.P;
+  const auto phases = s.flat();
+  int G = 0;
+  for (auto* ph : phases) G = std::max(G, ph->G);
+  std::vector<uint32_t> dep(size_t(G) * P, 0);  // ranks the value of chunk c at node n waited for
+  std::vector<uint32_t> done(P, 0);             // ranks node n's launch completion waits for
+  for (auto* ph : phases)
+    for (int st = 0; st < ph->S; ++st) {
+      std::vector<uint32_t> nd = dep;  // sends at step st read the values at its start
+      for (const Send& t : ph->sends)
+        if (t.step == st) {
+          const uint32_t m = dep[size_t(t.chunk) * P + t.src] | (1u << t.src);
+          nd[size_t(t.chunk) * P + t.dst] |= m;
+          done[t.dst] |= m;
+        }
+      dep.swap(nd);
+    }
+  for (auto* ph : phases)
+    for (const Send& t : ph->sends)
+      if (!((done[t.src] >> t.dst) & 1u)) return false;
+  return true;
 }
 
 // Stage (= copy tile) size and pipeline depth.  Streaming copies and
@@ -562,7 +604,8 @@ void layout_memory(sccl_plan& p, bool loopback) {
   p.entry_base = p.pg.max_slots * p.nch;
   p.flags_bytes = up(sizeof(uint64_t) * size_t(p.entry_base + p.sched.P * p.nch), 4096);
   p.scratch_off = p.flags_bytes;
-  const size_t scratch = up(size_t(p.pg.scratch_bytes), 4096);
+  p.scratch_set = up(size_t(p.pg.scratch_bytes), 4096);
+  const size_t scratch = p.scratch_set * (p.ll_parity ? 2 : 1);
   p.recv_off = p.scratch_off + scratch;
   p.region_bytes = p.recv_off + (loopback ? 0 : up(size_t(p.pg.recv_bytes), 4096));
   p.region_bytes = up(p.region_bytes, 1 << 21);
@@ -591,6 +634,9 @@ void plan_build_host(sccl_plan& p, const std::string& json, int rank, int nranks
   if (req.pull > 0 && !loopback) throw invalid_argument_error("pull needs a loopback plan (peers' send buffers are not mapped)");
   const bool pull = loopback && req.pull >= 0;
   p.ll = choose_ll(p, bytes, es, req.protocol, loopback, pull);
+  // SCCL_LL_PARITY=0: keep the entry handshake (A/B)
+  const char* par_env = std::getenv("SCCL_LL_PARITY");
+  p.ll_parity = p.ll && !loopback && !(par_env && par_env[0] == '0') && ll_parity_safe(p.sched);
   p.rank = loopback ? 0 : rank;
   p.nranks = p.sched.P;
   p.loopback = loopback;
@@ -724,6 +770,7 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.nstage = p.nstage;
   k.ll = p.ll ? 1 : 0;
   k.entry_base = p.entry_base;
+  k.ll_parity = p.ll_parity ? uint64_t(p.scratch_set) : 0;
   k.trace = p.d_trace;
   k.trace_cap = p.trace_cap;
   k.selfpub = p.selfpub ? 1 : 0;
@@ -886,7 +933,7 @@ int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
       return;
     }
     IpcBlob b{};
-    std::memcpy(b.magic, "SCCLIPC2", 8);
+    std::memcpy(b.magic, "SCCLIPC3", 8);
     std::strncpy(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1);
     b.rank = p->rank;
     b.nranks = p->nranks;
@@ -896,6 +943,7 @@ int sccl_plan_export_handles(sccl_plan* p, void* blob, size_t* len) {
     b.tile = p->tile;
     b.dtype = p->dtype;
     b.redop = p->redop;
+    b.ll_parity = p->ll_parity ? 1 : 0;
     b.region_bytes = p->region_bytes;
     if (!p->host_only && !p->vmm && !p->external) {
       cuda_check(cudaSetDevice(p->device), "cudaSetDevice");
@@ -916,13 +964,15 @@ static std::vector<IpcBlob> check_blobs(sccl_plan* p, const void* const* blobs, 
     if (!blobs[r]) throw invalid_argument_error("missing blob for rank " + std::to_string(r));
     std::memcpy(&bs[r], blobs[r], sizeof(IpcBlob));
     const IpcBlob& b = bs[r];
-    if (std::memcmp(b.magic, "SCCLIPC2", 8)) throw invalid_argument_error("bad blob magic from rank " + std::to_string(r));
+    if (std::memcmp(b.magic, "SCCLIPC3", 8)) throw invalid_argument_error("bad blob magic from rank " + std::to_string(r));
     if (b.rank != r || b.nranks != p->nranks)
       throw invalid_argument_error("blob " + std::to_string(r) + " has rank/nranks mismatch");
     if (std::strncmp(b.fingerprint, p->pg.fingerprint.c_str(), sizeof b.fingerprint - 1))
       throw invalid_argument_error("rank " + std::to_string(r) + " lowered a different program (fingerprint mismatch)");
     if (b.nch != p->nch || b.kc != p->kc || b.kb != p->kb || b.tile != p->tile || b.region_bytes != p->region_bytes)
       throw invalid_argument_error("rank " + std::to_string(r) + " uses different channels/tile/region size");
+    if (b.ll_parity != (p->ll_parity ? 1 : 0))
+      throw invalid_argument_error("rank " + std::to_string(r) + " uses a different LL slot protocol (SCCL_LL_PARITY)");
     if (b.dtype != p->dtype || b.redop != p->redop)
       throw invalid_argument_error("rank " + std::to_string(r) + " uses a different dtype/redop (dtype " +
                                    std::to_string(b.dtype) + " vs " + std::to_string(p->dtype) + ")");
@@ -1234,7 +1284,7 @@ int sccl_plan_info(sccl_plan* p, char* out, size_t* len) {
     if (!p) throw invalid_argument_error("NULL plan");
     std::ostringstream o;
     o << "{\"nchannels\":" << p->nch << ",\"chunk_groups\":" << p->kc << ",\"byte_parts\":" << p->kb
-      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"groups_balanced\":" << (p->groups_balanced ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"pull\":" << (p->pg.pull ? 1 : 0) << ",\"policy\":\"" << p->policy << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
+      << ",\"storer_warps\":" << kStorerWarps << ",\"selfpub\":" << (p->selfpub ? 1 : 0) << ",\"window\":" << p->window << ",\"l2hint\":" << (p->l2hint & 1) << ",\"relay_evict_last\":" << ((p->l2hint & 1) && !(p->l2hint & kL2RelayPlain) ? 1 : 0) << ",\"discard\":" << (p->discard ? 1 : 0) << ",\"groups_balanced\":" << (p->groups_balanced ? 1 : 0) << ",\"nstage\":" << p->nstage << ",\"protocol\":\"" << (p->ll ? "ll" : "simple") << "\"" << ",\"ll_parity\":" << (p->ll_parity ? 1 : 0) << ",\"pull\":" << (p->pg.pull ? 1 : 0) << ",\"policy\":\"" << p->policy << "\"" << ",\"tile_bytes\":" << p->tile << ",\"threads\":" << exec_threads()
       << ",\"loopback\":" << (p->loopback ? 1 : 0) << ",\"rank\":" << p->rank << ",\"nranks\":" << p->nranks
       << ",\"grid\":" << (p->loopback ? p->nranks : 1) * p->nch << ",\"region_bytes\":" << p->region_bytes
       << ",\"nops\":" << p->ops.size() << ",\"program\":" << p->pg.summary_json() << "}";

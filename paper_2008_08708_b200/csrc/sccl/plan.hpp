@@ -20,6 +20,7 @@ struct sccl_plan {
   int nch = 1, kc = 1, kb = 1, tile = 32768, nstage = 6;
   int resident_cap = 0;  // loopback: CTAs that fit on the device at once
   bool ll = false;       // low-latency protocol
+  bool ll_parity = false;  // LL, one rank per GPU: two scratch slot sets by launch parity, no entry handshake
   bool selfpub = false;  // simple protocol: storer warps release their own counters (latency-bound plans)
   long long timeout_ns = 0;
   std::string policy;    // version of the policy table the plan was built under
@@ -50,6 +51,7 @@ struct sccl_plan {
   // plan memory: per rank region = [flags | scratch | recv (multi-process)]
   char* d_region = nullptr;
   size_t region_bytes = 0, flags_bytes = 0, scratch_off = 0, recv_off = 0;
+  size_t scratch_set = 0;  // bytes of one scratch slot set (ll_parity: the scratch holds two)
   int entry_base = 0;
   std::vector<char*> peer_region;  // multi-process: every rank's region (own included)
   // VMM mode (opts.mem_handles = 1): cuMem allocation handles (CUmemGenericAllocationHandle)
