@@ -709,6 +709,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         if (op.raw && lane == 0)  // input written by an earlier tile of this CTA
           while (ld_acquire_cta(&S.published) < it) __nanosleep(32);
         __syncwarp();
+        if (lane == 0) trace_ev(p, &S.trace_n, TR_ENTRY, oi, 0);  // producer: op descriptors read
         for (uint32_t t = 0; t < ntiles; ++t, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
           const uint64_t lo = wlo + uint64_t(t) * T;
@@ -720,9 +721,15 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
               ready = wait_ge<SYS>(myflags + uint64_t(flag) * p.nch + ch, need, p, rank, ch, int(oi - ob), flag);
           }
           __syncwarp();
-          if (lane == 0) trace_ev(p, &S.trace_n, TR_FLAG, oi, t);
+          if (p.trace) {  // (tile bit 31: some input of this tile has a receipt counter)
+            const bool waited = __any_sync(0xffffffffu, flag >= 0);
+            if (lane == 0) trace_ev(p, &S.trace_n, TR_FLAG, oi, t | (waited ? 0x80000000u : 0u));
+          }
           uint64_t* const fb = op.kind == 1 ? &S.fullr[s] : &S.full[s];
-          if (lane == 0) mbar_wait_wd(&S.empty[s], ph ^ 1, p, rank, ch, int(oi - ob));
+          if (lane == 0) {
+            mbar_wait_wd(&S.empty[s], ph ^ 1, p, rank, ch, int(oi - ob));
+            trace_ev(p, &S.trace_n, TR_EMPTY, oi, t);
+          }
           __syncwarp();
           if (p.discard && op.kind == 1) {  // dead scratch receipts of this reduce tile
             S.dsc[s][lane] = (dead_after && nv) ? src + lo : nullptr;
@@ -734,6 +741,10 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
             if (p.l2hint) bulk_load_hint(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, fb, pol_first);
             else bulk_load(bufs + size_t(s) * STAGE + size_t(lane) * T, src + lo, nv, fb);
+          }
+          if (p.trace) {
+            __syncwarp();
+            if (lane == 0) trace_ev(p, &S.trace_n, TR_ISSUED, oi, t);
           }
         }
       } else if (warp >= CW0) {

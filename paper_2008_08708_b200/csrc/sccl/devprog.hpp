@@ -86,6 +86,7 @@ struct KParams {
 
 // debug trace events of the simple-protocol kernel (record = {globaltimer ns,
 // event | op << 8 | tile << 32}); see tools/probes/trace_hops.py
-enum TraceEvent : int { TR_START = 0, TR_FLAG = 1, TR_FULL = 2, TR_READY = 3, TR_DONE = 4, TR_PUB = 5, TR_END = 6 };
+enum TraceEvent : int { TR_START = 0, TR_FLAG = 1, TR_FULL = 2, TR_READY = 3, TR_DONE = 4, TR_PUB = 5, TR_END = 6,
+                        TR_EMPTY = 7, TR_ISSUED = 8, TR_ENTRY = 9 };
 
 }  // namespace sccl
