@@ -66,9 +66,10 @@ dist.destroy_process_group()
 """
 
 
-@pytest.mark.parametrize("parity", ["on", "off"])
-@pytest.mark.parametrize("mem", ["ipc", "vmm"])
-@pytest.mark.parametrize("world", [2, 4])
+CASES = [(w, m, par) for w in (2, 4) for m in ("ipc", "vmm") for par in ("on", "off")] + [(8, "ipc", "on")]
+
+
+@pytest.mark.parametrize("world,mem,parity", CASES, ids=[f"w{w}-{m}-{par}" for w, m, par in CASES])
 def test_ll_back_to_back_without_barriers(tmp_path, world, mem, parity):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
