@@ -918,7 +918,12 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
     g_ring = group_with({"NCCL_ALGO": "Ring"})
     g_tree = group_with({"NCCL_ALGO": "Tree"})
     bw = lambda coll, nbytes, t: round(busbytes(coll, P, nbytes) / (t * 1e-3) / 1e9, 2)
-    agree = lambda ok: (lambda v: (dist.all_gather_object(v, bool(ok)), v)[1])([None] * P)
+
+    def agree(ok):
+        """every rank's check result (collective)"""
+        res = [None] * P
+        dist.all_gather_object(res, bool(ok))
+        return res
 
     def allgather():  # at the workload size
         ag = {"ours_ms": round(ms_ours, 4), "ours_busbw": bw("allgather", m, ms_ours)}
