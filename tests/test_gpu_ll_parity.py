@@ -62,6 +62,32 @@ for name, js, nb, dt, want_parity in cases:
     dist.barrier()
     plan.close()
     print("OK", rank, name, info["ll_parity"], flush=True)
+# registered (zero-copy) receive buffers: receipts still land in the parity
+# slot sets and the receiver unpacks into each launch's own registered target
+js = S.allreduce_from(S.ring_allgather(W))
+d = json.loads(js)
+nb, K = 8192, 8
+plan = sccl.Plan(js, rank, W, nb, O.F32, device=0, protocol="ll", timeout_ms=120000, mem_handles=MEM)
+plan.bind_with()
+targets = [torch.full((nb,), 0xEE, dtype=torch.uint8, device="cuda") for _ in range(K)]
+for t in targets:
+    plan.register(t)
+ins = [O.seeded_inputs("allreduce", W, nb, O.F32, 300 + i) for i in range(K)]
+refs = [O.execute(d, x, nb, O.F32)[rank] for x in ins]
+sends = [torch.from_numpy(x[rank]).cuda() for x in ins]
+torch.cuda.synchronize()
+dist.barrier()
+for i in range(K):
+    if rank == 0 and rng.random() < 0.5:
+        time.sleep(rng.random() * 0.002)
+    plan.launch(sends[i], targets[i])
+torch.cuda.synchronize()
+plan.check()
+bad = [i for i in range(K) if not np.array_equal(targets[i].cpu().numpy(), refs[i])]
+assert not bad, ("registered", bad)
+dist.barrier()
+plan.close()
+print("OK", rank, "registered", flush=True)
 dist.destroy_process_group()
 """
 
@@ -92,4 +118,4 @@ def test_ll_back_to_back_without_barriers(tmp_path, world, mem, parity):
                 p.kill()
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
-    assert "".join(o for o, _ in outs).count("OK") == 6 * world
+    assert "".join(o for o, _ in outs).count("OK") == 7 * world
