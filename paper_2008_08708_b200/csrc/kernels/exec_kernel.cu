@@ -70,8 +70,10 @@ __device__ __forceinline__ DPart dsplit16m(int64_t L, int K, uint64_t magic, int
   const int64_t hi = (i == K - 1) ? L : int64_t(__umul64hi(uint64_t(i + 1) * Uu, magic) << 4);
   return {lo, hi - lo};
 }
-// tiles of T bytes covering n bytes
+// tiles of T bytes covering n bytes: a shift for power-of-two tiles (copies,
+// and reductions of fan-in 2, 4, 8, ...), a divide otherwise
 __device__ __forceinline__ uint32_t ntiles_of(uint64_t n, uint32_t T) {
+  if ((T & (T - 1)) == 0) return uint32_t((n + T - 1) >> (__ffs(T) - 1));
   return n >> 31 ? uint32_t((n + T - 1) / T) : (uint32_t(n) + T - 1) / T;
 }
 
@@ -597,6 +599,16 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       }
 
   uint32_t it = 0;  // tile number (same sequence in every role)
+  // it % NST and (it / NST) & 1, kept incrementally (NST is a runtime
+  // value: a modulo per tile was a divide on every role's tile path)
+  uint32_t st = 0, sph = 0;
+  auto next_tile = [&]() {
+    ++it;
+    if (++st == NST) {
+      st = 0;
+      sph ^= 1u;
+    }
+  };
   const uint32_t my_stage_class = uint32_t(warp - 1);  // storer warps
   // bit s = parity of stage s's next phase of a barrier that only some uses
   // touch: storers track `full` (copy uses) and `ready` (reduce uses),
@@ -691,7 +703,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
       }
 
       // ---- pipelined op: tiles of this window ----
-      const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
+      const uint32_t T = op.tile;  // (host-computed: stage, or stage / fan-in for reductions)
       const uint32_t ntiles = ntiles_of(whi - wlo, T);
 
       if (warp == 0) {
@@ -710,8 +722,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           while (ld_acquire_cta(&S.published) < it) __nanosleep(32);
         __syncwarp();
         if (lane == 0) trace_ev(p, &S.trace_n, TR_ENTRY, oi, 0);  // producer: op descriptors read
-        for (uint32_t t = 0; t < ntiles; ++t, ++it) {
-          const uint32_t s = it % NST, ph = (it / NST) & 1;
+        for (uint32_t t = 0; t < ntiles; ++t, next_tile()) {
+          const uint32_t s = st, ph = sph;
           const uint64_t lo = wlo + uint64_t(t) * T;
           const uint32_t n = uint32_t(min(uint64_t(T), whi - lo));
           const uint32_t nv = n & ~15u;
@@ -749,8 +761,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
         }
       } else if (warp >= CW0) {
         // ================= compute (REDUCE tiles; copy tiles go straight to the storer) =================
-        for (uint32_t t = 0; t < ntiles; ++t, ++it) {
-          const uint32_t s = it % NST;
+        for (uint32_t t = 0; t < ntiles; ++t, next_tile()) {
+          const uint32_t s = st;
           if (op.kind == 1) {
             mbar_wait_wd(&S.fullr[s], (rpar >> s) & 1u, p, rank, ch, int(oi - ob));
             rpar ^= 1u << s;
@@ -794,8 +806,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           if (p.multiprocess && d.rank != rank) await_entry(d.rank, int(oi - ob));
         }
         __syncwarp();
-        for (uint32_t t = 0; t < ntiles; ++t, ++it) {
-          const uint32_t s = it % NST;
+        for (uint32_t t = 0; t < ntiles; ++t, next_tile()) {
+          const uint32_t s = st;
           if (s % NSW != my_stage_class) continue;
           const uint64_t lo = wlo + uint64_t(t) * T;
           const uint32_t n = uint32_t(min(uint64_t(T), whi - lo));
@@ -888,7 +900,7 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
           every = d.every_tile;
         }
         const uint32_t em = __ballot_sync(0xffffffffu, every);
-        const uint32_t T = op.kind == 0 ? uint32_t(p.tile) : max(16u, uint32_t(p.tile / op.nin) & ~15u);
+        const uint32_t T = op.tile;
         const uint32_t nt = ntiles_of(whi - wlo, T);
         if (lane == 0) {
           x.fbase = (e - 1) * uint64_t(q.len);

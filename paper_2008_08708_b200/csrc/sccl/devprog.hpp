@@ -42,7 +42,8 @@ struct DevOut {
 struct DevOp {
   uint64_t len;   // chunk length in bytes
   uint32_t chunk; // chunk group of the op's chunk: CTA channel (g, b) runs ops with chunk % kc == g
-  uint32_t pad2;
+  uint32_t tile;  // simple protocol: bytes per tile of this op (the stage for copies, stage / nin
+                  // rounded down to 16 for reductions; precomputed: no divide on the device)
   uint32_t in_begin, out_begin;
   uint16_t nin, nout;
   uint8_t kind;   // 0 copy, 1 reduce, 2 wait

@@ -461,6 +461,9 @@ void encode_program(sccl_plan& p) {
     d.out_begin = uint32_t(p.outs.size());
     d.nin = uint16_t(ins.size());
     d.nout = uint16_t(op.outs.size());
+    // the kernel's tile of this op (exec_kernel.cu: copies move a whole
+    // stage, reductions stage / fan-in rounded down to 16 bytes)
+    d.tile = op.kind == OP_COPY ? uint32_t(p.tile) : std::max(16u, uint32_t(p.tile / std::max<size_t>(1, ins.size())) & ~15u);
     bool vec = true;
     for (auto& in : ins) {
       // remote reads only of untouched SEND buffers, and only in pull mode
