@@ -266,12 +266,14 @@ __device__ __forceinline__ bool join_abort(const KParams& p) {
 // never completes (a bug, not a peer) aborts instead of hanging the GPU.
 __device__ __noinline__ void mbar_wait_slow(uint64_t* b, uint32_t parity, const KParams& p, int rank, int ch,
                                             int op) {
-  const uint64_t t0 = globaltimer();
+  uint64_t t0 = 0;  // clock first read after 1024 tries (not on every missed hand-off)
   for (uint32_t spins = 1;; ++spins) {
     if (mbar_try(b, parity)) return;
     if ((spins & 1023) == 0) {
       if (join_abort(p)) return;
-      if (p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+      const uint64_t now = globaltimer();
+      if (!t0) t0 = now;
+      else if (p.timeout_ns > 0 && (long long)(now - t0) > p.timeout_ns) {
         watchdog_fire(p, rank, ch, op, -4, parity, 0);
         return;
       }
@@ -289,16 +291,21 @@ __device__ uint64_t wait_ge(const uint64_t* f, uint64_t target, const KParams& p
                             int slot) {
   uint64_t v = ld_acquire<SYS>(f);
   if (v >= target) return v;
-  if (join_abort(p)) return target;
+  if (cta_aborted()) return target;
   // poll with relaxed (strong) loads -- no L1 invalidation per poll -- and
-  // acquire once the target is reached
-  uint64_t t0 = globaltimer();
+  // acquire once the target is reached.  The launch-wide abort word (a
+  // global load) and the clock are first read after 1024 polls: on the
+  // first miss they only delayed noticing the value (a dependent global
+  // round trip per missed wait); the watchdog then counts from there.
+  uint64_t t0 = 0;
   uint32_t spins = 0;
   while ((v = ld_relaxed<SYS>(f)) < target) {
     if (++spins > 64) __nanosleep(32);
     if ((spins & 1023) == 0) {
       if (join_abort(p)) return target;
-      if (p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+      const uint64_t now = globaltimer();
+      if (!t0) t0 = now;
+      else if (p.timeout_ns > 0 && (long long)(now - t0) > p.timeout_ns) {
         watchdog_fire(p, rank, ch, op, slot, target, v);
         return target;
       }
@@ -1048,8 +1055,8 @@ __device__ uint2 ll_read(const char* slot, int64_t pair, bool two, uint32_t ef, 
   const char* a = slot + pair * 16;
   uint4 v = ld_ll(a);
   if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
-  if (join_abort(p)) return make_uint2(0, 0);
-  const uint64_t t0 = globaltimer();
+  if (cta_aborted()) return make_uint2(0, 0);
+  uint64_t t0 = 0;  // (abort word and clock first read after 1024 polls, as in wait_ge)
   uint32_t spins = 0;
   for (;;) {
     v = ld_ll(a);
@@ -1057,7 +1064,9 @@ __device__ uint2 ll_read(const char* slot, int64_t pair, bool two, uint32_t ef, 
     if (++spins > 32) __nanosleep(20);
     if ((spins & 1023) == 0) {
       if (join_abort(p)) return make_uint2(0, 0);
-      if (p.timeout_ns > 0 && (long long)(globaltimer() - t0) > p.timeout_ns) {
+      const uint64_t now = globaltimer();
+      if (!t0) t0 = now;
+      else if (p.timeout_ns > 0 && (long long)(now - t0) > p.timeout_ns) {
         watchdog_fire(p, rank, ch, op, -3, ef, v.y);
         return make_uint2(0, 0);
       }

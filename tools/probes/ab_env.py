@@ -49,9 +49,27 @@ def main():
             for v in (va, vb):
                 plans[v].launch(send, outs[v])
         torch.cuda.synchronize()
+        graphs = {}
+        if os.environ.get("AB_GRAPH") == "1":  # small sizes: time CUDA-graph replays (no host launch cost)
+            st = torch.cuda.Stream()
+            for v in (va, vb):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for _ in range(iters * 10):
+                        plans[v].launch(send, outs[v], st)
+                graphs[v] = g
         for _ in range(reps):
             for v in (va, vb):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                if graphs:
+                    graphs[v].replay()
+                    torch.cuda.synchronize()
+                    a.record()
+                    graphs[v].replay()
+                    b.record()
+                    torch.cuda.synchronize()
+                    t[v].append(a.elapsed_time(b) * 1e3 / (iters * 10))
+                    continue
                 a.record()
                 for _ in range(iters):
                     plans[v].launch(send, outs[v])
