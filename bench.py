@@ -734,14 +734,45 @@ def run_multi(args):
     name = workload_schedule(P, args.schedule)
     js = load_schedule(name)
     m = args.bytes
-    plan = sccl.Plan(js, rank, P, m, sccl.U8, device=dev_index, nchannels=args.nchannels, tile_bytes=args.tile,
-                     mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
-    plan.bind_with()
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
     send = torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev, generator=g)
     recv = torch.empty(P * m, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    # CTAs per rank: the multi-process policy table's default (32) was fitted
+    # on a loopback proxy, so on a real NVLink box the
+    # bench first times the default against 16 and 64 (max over ranks, a few
+    # launches each) and runs the workload with the fastest; the line reports
+    # every candidate.  --nchannels N pins it.
+    tune = {}
+    nch_use = args.nchannels
+    if args.nchannels == 0:
+        for cand in (0, 16, 64):
+            tp = sccl.Plan(js, rank, P, m, sccl.U8, device=dev_index, nchannels=cand, tile_bytes=args.tile,
+                           mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
+            try:
+                tp.bind_with()
+                treg, _ = tp.recv_buffer()
+                for _ in range(2):
+                    tp.launch(send, treg, stream)
+                dist.barrier()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(5):
+                    tp.launch(send, treg, stream)
+                b.record()
+                torch.cuda.synchronize()
+                tp.check()
+                t = torch.tensor([a.elapsed_time(b) / 5], device="cpu" if shared else dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                tune[tp.info()["nchannels"] if cand == 0 else cand] = (cand, round(float(t), 4))
+            finally:
+                tp.close()
+        nch_use = min(tune.values(), key=lambda x: x[1])[0]
+    plan = sccl.Plan(js, rank, P, m, sccl.U8, device=dev_index, nchannels=nch_use, tile_bytes=args.tile,
+                     mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
+    plan.bind_with()
     for _ in range(args.warmup):
         plan.launch(send, recv, stream)
     torch.cuda.synchronize()
@@ -805,6 +836,7 @@ def run_multi(args):
                        else _workload_text(P, P, name, multi=True),
                        "ranks": P, "bytes_per_rank": m, "schedule_file": f"tests/golden/schedules/bench/{name}.json",
                        "parallelism": f"ranks{P}", "nchannels": plan.info()["nchannels"],
+                       "nchannels_autotune_ms": {str(k): v[1] for k, v in tune.items()} or None,
                        "l2": "no flush: buffers >> L2", "shared_gpu": shared, "mem_handles": args.mem,
                        "value_convention": "sum over GPUs of per-rank bus GB/s (nccl-tests busBW)"},
             "busbw_per_rank_GBps": round(per_rank, 2),
