@@ -178,7 +178,11 @@ def main_multi(grid):
         for proto in ("ll", "simple"):
             pts = [r for r in rows if r["protocol"] == proto]
             A = np.array([[1.0 / r["us"], r["steps"] / r["us"], r["mb"] / r["us"]] for r in pts])
-            sol, *_ = np.linalg.lstsq(A, np.ones(len(pts)), rcond=None)
+            try:  # the constants are times: non-negative least squares
+                from scipy.optimize import nnls
+                sol, _ = nnls(A, np.ones(len(pts)))
+            except ImportError:
+                sol, *_ = np.linalg.lstsq(A, np.ones(len(pts)), rcond=None)
             co[proto] = [round(float(x), 4) for x in sol]
         wins = {}
         for key in {(r["sched"], r["bytes"]) for r in rows}:
