@@ -95,6 +95,30 @@ for name, js, dts in scheds:
                     dist.barrier()
                 plan.close()
                 n_ok += 1
+# bursts: 12 launches back to back, no barrier or synchronize between them,
+# each with its own input and output (LL: the epoch-parity slot sets; simple:
+# the entry handshake into the peers' receive buffers), then every output
+# against the oracle
+for name, js, dts in scheds:
+    d = json.loads(js)
+    for proto, nb in (("ll", 4096), ("simple", 1 << 18)):
+        plan = sccl.Plan(js, rank, W, nb, dts[0], device=dev, protocol=proto, timeout_ms=120000, mem_handles=MEM)
+        plan.bind_with()
+        ins = [O.seeded_inputs(d["collective"], W, nb, dts[0], 500 + i) for i in range(12)]
+        wants = [O.execute(d, x, nb, dts[0])[rank] for x in ins]
+        sends = [torch.from_numpy(x[rank]).cuda() for x in ins]
+        recvs = [torch.full((plan.recv_bytes,), 0xEE, dtype=torch.uint8, device="cuda") for _ in ins]
+        torch.cuda.synchronize()
+        dist.barrier()
+        for sb, rb in zip(sends, recvs):
+            plan.launch(sb, rb)
+        torch.cuda.synchronize()
+        plan.check()
+        bad = [i for i, (rb, w) in enumerate(zip(recvs, wants)) if not np.array_equal(rb.cpu().numpy(), w)]
+        assert not bad, ("burst", name, proto, rank, bad)
+        dist.barrier()
+        plan.close()
+        n_ok += 1
 # torch symmetric memory as the plan region (one rank per GPU)
 if MEM == "ipc" and not SHARE:
     for name, js, dts in scheds[:3]:
