@@ -6,6 +6,7 @@ order"); no tolerance is needed or used.  Loopback mode runs every rank of
 the schedule on cuda:0 (one launch, P x nchannels CTAs).
 """
 import json
+import os
 
 import numpy as np
 import pytest
@@ -603,3 +604,21 @@ def test_auto_plan_from_machine_gpu():
             assert all(np.array_equal(a.cpu().numpy(), b) for a, b in zip(recv, ref)), (coll, nb)
         assert len(chosen) >= 2, chosen  # the choice changes with size
         ap.close()
+
+
+FRONTIER_DIR = os.path.join(os.path.dirname(S.__file__), "frontiers")
+FRONTIERS = sorted(f[:-5] for f in os.listdir(FRONTIER_DIR) if f.endswith(".json") and f != "index.json")
+
+
+@pytest.mark.parametrize("name", FRONTIERS)
+@pytest.mark.parametrize("protocol", ["ll", "simple"])
+def test_every_committed_frontier_schedule(name, protocol):
+    """Every Pareto-frontier schedule shipped in frontiers/ (ring(P), full(P)
+    and the NVSwitch target switch(P), P = 2/4/8; SURVEY.md 8(d) cfg 5):
+    the allgather itself and the allreduce composed from it (RS = its
+    inversion, bf16), bit-exact against the oracle under both protocols,
+    sentinel-checked."""
+    with open(os.path.join(FRONTIER_DIR, name + ".json")) as f:
+        js = f.read()
+    run_gpu(js, 24576 + 48, O.U8, seed=61, protocol=protocol)
+    run_gpu(S.allreduce_from(json.loads(js)), 8 * 4096, O.BF16, seed=62, protocol=protocol)
