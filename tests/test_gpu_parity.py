@@ -622,3 +622,20 @@ def test_every_committed_frontier_schedule(name, protocol):
         js = f.read()
     run_gpu(js, 24576 + 48, O.U8, seed=61, protocol=protocol)
     run_gpu(S.allreduce_from(json.loads(js)), 8 * 4096, O.BF16, seed=62, protocol=protocol)
+
+
+BENCH_FILES = sorted(__import__("glob").glob(os.path.join(os.path.dirname(__file__), "golden", "schedules", "bench",
+                                                          "*.json")))
+
+
+@pytest.mark.parametrize("path", BENCH_FILES, ids=[p.split("/")[-1][:-5] for p in BENCH_FILES])
+def test_bench_schedule_files_gpu(path):
+    """Every schedule file bench.py runs (N = 1 loopback and the N = 2/4/8
+    workloads, NCCL comparisons and sweeps, P = 1 self-test files included),
+    executed in loopback at a small size, bit-exact against the oracle."""
+    js = open(path).read().strip()
+    d = json.loads(js)
+    dt = O.BF16 if d["collective"] == "allreduce" else O.U8
+    nb = 4096 * max(1, d["P"])
+    for protocol in ("ll", "simple"):
+        run_gpu(js, nb, dt, seed=71, protocol=protocol)
