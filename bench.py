@@ -712,6 +712,38 @@ def nvlink_counters(index: int):
     return None
 
 
+def tune_nchannels(dist, sccl, js, rank, P, nbytes, dtype, dev_index, args, send, stream, tdev):
+    """CTAs per rank of a one-rank-per-GPU plan: the multi-process policy
+    table's default (fitted on a loopback proxy) against
+    16 and 64, 5 launches each into the plan's registered buffer, max over
+    ranks.  Returns (nchannels to use, {nchannels: (request, ms)})."""
+    import torch
+    tune = {}
+    for cand in (0, 16, 64):
+        tp = sccl.Plan(js, rank, P, nbytes, dtype, device=dev_index, nchannels=cand, tile_bytes=args.tile,
+                       mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
+        try:
+            tp.bind_with()
+            treg, _ = tp.recv_buffer()
+            for _ in range(2):
+                tp.launch(send, treg, stream)
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(5):
+                tp.launch(send, treg, stream)
+            b.record()
+            torch.cuda.synchronize()
+            tp.check()
+            t = torch.tensor([a.elapsed_time(b) / 5], device=tdev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tune[tp.info()["nchannels"] if cand == 0 else cand] = (cand, round(float(t), 4))
+        finally:
+            tp.close()
+    return min(tune.values(), key=lambda x: x[1])[0], tune
+
+
 def run_multi(args):
     import torch
     import torch.distributed as dist
@@ -747,29 +779,8 @@ def run_multi(args):
     tune = {}
     nch_use = args.nchannels
     if args.nchannels == 0:
-        for cand in (0, 16, 64):
-            tp = sccl.Plan(js, rank, P, m, sccl.U8, device=dev_index, nchannels=cand, tile_bytes=args.tile,
-                           mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
-            try:
-                tp.bind_with()
-                treg, _ = tp.recv_buffer()
-                for _ in range(2):
-                    tp.launch(send, treg, stream)
-                dist.barrier()
-                torch.cuda.synchronize()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                for _ in range(5):
-                    tp.launch(send, treg, stream)
-                b.record()
-                torch.cuda.synchronize()
-                tp.check()
-                t = torch.tensor([a.elapsed_time(b) / 5], device="cpu" if shared else dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                tune[tp.info()["nchannels"] if cand == 0 else cand] = (cand, round(float(t), 4))
-            finally:
-                tp.close()
-        nch_use = min(tune.values(), key=lambda x: x[1])[0]
+        nch_use, tune = tune_nchannels(dist, sccl, js, rank, P, m, sccl.U8, dev_index, args, send, stream,
+                                       "cpu" if shared else dev)
     plan = sccl.Plan(js, rank, P, m, sccl.U8, device=dev_index, nchannels=nch_use, tile_bytes=args.tile,
                      mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
     plan.bind_with()
@@ -976,8 +987,11 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
     def allreduce():
         ar = {"bytes_per_rank": M}
         for nm in ([f"ar_oneshot_full{P}"] + ([f"ar_ham_full{P}"] if P in (2, 8) else [])):
+            nch, tn = tune_nchannels(dist, sccl, load_schedule(nm), rank, P, M, sccl.BF16, dev_index, args,
+                                     x.view(torch.uint8), torch.cuda.current_stream(), dev)
+            ar[f"ours_{nm}_nchannels_autotune_ms"] = {str(k): v[1] for k, v in tn.items()}
             p2 = sccl.Plan(load_schedule(nm), rank, P, M, sccl.BF16, device=dev_index, mem_handles=args.mem,
-                           timeout_ms=BENCH_TIMEOUT_MS)
+                           timeout_ms=BENCH_TIMEOUT_MS, nchannels=nch)
             try:
                 p2.bind_with()
                 reg, _ = p2.recv_buffer()
@@ -1024,8 +1038,10 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
     def alltoall():  # at 64 MiB: direct (P,1,1) vs NCCL grouped send/recv
         a_in = torch.randint(0, 256, (M,), dtype=torch.uint8, device=dev)
         a_out = torch.empty_like(a_in)
+        nch, tune_a2a = tune_nchannels(dist, sccl, load_schedule(f"a2a_direct_full{P}"), rank, P, M, sccl.U8,
+                                       dev_index, args, a_in, torch.cuda.current_stream(), dev)
         p3 = sccl.Plan(load_schedule(f"a2a_direct_full{P}"), rank, P, M, sccl.U8, device=dev_index,
-                       mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS)
+                       mem_handles=args.mem, timeout_ms=BENCH_TIMEOUT_MS, nchannels=nch)
         try:
             p3.bind_with()
             reg3, _ = p3.recv_buffer()
@@ -1037,7 +1053,8 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
             p3.check()
             same = agree(torch.equal(chk, a_out))
             tn = timed(lambda: dist.all_to_all_single(chk, a_in), args.steps)
-            return {"bytes_per_rank": M, "ours_ms": round(t, 4), "ours_busbw": bw("alltoall", M, t),
+            return {"bytes_per_rank": M, "ours_nchannels_autotune_ms": {str(k): v[1] for k, v in tune_a2a.items()},
+                    "ours_ms": round(t, 4), "ours_busbw": bw("alltoall", M, t),
                     "nccl_ms": round(tn, 4), "nccl_busbw": bw("alltoall", M, tn), "equals_nccl": same}
         finally:
             p3.close()
