@@ -149,7 +149,15 @@ int sccl_plan_register_export(sccl_plan* plan, void* buf, size_t bytes, void* bl
 int sccl_plan_register_bind(sccl_plan* plan, void* buf, const void* const* peer_blobs, size_t blob_len);
 int sccl_plan_deregister(sccl_plan* plan, void* buf);
 
-/* Asynchronous, stream-ordered launch (multi-process). */
+/* Asynchronous, stream-ordered launch (multi-process).  Launches of one plan
+ * must be ordered on every rank (one stream, or events between streams):
+ * launch e-1 finishes on a rank before its launch e starts.  The simple
+ * protocol stores into peers' receive buffers only after the peer's CTA has
+ * entered the same launch (entry handshake); LL plans whose schedule proves
+ * it (sccl_plan_info "ll_parity": allgather, alltoall, reduce-scatter,
+ * allreduce) instead alternate two scratch slot sets by launch parity and
+ * skip the handshake (SCCL_LL_PARITY=0 keeps it; every rank must agree --
+ * bind refuses a mix). */
 int sccl_launch(sccl_plan* plan, const void* sendbuf, void* recvbuf, void* stream);
 
 /* Loopback launch: sendbufs[r]/recvbufs[r] for r < P, all on the plan's device. */
