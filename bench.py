@@ -1121,6 +1121,10 @@ def main():
             os.environ.get("SCCL_BENCH_FORCE_MULTI") != "1":
         run_loopback(args)
     else:
+        if "RANK" not in os.environ:
+            sys.exit(f"bench.py --gpus {args.gpus}: launch one process per GPU with torchrun, e.g. python -m "
+                     f"torch.distributed.run --nnodes=1 --nproc-per-node {args.gpus} --master-addr 127.0.0.1 "
+                     f"bench.py --gpus {args.gpus}")
         run_multi(args)
 
 
