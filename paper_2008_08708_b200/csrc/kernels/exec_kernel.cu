@@ -1101,6 +1101,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
   const int cg = ch % p.kc, cb = ch / p.kc;
   const int rank = p.rank0 + lr;
   __shared__ uint64_t s_e;
+  __shared__ uint64_t s_spar;  // scratch slot-set offset of this launch (epoch parity)
   __shared__ uint32_t s_entry_mask;
   __shared__ const char* s_inp[kMaxOpIn];
   __shared__ char* s_outp[kMaxOpOut];
@@ -1116,6 +1117,7 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
     s_trace_n = 0;
     trace_ev(p, &s_trace_n, TR_START, 0, 0);
     s_e = p.epochs[blockIdx.x] + 1;
+    s_spar = (s_e & 1) * p.ll_parity;
     s_entry_mask = 1u << rank;
     cta_abort = 0;
   }
@@ -1132,8 +1134,11 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
   // epoch-parity slot sets (one rank per GPU, plan.cpp ll_parity_safe):
   // launch e reads and writes scratch set e & 1 and skips the entry
   // handshake -- no flag stores at entry, no waits before the first store
-  const uint64_t spar = (e & 1) * p.ll_parity;
-  auto sc = [&](int space) -> uint64_t { return space == SP_SCRATCH_IDX ? spar : 0; };
+  // (kept in shared memory, read where an address is formed: as a register
+  // live across the op loop it cost the kernel 8-22 registers)
+  auto sc = [&](int space) -> uint64_t {
+    return space == SP_SCRATCH_IDX ? *reinterpret_cast<volatile uint64_t*>(&s_spar) : 0;
+  };
   const bool handshake = p.multiprocess && !p.ll_parity;
   if (handshake)
     for (int t = tid; t < p.P; t += LL_NT)
