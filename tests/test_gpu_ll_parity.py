@@ -88,6 +88,37 @@ assert not bad, ("registered", bad)
 dist.barrier()
 plan.close()
 print("OK", rank, "registered", flush=True)
+# CUDA-graph replays: the slot-set parity comes from the device-side launch
+# epoch, so a captured launch replayed many times keeps alternating sets;
+# 5 captured launches (odd, so consecutive replays start on different sets),
+# replayed 3 times back to back, ranks drifting; the last output is checked
+js = S.to_json(S.ring_allgather(W))
+d = json.loads(js)
+nb = 4096
+plan = sccl.Plan(js, rank, W, nb, O.U8, device=0, protocol="ll", timeout_ms=120000, mem_handles=MEM)
+plan.bind_with()
+x = O.seeded_inputs("allgather", W, nb, O.U8, 900)
+want = O.execute(d, x, nb, O.U8)[rank]
+send = torch.from_numpy(x[rank]).cuda()
+recv = torch.full((want.size,), 0xEE, dtype=torch.uint8, device="cuda")
+st = torch.cuda.Stream()
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=st):
+    for _ in range(5):
+        plan.launch(send, recv, st)
+dist.barrier()
+with torch.cuda.stream(st):
+    for _ in range(3):
+        if rank == 0:
+            time.sleep(rng.random() * 0.002)
+        g.replay()
+torch.cuda.synchronize()
+plan.check()
+assert np.array_equal(recv.cpu().numpy(), want), ("graph", rank)
+dist.barrier()
+plan.close()
+print("OK", rank, "graph", flush=True)
 dist.destroy_process_group()
 """
 
@@ -118,4 +149,4 @@ def test_ll_back_to_back_without_barriers(tmp_path, world, mem, parity):
                 p.kill()
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
-    assert "".join(o for o, _ in outs).count("OK") == 7 * world
+    assert "".join(o for o, _ in outs).count("OK") == 8 * world
