@@ -755,6 +755,7 @@ def run_multi(args):
     # one-GPU box; the ranks time-slice one GPU, so its numbers are not
     # performance).  NCCL refuses duplicate GPUs: gloo, no NCCL baselines.
     shared = os.environ.get("SCCL_BENCH_SHARE_GPU") == "1"
+    mps = shared and bool(os.environ.get("CUDA_MPS_PIPE_DIRECTORY"))  # ranks concurrent under MPS, not time-sliced
     dev_index = 0 if shared else local
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
@@ -778,7 +779,9 @@ def run_multi(args):
     # every candidate.  --nchannels N pins it.
     tune = {}
     nch_use = args.nchannels
-    if args.nchannels == 0:
+    # (not in shared-GPU mode: there every rank's CTAs share one GPU's slots,
+    # and a 64-CTA candidate x P ranks need not be co-resident under MPS)
+    if args.nchannels == 0 and not shared:
         nch_use, tune = tune_nchannels(dist, sccl, js, rank, P, m, sccl.U8, dev_index, args, send, stream,
                                        "cpu" if shared else dev)
     plan = sccl.Plan(js, rank, P, m, sccl.U8, device=dev_index, nchannels=nch_use, tile_bytes=args.tile,
@@ -842,8 +845,11 @@ def run_multi(args):
             "metric": METRIC, "value": round(per_rank * P, 2), "unit": "GB/s", "n_gpus": 1 if shared else P,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (uniform random bytes)",
-            "config": {"workload": (f"{sched_label(name)}; {P} ranks as {P} processes time-sliced on ONE GPU "
-                                    "(multi-process path validation, not performance)") if shared
+            "config": {"workload": (f"{sched_label(name)}; {P} ranks as {P} processes "
+                                    + ("running concurrently on ONE GPU under MPS (the multi-process kernel path "
+                                       "timed with every rank in one HBM: no NVLink)" if mps else
+                                       "time-sliced on ONE GPU (multi-process path validation, not performance)"))
+                       if shared
                        else _workload_text(P, P, name, multi=True),
                        "ranks": P, "bytes_per_rank": m, "schedule_file": f"tests/golden/schedules/bench/{name}.json",
                        "parallelism": f"ranks{P}", "nchannels": plan.info()["nchannels"],
