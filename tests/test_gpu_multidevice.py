@@ -39,6 +39,9 @@ rank, W, MEM, SHARE = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[
 dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=W)
 dev = 0 if SHARE else rank
 torch.cuda.set_device(dev)
+# SCCL_MULTIDEVICE_NCH: CTAs per rank (0 = policy).  Under MPS the shared-GPU
+# ranks run concurrently and must be co-resident together (W x CTAs <= SM slots)
+NCH = int(os.environ.get("SCCL_MULTIDEVICE_NCH", "0"))
 ag1 = S.one_shot_allgather(W)
 scheds = [("ag111", S.to_json(ag1), [O.U8]),
           ("ag_ring", S.to_json(S.ring_allgather(W)), [O.U8]),
@@ -57,7 +60,7 @@ for name, js, dts in scheds:
             for proto in ("ll", "simple"):
                 if proto == "ll" and nb > (1 << 20):
                     continue
-                plan = sccl.Plan(js, rank, W, nb, dt, device=dev, protocol=proto, timeout_ms=120000,
+                plan = sccl.Plan(js, rank, W, nb, dt, device=dev, protocol=proto, timeout_ms=120000, nchannels=NCH,
                                  mem_handles=MEM)
                 plan.bind_with()
                 for it in range(3):  # back-to-back: entry handshake + epochs advance
@@ -102,7 +105,8 @@ for name, js, dts in scheds:
 for name, js, dts in scheds:
     d = json.loads(js)
     for proto, nb in (("ll", 4096), ("simple", 1 << 18)):
-        plan = sccl.Plan(js, rank, W, nb, dts[0], device=dev, protocol=proto, timeout_ms=120000, mem_handles=MEM)
+        plan = sccl.Plan(js, rank, W, nb, dts[0], device=dev, protocol=proto, timeout_ms=120000, mem_handles=MEM,
+                         nchannels=NCH)
         plan.bind_with()
         ins = [O.seeded_inputs(d["collective"], W, nb, dts[0], 500 + i) for i in range(12)]
         wants = [O.execute(d, x, nb, dts[0])[rank] for x in ins]
