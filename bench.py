@@ -1027,7 +1027,7 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
     def nvls():
         if not all(sup):
             return {"skipped": f"no multicast team (nvls_supported per rank: {sup})"}
-        nv = sccl.NvlsAllreduce(rank, P, M, sccl.BF16, device=dev_index)
+        nv = sccl.NvlsAllreduce(rank, P, M, sccl.BF16, device=dev_index, timeout_ms=BENCH_TIMEOUT_MS)
         try:
             nv.launch(x, y)
             torch.cuda.synchronize()

@@ -207,6 +207,8 @@ int sccl_nvls_bind(sccl_nvls* nvls);
 int sccl_nvls_buffer(sccl_nvls* nvls, void** ptr, size_t* bytes);
 int sccl_nvls_launch(sccl_nvls* nvls, const void* sendbuf, void* recvbuf, void* stream);
 int sccl_nvls_check(sccl_nvls* nvls);
+/* barrier watchdog of later launches: 0 = default (600 s), < 0 = disabled */
+int sccl_nvls_set_timeout(sccl_nvls* nvls, int64_t timeout_ms);
 int sccl_nvls_destroy(sccl_nvls* nvls);
 
 /* thread-local message of the last failing call */

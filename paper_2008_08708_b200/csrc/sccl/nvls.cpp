@@ -215,6 +215,13 @@ int sccl_nvls_check(sccl_nvls* n) {
   });
 }
 
+int sccl_nvls_set_timeout(sccl_nvls* n, int64_t timeout_ms) {
+  return guarded([&] {
+    if (!n) throw invalid_argument_error("NULL plan");
+    n->timeout_ns = timeout_ms < 0 ? 0 : (timeout_ms == 0 ? 600LL * 1000000000LL : timeout_ms * 1000000LL);
+  });
+}
+
 int sccl_nvls_destroy(sccl_nvls* n) {
   if (!n) return SCCL_OK;
   cudaSetDevice(n->device);

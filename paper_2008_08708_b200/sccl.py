@@ -87,6 +87,7 @@ def lib():
         L.sccl_nvls_buffer.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_sz)]
         L.sccl_nvls_launch.argtypes = [c_p, c_p, c_p, c_p]
         L.sccl_nvls_check.argtypes = [c_p]
+        L.sccl_nvls_set_timeout.argtypes = [c_p, ctypes.c_int64]
         L.sccl_nvls_destroy.argtypes = [c_p]
         L.sccl_launch.argtypes = [c_p, c_p, c_p, c_p]
         L.sccl_launch_loopback.argtypes = [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
@@ -640,8 +641,9 @@ class NvlsAllreduce:
     the NVSwitch (multimem.ld_reduce / multimem.st).  One rank per GPU;
     nranks = 1 needs no process group (a one-device multicast team)."""
 
-    def __init__(self, rank: int, nranks: int, nbytes: int, dtype: int = BF16, device: int = 0, group=None):
-        """Collective for nranks > 1, and it fails collectively: every step
+    def __init__(self, rank: int, nranks: int, nbytes: int, dtype: int = BF16, device: int = 0, group=None,
+                 timeout_ms: int = 0):
+        """timeout_ms: barrier watchdog (0 = 600 s, < 0 = off).  Collective for nranks > 1, and it fails collectively: every step
         (create, rank 0's export, join, bind) is agreed across the ranks
         (_collective_step), so a multicast team that cannot form raises on
         every rank instead of leaving peers in a barrier."""
@@ -650,6 +652,7 @@ class NvlsAllreduce:
         multi = nranks > 1
         step = (lambda fn, **kw: _collective_step(fn, group, **kw)) if multi else (lambda fn, **kw: fn())
         step(lambda: _raise(lib().sccl_nvls_create(rank, nranks, nbytes, dtype, device, ctypes.byref(self._h))))
+        _raise(lib().sccl_nvls_set_timeout(self._h, timeout_ms))
         fd = -1
         if multi:
             import torch.distributed as dist
