@@ -966,6 +966,8 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
     g_simple = group_with({"NCCL_PROTO": "Simple"})
     g_ring = group_with({"NCCL_ALGO": "Ring"})
     g_tree = group_with({"NCCL_ALGO": "Tree"})
+    g_ll = group_with({"NCCL_PROTO": "LL"})  # SURVEY.md 8(d) cfg 3: NCCL_PROTO=Simple/LL/LL128
+    g_ll128 = group_with({"NCCL_PROTO": "LL128"})
     bw = lambda coll, nbytes, t: round(busbytes(coll, P, nbytes) / (t * 1e-3) / 1e9, 2)
 
     def agree(ok):
@@ -1012,7 +1014,7 @@ def nccl_baselines(args, dist, sccl, rank, P, dev, dev_index, send, ref, ms_ours
             finally:
                 p2.close()
         for tag, grp in (("nccl_default", None), ("nccl_ring", g_ring), ("nccl_tree", g_tree),
-                         ("nccl_simple", g_simple)):
+                         ("nccl_simple", g_simple), ("nccl_ll", g_ll), ("nccl_ll128", g_ll128)):
             z = x.clone()
             t = timed(lambda: dist.all_reduce(z, group=grp), args.steps)
             ar[f"{tag}_ms"], ar[f"{tag}_busbw"] = round(t, 4), bw("allreduce", M, t)
