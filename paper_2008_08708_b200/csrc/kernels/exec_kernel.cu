@@ -1051,11 +1051,14 @@ __device__ __forceinline__ void st_ll(void* p, uint2 d, uint32_t f) {
 // stores nothing, cta_abort is set)
 template <bool SYS>
 __device__ uint2 ll_read(const char* slot, int64_t pair, bool two, uint32_t ef, const KParams& p, int rank, int ch,
-                         int op) {
+                         int op, bool& ok) {
   const char* a = slot + pair * 16;
   uint4 v = ld_ll(a);
   if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
-  if (cta_aborted()) return make_uint2(0, 0);
+  if (cta_aborted()) {
+    ok = false;
+    return make_uint2(0, 0);
+  }
   uint64_t t0 = 0;  // (abort word and clock first read after 1024 polls, as in wait_ge)
   uint32_t spins = 0;
   for (;;) {
@@ -1063,11 +1066,15 @@ __device__ uint2 ll_read(const char* slot, int64_t pair, bool two, uint32_t ef, 
     if (v.y == ef && (!two || v.w == ef)) return make_uint2(v.x, v.z);
     if (++spins > 32) __nanosleep(20);
     if ((spins & 1023) == 0) {
-      if (join_abort(p)) return make_uint2(0, 0);
+      if (join_abort(p)) {
+        ok = false;
+        return make_uint2(0, 0);
+      }
       const uint64_t now = globaltimer();
       if (!t0) t0 = now;
       else if (p.timeout_ns > 0 && (long long)(now - t0) > p.timeout_ns) {
         watchdog_fire(p, rank, ch, op, -3, ef, v.y);
+        ok = false;
         return make_uint2(0, 0);
       }
     }
@@ -1159,8 +1166,9 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
         const DPart q = dsplit16m(int64_t(in.len), p.kb, p.kb_magic, cb);
         const char* slot = p.base[in.rank][in.space] + sc(in.space) + in.off + 2 * q.off;
         const int64_t npair = (q.len + 7) / 8;
+        bool ok = true;  // (a consumed receipt: nothing to publish either way)
         for (int64_t k = tid; k < npair; k += LL_NT)
-          ll_read<SYS>(slot, k, q.len - 8 * k > 4, ef, p, rank, ch, int(oi - ob));
+          ll_read<SYS>(slot, k, q.len - 8 * k > 4, ef, p, rank, ch, int(oi - ob), ok);
       }
       continue;
     }
@@ -1189,17 +1197,22 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
     for (int64_t k = tid; k < npair; k += LL_NT) {
       const int n = int(min(int64_t(8), q.len - 8 * k));
       const bool two = n > 4;
-      uint2 v = s_inll[0] ? ll_read<SYS>(s_inp[0], k, two, ef, p, rank, ch, int(oi - ob))
+      bool ok = true;  // every input word of this element arrived (a read that gave up clears it)
+      uint2 v = s_inll[0] ? ll_read<SYS>(s_inp[0], k, two, ef, p, rank, ch, int(oi - ob), ok)
                           : ld_plain8(s_inp[0] + 8 * k, n, op.vec);
       if (op.kind == 1) {
         Acc8<DT> acc;
         acc.init(v);
         for (int i = 1; i < op.nin; ++i)
-          acc.add(s_inll[i] ? ll_read<SYS>(s_inp[i], k, two, ef, p, rank, ch, int(oi - ob))
+          acc.add(s_inll[i] ? ll_read<SYS>(s_inp[i], k, two, ef, p, rank, ch, int(oi - ob), ok)
                             : ld_plain8(s_inp[i] + 8 * k, n, op.vec));
         v = acc.out();
       }
-      if (cta_aborted()) continue;  // a read above gave up: publish nothing (see watchdog_fire)
+      // a read above gave up (watchdog / abort): publish nothing computed
+      // from it (see watchdog_fire); values whose inputs all arrived are
+      // correct and may still go out.  (A per-thread register, not the
+      // CTA's shared abort word: no shared load per element.)
+      if (!ok) continue;
       for (int o = 0; o < op.nout; ++o) {
         if (s_outll[o]) st_ll(s_outp[o] + 16 * k, v, ef);
         else st_plain8(s_outp[o] + 8 * k, v, n, op.vec);
