@@ -70,6 +70,9 @@ __device__ __forceinline__ DPart dsplit16m(int64_t L, int K, uint64_t magic, int
   const int64_t hi = (i == K - 1) ? L : int64_t(__umul64hi(uint64_t(i + 1) * Uu, magic) << 4);
   return {lo, hi - lo};
 }
+// x / d for the launch geometry (x, d < 2^16) with the host's magic
+// floor(2^32 / d) + 1; magic 0 means d == 1
+__device__ __forceinline__ int fastdiv(uint32_t x, uint32_t magic) { return int(magic ? __umulhi(x, magic) : x); }
 // tiles of T bytes covering n bytes: a shift for power-of-two tiles (copies,
 // and reductions of fan-in 2, 4, 8, ...), a divide otherwise
 __device__ __forceinline__ uint32_t ntiles_of(uint64_t n, uint32_t T) {
@@ -547,8 +550,8 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
   __shared__ uint32_t s_nwin;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int lr = blockIdx.x / p.nch, ch = blockIdx.x % p.nch;
-  const int cg = ch % p.kc, cb = ch / p.kc;  // chunk group, byte part
+  const int lr = fastdiv(blockIdx.x, p.nch_magic), ch = int(blockIdx.x) - lr * p.nch;
+  const int cb = fastdiv(uint32_t(ch), p.kc_magic), cg = ch - cb * p.kc;  // chunk group, byte part
   const int rank = p.rank0 + lr;
   uint64_t* const myflags = reinterpret_cast<uint64_t*>(p.base[rank][SP_FLAGS_IDX]);
 
@@ -1104,8 +1107,8 @@ __device__ __forceinline__ void st_plain8(char* a, uint2 v, int n, bool aligned)
 template <int DT, bool SYS>
 __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ KParams p) {
   const int tid = threadIdx.x;
-  const int lr = blockIdx.x / p.nch, ch = blockIdx.x % p.nch;
-  const int cg = ch % p.kc, cb = ch / p.kc;
+  const int lr = fastdiv(blockIdx.x, p.nch_magic), ch = int(blockIdx.x) - lr * p.nch;
+  const int cb = fastdiv(uint32_t(ch), p.kc_magic), cg = ch - cb * p.kc;  // (no divides in the prologue)
   const int rank = p.rank0 + lr;
   __shared__ uint64_t s_e;
   __shared__ uint64_t s_spar;  // scratch slot-set offset of this launch (epoch parity)

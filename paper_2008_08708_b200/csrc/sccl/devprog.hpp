@@ -69,6 +69,8 @@ struct KParams {
   int P, nch, rank0, nranks_launch;
   int kc, kb;            // nch = kc * kb: chunk groups x byte parts per chunk
   uint64_t kb_magic;     // ceil(2^64 / kb) (0 if kb == 1): byte-part split without a 64-bit divide
+  uint32_t nch_magic;    // ceil(2^32 / nch): blockIdx / nch = umulhi(blockIdx, nch_magic), exact below 2^16
+  uint32_t kc_magic;     // ceil(2^32 / kc): channel / kc likewise
   int tile;              // copy tile = pipeline stage bytes (<= kMaxTile); reduce tiles tile/nin
   int nstage;            // pipeline stages (<= kMaxStages, a multiple of kStorerWarps)
   int entry_base;        // index of the entry-handshake flags in FLAGS

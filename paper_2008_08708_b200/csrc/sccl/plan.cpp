@@ -769,6 +769,11 @@ void fill_common(const sccl_plan& p, KParams& k) {
   k.kc = p.kc;
   k.kb = p.kb;
   k.kb_magic = p.kb > 1 ? ~uint64_t(0) / uint64_t(p.kb) + 1 : 0;
+  // x / d == umulhi(x, floor(2^32 / d) + 1) exactly for x, d < 2^16 (the
+  // kernel's fastdiv; d == 1 is passed as 0 and handled there)
+  auto magic32 = [](int d) -> uint32_t { return d <= 1 ? 0u : uint32_t((uint64_t(1) << 32) / uint64_t(d) + 1); };
+  k.nch_magic = magic32(p.nch);
+  k.kc_magic = magic32(p.kc);
   k.tile = p.tile;
   k.nstage = p.nstage;
   k.ll = p.ll ? 1 : 0;
