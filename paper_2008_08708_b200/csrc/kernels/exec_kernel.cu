@@ -1221,8 +1221,13 @@ __global__ void __launch_bounds__(LL_NT) exec_ll_kernel(const __grid_constant__ 
         else st_plain8(s_outp[o] + 8 * k, v, n, op.vec);
       }
     }
-    __syncthreads();
-    if (tid == 0) trace_ev(p, &s_trace_n, TR_DONE, oi, 0);  // op's data moved
+    // (no barrier here: the next op's first barrier already keeps its
+    // descriptor writes behind every thread's data loop of this op; the
+    // debug trace wants the op's end, so it alone pays for one)
+    if (p.trace) {
+      __syncthreads();
+      if (tid == 0) trace_ev(p, &s_trace_n, TR_DONE, oi, 0);  // op's data moved
+    }
   }
   __syncthreads();
   if (tid == 0) {
