@@ -783,13 +783,32 @@ __global__ void __launch_bounds__(NT, 2) exec_kernel(const __grid_constant__ KPa
             if ((DT == 3 || DT == 4) && op.nin == 2) {  // bf16 / f16 pair: one packed add per 2 elements
               const uint4* b1 = reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(T));
               for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) b0[v] = add_pair<DT>(b0[v], b1[v]);
-            } else
-            for (uint32_t v = tid - CW0 * 32; v < nv; v += NCW * 32) {
-              Vec<DT> acc;
-              acc.init(b0[v]);
-              for (int k = 1; k < op.nin; ++k)
-                acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T)[v]);
-              b0[v] = acc.out();
+            } else {
+              // two vectors per thread in flight (same operands, same order;
+              // float types only: the integer kernels keep their registers)
+              const uint32_t step = NCW * 32;
+              uint32_t v = tid - CW0 * 32;
+              if constexpr (DT >= 2)
+              for (; v + step < nv; v += 2 * step) {
+                Vec<DT> acc0, acc1;
+                acc0.init(b0[v]);
+                acc1.init(b0[v + step]);
+                for (int k = 1; k < op.nin; ++k) {
+                  const uint4* bk = reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T);
+                  const uint4 x0 = bk[v], x1 = bk[v + step];
+                  acc0.add(x0);
+                  acc1.add(x1);
+                }
+                b0[v] = acc0.out();
+                b0[v + step] = acc1.out();
+              }
+              for (; v < nv; v += step) {
+                Vec<DT> acc;
+                acc.init(b0[v]);
+                for (int k = 1; k < op.nin; ++k)
+                  acc.add(reinterpret_cast<const uint4*>(bufs + size_t(s) * STAGE + size_t(k) * T)[v]);
+                b0[v] = acc.out();
+              }
             }
             if (p.discard) {  // dead scratch receipts of this tile: drop their L2 lines (no write-back)
               const uint32_t dn = S.dsn[s];

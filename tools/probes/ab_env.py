@@ -23,6 +23,8 @@ SCHED = {
     "ar56f": lambda: (S.allreduce_from(S.hamiltonian_allgather(P)), sccl.F32, 1),
     "ar_ring": lambda: (S.allreduce_from(S.ring_allgather(P)), sccl.BF16, 1),
     "ar822": lambda: (S.allreduce_from(S.one_shot_allgather(P)), sccl.BF16, 1),
+    "ar822f": lambda: (S.allreduce_from(S.one_shot_allgather(P)), sccl.F32, 1),
+    "ar_ringf": lambda: (S.allreduce_from(S.ring_allgather(P)), sccl.F32, 1),
     "ag777": lambda: (S.to_json(S.hamiltonian_allgather(P)), sccl.U8, P),
     "ag_ring": lambda: (S.to_json(S.ring_allgather(P)), sccl.U8, P),
     "ag111": lambda: (S.to_json(S.one_shot_allgather(P)), sccl.U8, P),
