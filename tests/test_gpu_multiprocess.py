@@ -193,3 +193,66 @@ def test_processes_one_gpu(tmp_path, world, mem):
     if os.environ.get("SCCL_TEST_VERBOSE"):
         print(text)
     assert text.count("OK") == (5 if world == 2 else 7) * world + 4 * world, text
+
+
+FRONTIER_WORKER = r"""
+import json, os, sys
+sys.path[:0] = [{root!r}, {oracle!r}]
+import numpy as np, torch, torch.distributed as dist
+import oracle as O
+from paper_2008_08708_b200 import sccl, schedules as S
+rank, W = int(sys.argv[1]), int(sys.argv[2])
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=W)
+torch.cuda.set_device(0)
+fdir = os.path.join({root!r}, "paper_2008_08708_b200", "frontiers")
+idx = json.load(open(os.path.join(fdir, "index.json")))
+n = 0
+for e in idx:
+    if e["P"] != W:
+        continue
+    ag = open(os.path.join(fdir, e["file"])).read()
+    for js, nb, dt in ((ag, 8192 + 48, O.U8), (S.allreduce_from(json.loads(ag)), 4096 * W, O.BF16)):
+        d = json.loads(js)
+        for proto in ("ll", "simple"):
+            plan = sccl.Plan(js, rank, W, nb, dt, device=0, protocol=proto, timeout_ms=120000)
+            plan.bind_with()
+            ins = O.seeded_inputs(d["collective"], W, nb, dt, 81)
+            want = O.execute(d, ins, nb, dt)[rank]
+            recv = torch.full((want.size,), 0xEE, dtype=torch.uint8, device="cuda")
+            plan.launch(torch.from_numpy(ins[rank]).cuda(), recv)
+            torch.cuda.synchronize()
+            plan.check()
+            assert np.array_equal(recv.cpu().numpy(), want), (e["file"], d["collective"], proto, rank)
+            dist.barrier()
+            plan.close()
+            n += 1
+print("OK", rank, n, flush=True)
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_frontier_schedules_one_rank_per_process(tmp_path, world):
+    """Every committed Pareto-frontier schedule of this P (ring / full /
+    switch, frontiers/index.json) and the allreduce composed from it, on the
+    one-rank-per-process path (IPC peers, sys-scope counters, handshake or
+    parity slots), both protocols, bit-exact against the oracle on every
+    rank; the processes share cuda:0."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = tmp_path / "f.py"
+    script.write_text(FRONTIER_WORKER.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"), port=port))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    procs = [subprocess.Popen([sys.executable, str(script), str(r), str(world)], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True, env=env) for r in range(world)]
+    try:
+        outs = [p.communicate(timeout=900) for p in procs]
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, (o, e[-3000:])
+    counts = [int(line.split()[2]) for o, _ in outs for line in o.splitlines() if line.startswith("OK")]
+    assert len(counts) == world and min(counts) >= 4, counts
