@@ -206,12 +206,24 @@ dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank,
 torch.cuda.set_device(0)
 fdir = os.path.join({root!r}, "paper_2008_08708_b200", "frontiers")
 idx = json.load(open(os.path.join(fdir, "index.json")))
-n = 0
+import glob
+gdir = os.path.join({root!r}, "tests", "golden", "schedules")
+cases = []
 for e in idx:
-    if e["P"] != W:
-        continue
-    ag = open(os.path.join(fdir, e["file"])).read()
-    for js, nb, dt in ((ag, 8192 + 48, O.U8), (S.allreduce_from(json.loads(ag)), 4096 * W, O.BF16)):
+    if e["P"] == W:
+        ag = open(os.path.join(fdir, e["file"])).read()
+        cases.append((e["file"], ag, 8192 + 48, O.U8))
+        cases.append((e["file"] + "+AR", S.allreduce_from(json.loads(ag)), 4096 * W, O.BF16))
+for path in sorted(glob.glob(os.path.join(gdir, "*.json"))):  # synthesized schedules (DGX-1, AMD, ring(8) ...)
+    js = open(path).read()
+    d = json.loads(js)
+    if d["P"] == W:
+        kind = d["collective"]
+        cases.append((os.path.basename(path), js, 8192 * W if kind == "alltoall" else 8192 + 48 * (kind != "allreduce"),
+                      O.BF16 if kind == "allreduce" else O.U8))
+n = 0
+for name, js0, nb0, dt0 in cases:
+    for js, nb, dt in ((js0, nb0, dt0),):
         d = json.loads(js)
         for proto in ("ll", "simple"):
             plan = sccl.Plan(js, rank, W, nb, dt, device=0, protocol=proto, timeout_ms=120000)
@@ -222,7 +234,7 @@ for e in idx:
             plan.launch(torch.from_numpy(ins[rank]).cuda(), recv)
             torch.cuda.synchronize()
             plan.check()
-            assert np.array_equal(recv.cpu().numpy(), want), (e["file"], d["collective"], proto, rank)
+            assert np.array_equal(recv.cpu().numpy(), want), (name, d["collective"], proto, rank)
             dist.barrier()
             plan.close()
             n += 1
@@ -234,7 +246,10 @@ dist.destroy_process_group()
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_frontier_schedules_one_rank_per_process(tmp_path, world):
     """Every committed Pareto-frontier schedule of this P (ring / full /
-    switch, frontiers/index.json) and the allreduce composed from it, on the
+    switch, frontiers/index.json) and the allreduce composed from it, plus
+    the synthesized golden schedules of this P (DGX-1 (1,2,2) / (2,2,3) /
+    (6,3,7) and their allreduces, the DGX-1 multi-hop alltoall, AMD Z52 and
+    ring(8) (2,4,7)), on the
     one-rank-per-process path (IPC peers, sys-scope counters, handshake or
     parity slots), both protocols, bit-exact against the oracle on every
     rank; the processes share cuda:0."""
@@ -254,5 +269,10 @@ def test_frontier_schedules_one_rank_per_process(tmp_path, world):
                 p.kill()
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, (o, e[-3000:])
+    import json as _json
+    idx = _json.load(open(os.path.join(ROOT, "paper_2008_08708_b200", "frontiers", "index.json")))
+    golden = sum(_json.load(open(p))["P"] == world
+                 for p in __import__("glob").glob(os.path.join(ROOT, "tests", "golden", "schedules", "*.json")))
+    want = 2 * (2 * sum(e["P"] == world for e in idx) + golden)  # (AG + AR per frontier entry, + goldens) x 2 protocols
     counts = [int(line.split()[2]) for o, _ in outs for line in o.splitlines() if line.startswith("OK")]
-    assert len(counts) == world and min(counts) >= 4, counts
+    assert counts == [want] * world, (counts, want)
