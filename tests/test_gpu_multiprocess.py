@@ -276,3 +276,24 @@ def test_frontier_schedules_one_rank_per_process(tmp_path, world):
     want = 2 * (2 * sum(e["P"] == world for e in idx) + golden)  # (AG + AR per frontier entry, + goldens) x 2 protocols
     counts = [int(line.split()[2]) for o, _ in outs for line in o.splitlines() if line.startswith("OK")]
     assert counts == [want] * world, (counts, want)
+
+
+@pytest.mark.timeout(900)
+def test_multiprocess_fuzz_four_ranks():
+    """tools/fuzz_multiproc.py: 40 random valid schedules (allgather /
+    reduce-scatter / allreduce, random dtype, size, protocol, CTA grid, LL
+    parity on/off, counter-release mode) on the one-rank-per-process path
+    with 4 processes on cuda:0, each case launched twice back to back;
+    every rank bit-exact against the oracle."""
+    import json as _json
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "4",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "tools", "fuzz_multiproc.py"), "40", "29"],
+                       capture_output=True, text=True, timeout=850, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    summary = [_json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(summary) == 1 and summary[0]["cases"] == 40, r.stdout[-2000:]
+    assert summary[0]["failures"] == 0, summary[0]["failed"]
