@@ -197,6 +197,21 @@ def hbm_bytes_per_launch(plan) -> int:
                if op["kind"] != "wait")
 
 
+def host_cpu() -> str:
+    """CPU model and logical CPU count of the host the CPU baselines ran on
+    (SURVEY.md 8(d) cfg 1: record the GPU box's CPU)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return f"{model}, {os.cpu_count()} logical CPUs"
+
+
 def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
@@ -243,7 +258,7 @@ def run_reference(args):
                        "parallelism": f"{threads} host threads"},
             "aggregate_GBps": round(per_rank * P, 3),
             "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                             "sample": sample},
+                             "sample": sample, "host_cpu": host_cpu()},
             "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -578,6 +593,7 @@ def loopback_extras(args, sccl, plan, send, recv, stream, peaks):
         c1[f"{nm} ({d['C']},{d['S']},{d['R']})"] = row
     c1["host_memcpy_GBps"] = round(memcpy_gbs, 1)
     c1["host_threads"] = threads
+    c1["host_cpu"] = host_cpu()
     out["config1_cpu_vs_gpu_1MiB"] = c1
 
     # the same lowered program as per-op cudaMemcpyAsync copies (the paper's
