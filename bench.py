@@ -401,7 +401,8 @@ def run_loopback(args):
                      "frac_schedule_bytes": round(sched_bytes / (kern_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)},
         "cpu_baseline": {"value": round(cpu_val / P, 3), "unit": "GB/s", "cores": 1, "kind": "port",
                          "sample": f"oracle executor, same schedule file, {P} ranks x {cpu_m} B, {cpu_n} runs in "
-                                   f"{cpu_s:.1f} s, 1 thread (SPEC.md:447); per-rank bus GB/s"},
+                                   f"{cpu_s:.1f} s, 1 thread (SPEC.md:447); per-rank bus GB/s",
+                         "host_cpu": host_cpu()},
         "e2e": e2e,
         "clocks": clk.summary(),
         "gpu_launches": launches,
