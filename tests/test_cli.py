@@ -47,3 +47,25 @@ def test_exec_digest_matches_oracle(name, dtype):
     ins = [O.cli_payload(sb, 7, r) for r in range(d["P"])]
     ref = O.execute(d, ins, nbytes, O.DTYPE_NAMES[dtype])
     assert res["digests"] == [O.fnv1a(r) for r in ref]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,dtype,protocol", [("ag_ring8_2_4_7", "u8", "auto"), ("ar_from_dgx1_2_2_3", "i32", "simple"),
+                                                 ("a2a_dgx1_8_2_3", "u8", "ll"), ("ar_from_ring8_2_4_7", "bf16", "ll")])
+def test_exec_mp_digest_matches_oracle(name, dtype, protocol):
+    """`sccl-exec exec-mp`: the C++-host use of the multi-process boundary --
+    one forked process per rank, plan create / export / file-based handle
+    exchange / bind / two launches through the C-ABI only -- gives the
+    oracle's digests on every rank (all ranks on cuda:0 here, time-sliced)."""
+    path = os.path.join(SCHED, name + ".json")
+    nbytes = 8 * 4096
+    out = subprocess.run([CLI, "exec-mp", path, "--bytes", str(nbytes), "--seed", "9", "--dtype", dtype,
+                          "--protocol", protocol], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout)
+    d = json.load(open(path))
+    assert res["processes"] == d["P"]
+    sb, _ = O.buffer_sizes(d["collective"], d["P"], nbytes)
+    ins = [O.cli_payload(sb, 9, r) for r in range(d["P"])]
+    ref = O.execute(d, ins, nbytes, O.DTYPE_NAMES[dtype])
+    assert res["digests"] == [O.fnv1a(r) for r in ref]
