@@ -233,8 +233,13 @@ void choose_stages(sccl_plan& p, const ProgramStats& st, int64_t maxlen, const C
     // (8,2,2) bf16 at 4 / 16 / 32 / 48 MiB per rank 19.7 / 54.0 / 101.5 /
     // 148.5 -> 15.3 / 53.3 / 95.9 / 138.2 us; 8 and 12 MiB keep 64 KiB
     // (27.0 vs 31.6, 41.0 vs 42.4 us) (tools/gpu_runs/r02/s2_ar822_tile.sh)
-    if (wide && p.pg.pull && st.reduces && !st.rereads && (maxlen <= (512 << 10) || st.bytes >= 250e6))
-      tile = 16384;
+    // Re-measured with the session-3 kernels (cheaper per-tile path, two
+    // vectors in flight in the wide reduce loop): up to 512 KiB chunks 32
+    // KiB tiles now beat 16 KiB, AR (8,2,2) bf16 at 512 KiB / 1 / 4 MiB per
+    // rank 9.16 / 10.24 / 14.41 -> 8.39 / 9.28 / 13.89 us, 2 MiB even
+    // (profiles/r02/s3_ar822_mid.jsonl); the streaming range keeps 16 KiB.
+    if (wide && p.pg.pull && st.reduces && !st.rereads && maxlen <= (512 << 10)) tile = 32768;
+    else if (wide && p.pg.pull && st.reduces && !st.rereads && st.bytes >= 250e6) tile = 16384;
     // one-shot copies (one fan-out op per rank, nothing re-read) up to
     // 512 KiB: two 16 KiB tiles per CTA overlap the load of one with the
     // stores of the other (AG (1,1,1) 256 / 512 KiB: -27 / -16 %)

@@ -63,11 +63,12 @@ def test_no_chunk_group_split_for_big_copy_relays():
     assert info("ar56", 128 << 20, protocol="simple")["chunk_groups"] == 1
 
 
-@pytest.mark.parametrize("mb,tile", [(1, 16384), (4, 16384), (8, 65536), (12, 65536), (16, 16384), (48, 16384),
+@pytest.mark.parametrize("mb,tile", [(1, 32768), (4, 32768), (8, 65536), (12, 65536), (16, 16384), (48, 16384),
                                      (64, 32768), (128, 32768)])
 def test_pulled_one_shot_allreduce_tiles(mb, tile):
-    # round 2: 16 KiB tiles up to 512 KiB chunks and from 250 MB of program
-    # traffic to the streaming threshold (profiles/r02/s2_ar822_tile.jsonl)
+    # round 2: 32 KiB tiles up to 512 KiB chunks (session 3,
+    # profiles/r02/s3_ar822_mid.jsonl; 16 KiB before) and 16 KiB from 250 MB
+    # of program traffic to the streaming threshold (profiles/r02/s2_ar822_tile.jsonl)
     assert info("ar822", mb << 20, protocol="simple")["tile_bytes"] == tile
     if mb == 4:  # push-lowered (multi-process style) keeps the round-1 rule
         assert info("ar822", mb << 20, protocol="simple", pull="off")["tile_bytes"] == 65536
